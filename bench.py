@@ -1,0 +1,348 @@
+"""Benchmark of the SEM hot path on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload tgv|poisson] [--impl ours|reference]
+
+Workloads (BASELINE.json configs):
+  poisson  config 2: Jacobi-PCG on the 32^3-element lx=8 box, Dirichlet walls;
+           one step = one PCG solve (42 iterations, tol 1e-8, identical to the
+           reference's count); metric value = P * iterations / t (GDOF/s of
+           operator work).
+  tgv      configs 1/3: BDF3/EXT3 Taylor-Green step (see bench_tgv in this file).
+
+Timing: W untimed warm-up steps, then K steps bracketed by barrier +
+synchronize, timed with CUDA events on the launching stream, max over ranks.
+Inputs are larger than L2 (126 MB): at 32^3 one field is 134 MB and the
+geometric factors 805 MB, so every step streams from HBM.
+"""
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return PEAKS_FALLBACK, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- helpers
+
+def dist_setup():
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier_max(value, world):
+    """max over ranks of a host float (timing rule: max over ranks)."""
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def poisson_space(ne, dev):
+    import torch
+
+    from paper_2207_07098_b200.basis import make_basis
+    from paper_2207_07098_b200.mesh import gen_box_mesh
+    from paper_2207_07098_b200.space import build_space
+
+    sp = build_space(gen_box_mesh((0.0, 1.0, 0.0, 1.0, 0.0, 1.0), (ne, ne, ne)), make_basis(7), device=dev)
+    mask = torch.ones(sp.shape, dtype=torch.float64, device=dev)
+    mask.view(-1)[sp.facet_flat.reshape(-1)] = 0.0
+    x, y, z = sp.coords
+    f = 3.0 * math.pi ** 2 * torch.sin(math.pi * x) * torch.sin(math.pi * y) * torch.sin(math.pi * z)
+    return sp, mask, f
+
+
+def ax_dssum_bytes(sp, masked, helmholtz=False):
+    """Algorithmic bytes of one Ax+dssum application."""
+    P = sp.n_points
+    gs = sp.gs
+    b = P * (8 + 48 + 8) + (P * 8 if helmholtz else 0)
+    b += gs.shared_local_points * (8 + 8 + 4) + gs.n_shared * 4
+    return b
+
+
+def time_kernels(sp, op, u, reps=20):
+    """Average CUDA-event durations of the Ax kernel and the dssum kernel on the
+    launching stream (inputs > L2 at >= 32^3)."""
+    import torch
+
+    from paper_2207_07098_b200 import _lib
+    from paper_2207_07098_b200.operators import _ex
+
+    st = torch.cuda.current_stream()
+    stp = st.cuda_stream
+    w = torch.empty_like(u)
+    gs = sp.gs
+    E = sp.n_elements
+
+    def ax():
+        if op.masked:
+            _lib.call("sf_ax_masked_f64", sp.dmat.ctypes.data, sp.n, _lib.ptr(sp.geom), _lib.ptr(sp.bm),
+                      _lib.ptr(u), _lib.ptr(w), E, op.lam_visc, op.lam_mass, _lib.ptr(op.inmask),
+                      _lib.ptr(op.outsel), _ex(), stp)
+        else:
+            _lib.call("sf_ax_helm_f64", sp.dmat.ctypes.data, sp.n, _lib.ptr(sp.geom), _lib.ptr(sp.bm),
+                      _lib.ptr(u), _lib.ptr(w), E, op.lam_visc, op.lam_mass, _ex(), stp)
+
+    def dss():
+        if op.masked:
+            _lib.call("sf_dssum_f64", _lib.ptr(w), _lib.ptr(gs.sh_off), _lib.ptr(op.sh_perm), gs.n_shared, 2,
+                      _lib.ptr(u), stp)
+        else:
+            _lib.call("sf_dssum_f64", _lib.ptr(w), _lib.ptr(gs.sh_off), _lib.ptr(gs.sh_perm), gs.n_shared, 0,
+                      None, stp)
+
+    res = {}
+    for name, fn in (("ax", ax), ("dssum", dss)):
+        for _ in range(3):
+            fn()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        torch.cuda.synchronize()
+        for a, b in evs:
+            a.record(st)
+            fn()
+            b.record(st)
+        torch.cuda.synchronize()
+        res[name] = float(np.mean([a.elapsed_time(b) for a, b in evs])) * 1e-3
+    return res
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+
+def cpu_poisson_sample():
+    """Oracle (CPU port of the reference) Jacobi-PCG on the 8^3 lx=8 Poisson box."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import semflow_oracle as O
+
+    sp = O.build_space(O.gen_box_mesh((0.0, 1.0, 0.0, 1.0, 0.0, 1.0), (8, 8, 8)), O.make_basis(7))
+    mask = np.ones(sp.shape)
+    mask.reshape(-1)[sp.facet_flat.ravel()] = 0.0
+    x, y, z = sp.coords
+    f = 3.0 * np.pi ** 2 * np.sin(np.pi * x) * np.sin(np.pi * y) * np.sin(np.pi * z)
+    rhs = mask * sp.gs.add(sp.bm * f)
+    A = O.make_global_op(sp, 1.0, 0.0, mask)
+    M = O.block_jacobi(sp, 1.0, 0.0, mask)[0]
+    O.pcg(A, rhs, 1e-8, 500, M, sp.gs.dot)       # warm
+    t0 = time.perf_counter()
+    reps = 0
+    its = 0
+    while True:
+        info = O.pcg(A, rhs, 1e-8, 500, M, sp.gs.dot)
+        reps += 1
+        its += info.iterations
+        if time.perf_counter() - t0 > 10.0:
+            break
+    dt = time.perf_counter() - t0
+    P = int(np.prod(sp.shape))
+    return {"value": P * its / dt / 1e9, "unit": "GDOF/s", "cores": O.num_threads(), "kind": "port",
+            "sample": f"oracle Jacobi-PCG, 8^3 lx=8 Poisson box ({P} points), {reps} solves x "
+                      f"{its // reps} iterations in {dt:.1f} s"}
+
+
+# ----------------------------------------------------------------------------- workloads
+
+def bench_poisson(args, world, rank, dev):
+    import torch
+
+    from paper_2207_07098_b200 import _lib, krylov, operators as ops
+    from paper_2207_07098_b200.precond import BlockJacobi
+
+    ne = args.ne or 32
+    sp, mask, f = poisson_space(ne, dev)
+    A = ops.make_global_op(sp, 1.0, 0.0, mask)
+    M = BlockJacobi(sp, 1.0, 0.0, mask)
+    rhs = mask * sp.gs.add(sp.bm * f)
+    P = sp.n_points
+    solve = lambda b: krylov.pcg(A, b, tol=1e-8, max_iter=500, precond=M, dot=sp.gs.dot)
+    for _ in range(args.warmup):
+        info = solve(rhs)
+    st = torch.cuda.current_stream()
+    clk = ClockSampler(torch.cuda.current_device())
+    clk.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    l0 = _lib.LAUNCHES
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    its = 0
+    for _ in range(args.steps):
+        info = solve(rhs)
+        its += info.iterations
+    e1.record(st)
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = _lib.LAUNCHES - l0
+    clk.stop()
+    t = barrier_max(e0.elapsed_time(e1) * 1e-3, world)
+    value = world * P * its / t / 1e9
+    # end to end through the public API with host buffers: H2D of the rhs, solve, D2H of x
+    rhs_h = rhs.cpu().pin_memory()
+    x_h = torch.empty_like(rhs_h).pin_memory()
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e_its = 0
+    for _ in range(args.steps):
+        b = rhs_h.to(dev, non_blocking=True)
+        info = solve(b)
+        x_h.copy_(info.x, non_blocking=True)
+        torch.cuda.synchronize()
+        e_its += info.iterations
+    te = barrier_max(time.perf_counter() - t0, world)
+    e2e = {"value": world * P * e_its / te / 1e9, "unit": "GDOF/s",
+           "h2d_bytes_per_step": rhs_h.numel() * 8, "d2h_bytes_per_step": x_h.numel() * 8}
+    kt = time_kernels(sp, A, torch.randn(sp.shape, dtype=torch.float64, device=dev))
+    pk, src = peaks()
+    nbytes = ax_dssum_bytes(sp, True)
+    achieved = nbytes / (kt["ax"] + kt["dssum"]) / 1e9
+    line = {
+        "metric": "GDOF/s per PCG iteration (config 2: Poisson Ax+dssum+Jacobi-CG, 32^3 lx=8)",
+        "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"poisson {ne}^3 lx=8 Dirichlet box, Jacobi-PCG tol 1e-8 (config 2)",
+                   "points": P, "iterations_per_step": its // args.steps, "l2": "inputs larger than L2",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": None, "kernel": "ax_helm(masked)+dssum",
+                     "algorithmic_bytes": nbytes, "ax_us": kt["ax"] * 1e6, "dssum_us": kt["dssum"] * 1e6,
+                     "peak_source": src},
+        "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+    }
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--workload", default="poisson", choices=("poisson",))
+    ap.add_argument("--ne", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        base = cpu_poisson_sample()
+        line = {"impl": "reference", "metric": "GDOF/s per PCG iteration (config 2: Poisson Ax+dssum+Jacobi-CG, 32^3 lx=8)",
+                "value": base["value"], "unit": "GDOF/s", "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "poisson (bounded CPU sample, see cpu_baseline.sample)"},
+                "cpu_baseline": base, "e2e": {"value": base["value"], "unit": "GDOF/s",
+                                              "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    import torch
+
+    world, rank, local = dist_setup()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    line = bench_poisson(args, world, rank, dev)
+    if rank == 0:
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_poisson_sample()
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

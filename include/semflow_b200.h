@@ -1,0 +1,186 @@
+/*
+ * semflow_b200.h -- C ABI of libsemflow_b200.so, the B200 (sm_100a) drop-in for
+ * the matrix-free spectral-element hot path of the `semflow` reference
+ * (arXiv 2207.07098 restated in Python, /root/reference/pkg/src/semflow).
+ *
+ * Conventions
+ *   - All arrays are DEVICE pointers unless the parameter name ends in `_host`.
+ *   - Fields are float64, C order: scalar (E, n, n, n) with axes (element, r, s, t),
+ *     vector (3, E, n, n, n); geometric factors g (6, E, n, n, n) packed
+ *     rr, rs, rt, ss, st, tt; rx (3, 3, E, n, n, n) with rx[s][l] = dr_s/dx_l.
+ *     (space.py:1-6, 102-122)
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Every entry point returns 0 on success and a nonzero SF_ERR_* code on
+ *     failure; sf_last_error() returns the (thread-local) message.
+ *   - `exact` != 0 selects non-contracted arithmetic (no FMA) in the same loop
+ *     order as the reference numba lane, giving bit-identical results for the
+ *     element kernels; exact == 0 is the production (DFMA) path.
+ *   - Reductions use a caller-owned workspace: `partials` holds
+ *     sf_red_workspace_doubles() doubles and `counter` one zero-initialised
+ *     unsigned (it is reset by the kernel).  Reductions are deterministic: the
+ *     summation order depends only on the problem size.
+ *   - n (points per direction, order + 1) must be in 2..10.
+ *
+ * The python binding that loads this library is
+ * paper_2207_07098_b200/_lib.py; INTEGRATION.md shows how the reference's own
+ * kernel lane (semflow/kernels/__init__.py) binds it.
+ */
+#ifndef SEMFLOW_B200_H
+#define SEMFLOW_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SF_OK 0
+#define SF_ERR_ARG 1
+#define SF_ERR_CUDA 2
+#define SF_ERR_UNSUPPORTED 3
+
+const char* sf_version(void);
+const char* sf_last_error(void);
+/* doubles needed for the `partials` reduction workspace */
+int sf_red_workspace_doubles(void);
+
+/* ---------------------------------------------------------------------------
+ * Kernel lane -- the reference's plugin API, semflow/kernels/__init__.py:47-53
+ * ------------------------------------------------------------------------- */
+
+/* apply_r / apply_s / apply_t (axis 0 / 1 / 2): out = a (m x n) contracted along
+ * one reference axis of u (E, n, n, n); out has that axis of extent m.
+ * Replaces kernels/_numba.py:15-60 (apply_r :15, apply_s :31, apply_t :47). */
+int sf_apply_axis_f64(int axis, const double* a, int m, int n, const double* u, double* out,
+                      long long E, int exact, void* stream);
+
+/* grad_ref: (ur, us, ut) = reference derivatives of u.  d_host is the n x n GLL
+ * differentiation matrix in host memory.  Replaces kernels/_numba.py:63-83. */
+int sf_grad_ref_f64(const double* d_host, int n, const double* u, double* ur, double* us,
+                    double* ut, long long E, int exact, void* stream);
+
+/* ax_helmholtz_local: w = lam_visc * D^T G D u + lam_mass * B u per element
+ * (lam_mass == 0 skips the mass term).  Replaces kernels/_numba.py:86-131. */
+int sf_ax_helm_f64(const double* d_host, int n, const double* g, const double* b, const double* u,
+                   double* w, long long E, double lam_visc, double lam_mass, int exact,
+                   void* stream);
+
+/* gs_gather: sums[g] = sum of vals[perm[o]] for o in [offsets[g], offsets[g+1]),
+ * sequential in perm order.  Replaces kernels/_numba.py:134-143. */
+int sf_gs_gather_f64(const double* vals, const long long* perm, const long long* offsets,
+                     long long n_gid, double* sums, void* stream);
+
+/* gs_scatter: out[perm[o]] = sums[g] (in place).  Replaces kernels/_numba.py:146-153. */
+int sf_gs_scatter_f64(const double* sums, const long long* perm, const long long* offsets,
+                      long long n_gid, double* out, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Device operator API -- the performance boundary (device-resident fields)
+ * ------------------------------------------------------------------------- */
+
+/* Masked element operator, first half of make_global_op's closure
+ * (operators.py:51-54): um = inmask ? u : 0; w = lam_visc D^T G D um + lam_mass B um;
+ * the value stored is w where `outsel` is set and u where it is clear.
+ * inmask/outsel are packed per-element bitmasks: ceil(n^3/32) uint32 words per
+ * element, bit p of element e = local point p.  Callers set outsel = mask OR
+ * shared, then finish with sf_dssum_f64(mode=2). */
+int sf_ax_masked_f64(const double* d_host, int n, const double* g, const double* b,
+                     const double* u, double* w, long long E, double lam_visc, double lam_mass,
+                     const uint32_t* inmask, const uint32_t* outsel, int exact, void* stream);
+
+/* In-place dssum (QQ^T) over the shared part of the gather-scatter map:
+ * offsets (n_shared+1) / perm (int32 local indices) of the gids with
+ * multiplicity > 1, grouped by gid with ascending local index (space.py:303-305).
+ * mode 0: add (GatherScatter.add, space.py:38-49)
+ * mode 1: avg (GatherScatter.avg, space.py:51-60: sum * (1.0/count))
+ * mode 2: masked operator finalisation (operators.py:53-54): copies whose perm
+ *         entry is negative (bit 31 set) receive u[idx] instead of the sum.
+ * Each shared gid is summed by one thread in reference order: bit-identical to
+ * gs_gather + gs_scatter, atomics-free. */
+int sf_dssum_f64(double* v, const int* offsets, const int* perm, int n_shared, int mode,
+                 const double* u, void* stream);
+
+/* glsc3: out[k] = sum_p (a_k[p] / mult[p]) * b_k[p] for K = 1..4 pairs
+ * (GatherScatter.dot, space.py:72-76).  a, b are HOST arrays of K device
+ * pointers; mult is the uint8 multiplicity per local point (NULL = unweighted,
+ * FunctionSpace.integral, space.py:159-161).  out is a device array. */
+int sf_glsc3_f64(int K, const double* const* a, const double* const* b, const uint8_t* mult,
+                 long long P, double* partials, unsigned* counter, double* out, void* stream);
+
+/* PCG building blocks (krylov.py:36-75 with BlockJacobi, precond.py:43-59);
+ * invdiag == NULL means no preconditioner.  Scalars are device pointers.
+ *   cg_init:      p = M r;                           out[0] = <r, p>
+ *   cg_update:    alpha = *rz / *pap; x += alpha p; r -= alpha ap;
+ *                 out[0] = <r, r>, out[1] = <r, M r>
+ *   cg_direction: p = M r + (*rz_new / *rz) p                                   */
+int sf_cg_init_f64(const double* r, const double* invdiag, double* p, const uint8_t* mult,
+                   long long P, double* partials, unsigned* counter, double* out, void* stream);
+int sf_cg_update_f64(double* x, double* r, const double* p, const double* ap,
+                     const double* invdiag, const uint8_t* mult, const double* rz,
+                     const double* pap, long long P, double* partials, unsigned* counter,
+                     double* out, void* stream);
+int sf_cg_direction_f64(double* p, const double* r, const double* invdiag, const double* rz_new,
+                        const double* rz, long long P, void* stream);
+
+/* One modified Gram-Schmidt step (gmres krylov.py:109-123; ProjectionSpace.absorb
+ * krylov.py:229-231): if vprev, w -= (*hprev) vprev and, if w2, w2 -= (*hprev) v2prev;
+ * out[0] = <w, vnext> (if vnext), out[1] = <w, w> (if want_norm). */
+int sf_mgs_step_f64(double* w, const double* vprev, const double* hprev, const double* vnext,
+                    double* w2, const double* v2prev, const uint8_t* mult, int want_norm,
+                    long long P, double* partials, unsigned* counter, double* out, void* stream);
+
+/* x = x0 + sum_i coef[i] * M v[i] accumulated in i order; v is a DEVICE array
+ * of nv pointers, coef a device array (gmres update krylov.py:150-154 with
+ * zs[i] = M vs[i]; ProjectionSpace.prepare krylov.py:206-209 with M = I). */
+int sf_lincomb_f64(double* x, const double* x0, const double* const* v, const double* coef,
+                   const double* invdiag, int nv, long long P, void* stream);
+
+/* r = b - ax; out[0] = <r, r>  (krylov.py:155-157) */
+int sf_residual_f64(double* r, const double* b, const double* ax, const uint8_t* mult, long long P,
+                    double* partials, unsigned* counter, double* out, void* stream);
+
+/* y = x / *s (and y2 = x2 / *s if y2) -- krylov.py:98, 149, 235-236 */
+int sf_scale_div_f64(double* y, const double* x, double* y2, const double* x2, const double* s,
+                     long long P, void* stream);
+
+/* Strong-form operators (operators.py): op 0 grad (:59-66, in u -> out 3 comps),
+ * 1 div (:69-76, in v -> out), 2 curl (:79-88, in v -> out v), 3 advect_vec
+ * (:108-126, collocation; in v, c -> out = sign * (c . grad) v). */
+int sf_deriv_f64(int op, const double* d_host, int n, const double* in, const double* c,
+                 const double* rx, double* out, long long E, double sign, int exact,
+                 void* stream);
+
+/* weak_grad_dot / cdtp (operators.py:91-105): out = sum_s D_s^T (bm rx_s . w) */
+int sf_cdtp_f64(const double* d_host, int n, const double* w, const double* rx, const double* bm,
+                double* out, long long E, int exact, void* stream);
+
+/* cfl (operators.py:161-182) without the dt factor: *out_bits = max(*out_bits,
+ * bits of max_p sum_s |rx_s . v| / dxi_s).  Initialise *out_bits to 0. */
+int sf_cfl_f64(const double* v, const double* rx, const double* dxi_host, int n, long long E,
+               unsigned long long* out_bits, int exact, void* stream);
+
+/* BDF/EXT history sums (timestep.py:227-232) over P3 = 3*E*n^3 values:
+ * vhat = sum_q a_dt[q] vel[q] + beta[q] nl[q]; omega = sum_q beta[q] crl[q].
+ * vel/nl/crl are HOST arrays of `order` device pointers. */
+int sf_bdf_ext_f64(double* vhat, double* omega, const double* const* vel, const double* const* nl,
+                   const double* const* crl, const double* a_dt, const double* beta, int order,
+                   long long P3, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Function-space setup (space.py:182-245), bit-identical to build_space
+ * ------------------------------------------------------------------------- */
+
+/* coords (3, E, n^3) = sum_c corners[e, c, l] * wc[c, p] (space.py:182-192);
+ * corners (E, 8, 3), wc (8, n^3) trilinear corner weights, device arrays. */
+int sf_trilinear_coords_f64(const double* corners, const double* wc, int n, long long E,
+                            double* coords, void* stream);
+
+/* rx (9 planes), jac, bm, geom (6 planes) from coords (space.py:214-245). */
+int sf_metrics_f64(const double* d_host, const double* w_host, int n, const double* coords,
+                   long long E, double* rx, double* jac, double* bm, double* geom, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SEMFLOW_B200_H */

@@ -1,0 +1,114 @@
+"""ctypes binding of libsemflow_b200.so (the C ABI in include/semflow_b200.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (or ``python -m
+paper_2207_07098_b200.build``).  There is no fallback: if the shared object is
+missing or no CUDA device is visible, every device entry point raises.
+"""
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsemflow_b200.so")
+
+_lib = None
+
+_vp = ctypes.c_void_p
+_i = ctypes.c_int
+_ll = ctypes.c_longlong
+_d = ctypes.c_double
+
+# name -> argtypes (all return int status unless listed in _RESTYPES)
+_SIGS = {
+    "sf_version": [],
+    "sf_last_error": [],
+    "sf_red_workspace_doubles": [],
+    "sf_apply_axis_f64": [_i, _vp, _i, _i, _vp, _vp, _ll, _i, _vp],
+    "sf_grad_ref_f64": [_vp, _i, _vp, _vp, _vp, _vp, _ll, _i, _vp],
+    "sf_ax_helm_f64": [_vp, _i, _vp, _vp, _vp, _vp, _ll, _d, _d, _i, _vp],
+    "sf_gs_gather_f64": [_vp, _vp, _vp, _ll, _vp, _vp],
+    "sf_gs_scatter_f64": [_vp, _vp, _vp, _ll, _vp, _vp],
+    "sf_ax_masked_f64": [_vp, _i, _vp, _vp, _vp, _vp, _ll, _d, _d, _vp, _vp, _i, _vp],
+    "sf_dssum_f64": [_vp, _vp, _vp, _i, _i, _vp, _vp],
+    "sf_glsc3_f64": [_i, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp],
+    "sf_cg_init_f64": [_vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp],
+    "sf_cg_update_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp],
+    "sf_cg_direction_f64": [_vp, _vp, _vp, _vp, _vp, _ll, _vp],
+    "sf_mgs_step_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _ll, _vp, _vp, _vp, _vp],
+    "sf_lincomb_f64": [_vp, _vp, _vp, _vp, _vp, _i, _ll, _vp],
+    "sf_residual_f64": [_vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp],
+    "sf_scale_div_f64": [_vp, _vp, _vp, _vp, _vp, _ll, _vp],
+    "sf_deriv_f64": [_i, _vp, _i, _vp, _vp, _vp, _vp, _ll, _d, _i, _vp],
+    "sf_cdtp_f64": [_vp, _i, _vp, _vp, _vp, _vp, _ll, _i, _vp],
+    "sf_cfl_f64": [_vp, _vp, _vp, _i, _ll, _vp, _i, _vp],
+    "sf_bdf_ext_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _ll, _vp],
+    "sf_trilinear_coords_f64": [_vp, _vp, _i, _ll, _vp, _vp],
+    "sf_metrics_f64": [_vp, _vp, _i, _vp, _ll, _vp, _vp, _vp, _vp, _vp],
+}
+_RESTYPES = {"sf_version": ctypes.c_char_p, "sf_last_error": ctypes.c_char_p}
+
+EXPORTED = tuple(_SIGS)
+
+
+class LibraryError(RuntimeError):
+    """The CUDA extension is missing or a kernel call failed."""
+
+
+def load(path=LIB_PATH):
+    """Load (once) and return the ctypes handle; raises if the .so is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise LibraryError(
+            f"{path} not found: build it with `python -m paper_2207_07098_b200.build` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    for name, args in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _RESTYPES.get(name, ctypes.c_int)
+    _lib = lib
+    return lib
+
+
+#: number of library entry-point calls that launch kernels (bench.py's gpu_launches)
+LAUNCHES = 0
+
+
+def call(name, *args):
+    """Invoke an entry point and raise LibraryError on a nonzero status."""
+    global LAUNCHES
+    lib = _lib if _lib is not None else load()
+    LAUNCHES += 1
+    st = getattr(lib, name)(*args)
+    if st != 0:
+        msg = lib.sf_last_error().decode(errors="replace")
+        raise LibraryError(f"{name} failed (status {st}): {msg}")
+
+
+def ptr(t):
+    """Raw device (or host) address of a tensor, or NULL for None."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_ptr(device=None):
+    """cudaStream_t of torch's current stream on `device`."""
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def host_f64(a):
+    """Keep-alive contiguous float64 host buffer + its address (for *_host args)."""
+    import numpy as np
+
+    buf = np.ascontiguousarray(a, dtype=np.float64)
+    return buf, buf.ctypes.data
+
+
+def require_cuda(t):
+    if not (isinstance(t, torch.Tensor) and t.is_cuda):
+        raise LibraryError("semflow_b200 device kernels need CUDA tensors (no CPU fallback)")

@@ -1,0 +1,202 @@
+// C ABI of libsemflow_b200.so -- the drop-in boundary (see include/semflow_b200.h
+// for the reference interface each entry point replaces).  Plain pointers, sizes
+// and a cudaStream_t passed as void*; every function returns an int status
+// (0 = ok) and leaves a message for sf_last_error() on failure.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+#include "reduce.cuh"
+
+#include "../../include/semflow_b200.h"
+
+namespace sf {
+
+static thread_local char g_err[512] = {0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return SF_ERR_CUDA;
+  }
+  return SF_OK;
+}
+
+// implemented in ax.cu, gs.cu, vec.cu, ops.cu, geom.cu
+int ax_helm(const double*, int, const double*, const double*, const double*, double*, long long,
+            double, double, const uint32_t*, const uint32_t*, int, cudaStream_t);
+int grad_ref(const double*, int, const double*, double*, double*, double*, long long, int,
+             cudaStream_t);
+int apply_axis(int, const double*, int, int, const double*, double*, long long, int, cudaStream_t);
+int gs_gather(const double*, const long long*, const long long*, long long, double*, cudaStream_t);
+int gs_scatter(const double*, const long long*, const long long*, long long, double*, cudaStream_t);
+int dssum_shared(double*, const int*, const int*, int, int, const double*, cudaStream_t);
+int dot_multi(int, const double* const*, const double* const*, const uint8_t*, long long, RedWork,
+              double*, cudaStream_t);
+int cg_init(const double*, const double*, double*, const uint8_t*, long long, RedWork, double*,
+            cudaStream_t);
+int cg_update(double*, double*, const double*, const double*, const double*, const uint8_t*,
+              const double*, const double*, long long, RedWork, double*, cudaStream_t);
+int cg_direction(double*, const double*, const double*, const double*, const double*, long long,
+                 cudaStream_t);
+int mgs_step(double*, const double*, const double*, const double*, double*, const double*,
+             const uint8_t*, int, long long, RedWork, double*, cudaStream_t);
+int lincomb(double*, const double*, const double* const*, const double*, const double*, int,
+            long long, cudaStream_t);
+int residual(double*, const double*, const double*, const uint8_t*, long long, RedWork, double*,
+             cudaStream_t);
+int scale_div(double*, const double*, double*, const double*, const double*, long long,
+              cudaStream_t);
+int deriv(int, const double*, int, const double*, const double*, const double*, double*, long long,
+          double, int, cudaStream_t);
+int cdtp(const double*, int, const double*, const double*, const double*, double*, long long, int,
+         cudaStream_t);
+int cfl_max(const double*, const double*, const double*, int, long long, unsigned long long*, int,
+            cudaStream_t);
+int bdf_ext(double*, double*, const double* const*, const double* const*, const double* const*,
+            const double*, const double*, int, long long, cudaStream_t);
+int trilinear_coords(const double*, const double*, int, long long, double*, cudaStream_t);
+int metrics(const double*, const double*, int, const double*, long long, double*, double*, double*,
+            double*, cudaStream_t);
+
+}  // namespace sf
+
+using namespace sf;
+
+extern "C" {
+
+const char* sf_version(void) { return "semflow_b200 0.1.0 (sm_100a, fp64)"; }
+const char* sf_last_error(void) { return g_err; }
+
+int sf_red_workspace_doubles(void) { return K_MAX * RED_BLOCKS; }
+
+int sf_apply_axis_f64(int axis, const double* a, int m, int n, const double* u, double* out,
+                      long long E, int exact, void* stream) {
+  return apply_axis(axis, a, m, n, u, out, E, exact, as_stream(stream));
+}
+
+int sf_grad_ref_f64(const double* d_host, int n, const double* u, double* ur, double* us,
+                    double* ut, long long E, int exact, void* stream) {
+  return grad_ref(d_host, n, u, ur, us, ut, E, exact, as_stream(stream));
+}
+
+int sf_ax_helm_f64(const double* d_host, int n, const double* g, const double* b, const double* u,
+                   double* w, long long E, double lam_visc, double lam_mass, int exact,
+                   void* stream) {
+  return ax_helm(d_host, n, g, b, u, w, E, lam_visc, lam_mass, nullptr, nullptr, exact,
+                 as_stream(stream));
+}
+
+int sf_gs_gather_f64(const double* vals, const long long* perm, const long long* offsets,
+                     long long n_gid, double* sums, void* stream) {
+  return gs_gather(vals, perm, offsets, n_gid, sums, as_stream(stream));
+}
+
+int sf_gs_scatter_f64(const double* sums, const long long* perm, const long long* offsets,
+                      long long n_gid, double* out, void* stream) {
+  return gs_scatter(sums, perm, offsets, n_gid, out, as_stream(stream));
+}
+
+int sf_ax_masked_f64(const double* d_host, int n, const double* g, const double* b,
+                     const double* u, double* w, long long E, double lam_visc, double lam_mass,
+                     const uint32_t* inmask, const uint32_t* outsel, int exact, void* stream) {
+  if (!inmask || !outsel) {
+    set_error("sf_ax_masked_f64: inmask and outsel are required");
+    return SF_ERR_ARG;
+  }
+  return ax_helm(d_host, n, g, b, u, w, E, lam_visc, lam_mass, inmask, outsel, exact,
+                 as_stream(stream));
+}
+
+int sf_dssum_f64(double* v, const int* offsets, const int* perm, int n_shared, int mode,
+                 const double* u, void* stream) {
+  return dssum_shared(v, offsets, perm, n_shared, mode, u, as_stream(stream));
+}
+
+int sf_glsc3_f64(int K, const double* const* a, const double* const* b, const uint8_t* mult,
+                 long long P, double* partials, unsigned* counter, double* out, void* stream) {
+  return dot_multi(K, a, b, mult, P, RedWork{partials, counter}, out, as_stream(stream));
+}
+
+int sf_cg_init_f64(const double* r, const double* invdiag, double* p, const uint8_t* mult,
+                   long long P, double* partials, unsigned* counter, double* out, void* stream) {
+  return cg_init(r, invdiag, p, mult, P, RedWork{partials, counter}, out, as_stream(stream));
+}
+
+int sf_cg_update_f64(double* x, double* r, const double* p, const double* ap,
+                     const double* invdiag, const uint8_t* mult, const double* rz,
+                     const double* pap, long long P, double* partials, unsigned* counter,
+                     double* out, void* stream) {
+  return cg_update(x, r, p, ap, invdiag, mult, rz, pap, P, RedWork{partials, counter}, out,
+                   as_stream(stream));
+}
+
+int sf_cg_direction_f64(double* p, const double* r, const double* invdiag, const double* rz_new,
+                        const double* rz, long long P, void* stream) {
+  return cg_direction(p, r, invdiag, rz_new, rz, P, as_stream(stream));
+}
+
+int sf_mgs_step_f64(double* w, const double* vprev, const double* hprev, const double* vnext,
+                    double* w2, const double* v2prev, const uint8_t* mult, int want_norm,
+                    long long P, double* partials, unsigned* counter, double* out, void* stream) {
+  return mgs_step(w, vprev, hprev, vnext, w2, v2prev, mult, want_norm, P,
+                  RedWork{partials, counter}, out, as_stream(stream));
+}
+
+int sf_lincomb_f64(double* x, const double* x0, const double* const* v, const double* coef,
+                   const double* invdiag, int nv, long long P, void* stream) {
+  return lincomb(x, x0, v, coef, invdiag, nv, P, as_stream(stream));
+}
+
+int sf_residual_f64(double* r, const double* b, const double* ax, const uint8_t* mult, long long P,
+                    double* partials, unsigned* counter, double* out, void* stream) {
+  return residual(r, b, ax, mult, P, RedWork{partials, counter}, out, as_stream(stream));
+}
+
+int sf_scale_div_f64(double* y, const double* x, double* y2, const double* x2, const double* s,
+                     long long P, void* stream) {
+  return scale_div(y, x, y2, x2, s, P, as_stream(stream));
+}
+
+int sf_deriv_f64(int op, const double* d_host, int n, const double* in, const double* c,
+                 const double* rx, double* out, long long E, double sign, int exact,
+                 void* stream) {
+  return deriv(op, d_host, n, in, c, rx, out, E, sign, exact, as_stream(stream));
+}
+
+int sf_cdtp_f64(const double* d_host, int n, const double* w, const double* rx, const double* bm,
+                double* out, long long E, int exact, void* stream) {
+  return cdtp(d_host, n, w, rx, bm, out, E, exact, as_stream(stream));
+}
+
+int sf_cfl_f64(const double* v, const double* rx, const double* dxi_host, int n, long long E,
+               unsigned long long* out_bits, int exact, void* stream) {
+  return cfl_max(v, rx, dxi_host, n, E, out_bits, exact, as_stream(stream));
+}
+
+int sf_bdf_ext_f64(double* vhat, double* omega, const double* const* vel, const double* const* nl,
+                   const double* const* crl, const double* a_dt, const double* beta, int order,
+                   long long P3, void* stream) {
+  return bdf_ext(vhat, omega, vel, nl, crl, a_dt, beta, order, P3, as_stream(stream));
+}
+
+int sf_trilinear_coords_f64(const double* corners, const double* wc, int n, long long E,
+                            double* coords, void* stream) {
+  return trilinear_coords(corners, wc, n, E, coords, as_stream(stream));
+}
+
+int sf_metrics_f64(const double* d_host, const double* w_host, int n, const double* coords,
+                   long long E, double* rx, double* jac, double* bm, double* geom, void* stream) {
+  return metrics(d_host, w_host, n, coords, E, rx, jac, bm, geom, as_stream(stream));
+}
+
+}  // extern "C"

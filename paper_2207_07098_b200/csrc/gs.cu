@@ -1,0 +1,102 @@
+// Gather-scatter (direct stiffness summation, "dssum" / QQ^T) kernels (K2).
+//
+// Reference semantics:
+//   gs_gather   kernels/_numba.py:134-143  sums[g] = 0.0 + v[perm[o0]] + v[perm[o0+1]] ...
+//               (sequential, ascending local index within the gid segment)
+//   gs_scatter  kernels/_numba.py:146-153  out[perm[o]] = sums[g]
+//   GatherScatter.add / avg   space.py:38-60 (avg multiplies by 1.0/count)
+//   make_global_op            operators.py:51-54 (masked finalisation)
+//
+// The production dssum works on the *shared* part of the map only: gids with
+// multiplicity > 1 (S_g of them, S_l local copies).  Unshared points are
+// identity under QQ^T and are never touched.  One thread owns one shared gid and
+// sums its copies sequentially in the reference order, so the result is
+// bit-identical to the numba lane and independent of launch geometry; there are
+// no atomics.  perm entries are int32 local indices; in the masked-operator map a
+// negative entry (bit 31 set) marks a Dirichlet-masked copy, which receives the
+// operator input u instead of the sum (`mask*gs.add(w) + (1-mask)*u`).
+#include "common.cuh"
+
+namespace sf {
+
+__global__ void gs_gather_kernel(const double* __restrict__ vals, const long long* __restrict__ perm,
+                                 const long long* __restrict__ off, long long n_gid,
+                                 double* __restrict__ sums) {
+  long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_gid) return;
+  double acc = 0.0;
+  for (long long o = off[g]; o < off[g + 1]; ++o) acc = __dadd_rn(acc, vals[perm[o]]);
+  sums[g] = acc;
+}
+
+__global__ void gs_scatter_kernel(const double* __restrict__ sums, const long long* __restrict__ perm,
+                                  const long long* __restrict__ off, long long n_gid,
+                                  double* __restrict__ out) {
+  long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_gid) return;
+  const double v = sums[g];
+  for (long long o = off[g]; o < off[g + 1]; ++o) out[perm[o]] = v;
+}
+
+// MODE 0: add (QQ^T).  MODE 1: avg (sum * (1.0/count)).  MODE 2: masked-operator
+// finalisation (negative perm entry -> write u[idx]).  MODE 3: add, but write the
+// sum only to the copies (the caller guarantees the output already holds the
+// right values at unshared points) -- identical to MODE 0, kept for clarity.
+template <int MODE>
+__global__ void dssum_shared_kernel(double* __restrict__ v, const int* __restrict__ off,
+                                    const int* __restrict__ perm, int n_shared,
+                                    const double* __restrict__ u) {
+  int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_shared) return;
+  const int o0 = __ldg(off + g), o1 = __ldg(off + g + 1);
+  double acc = 0.0;
+  for (int o = o0; o < o1; ++o) {
+    int p = __ldg(perm + o) & 0x7fffffff;
+    acc = __dadd_rn(acc, v[p]);
+  }
+  if (MODE == 1) acc = __dmul_rn(acc, __drcp_rn((double)(o1 - o0)));
+  for (int o = o0; o < o1; ++o) {
+    int p = __ldg(perm + o);
+    if (MODE == 2 && p < 0) {
+      p &= 0x7fffffff;
+      v[p] = u[p];
+    } else {
+      v[p] = acc;
+    }
+  }
+}
+
+int gs_gather(const double* vals, const long long* perm, const long long* off, long long n_gid,
+              double* sums, cudaStream_t st) {
+  if (n_gid <= 0) return SF_OK;
+  int th = 256;
+  gs_gather_kernel<<<(unsigned)((n_gid + th - 1) / th), th, 0, st>>>(vals, perm, off, n_gid, sums);
+  return check_launch("gs_gather");
+}
+
+int gs_scatter(const double* sums, const long long* perm, const long long* off, long long n_gid,
+               double* out, cudaStream_t st) {
+  if (n_gid <= 0) return SF_OK;
+  int th = 256;
+  gs_scatter_kernel<<<(unsigned)((n_gid + th - 1) / th), th, 0, st>>>(sums, perm, off, n_gid, out);
+  return check_launch("gs_scatter");
+}
+
+int dssum_shared(double* v, const int* off, const int* perm, int n_shared, int mode,
+                 const double* u, cudaStream_t st) {
+  if (n_shared <= 0) return SF_OK;
+  int th = 256;
+  unsigned grid = (unsigned)((n_shared + th - 1) / th);
+  switch (mode) {
+    case 0: dssum_shared_kernel<0><<<grid, th, 0, st>>>(v, off, perm, n_shared, nullptr); break;
+    case 1: dssum_shared_kernel<1><<<grid, th, 0, st>>>(v, off, perm, n_shared, nullptr); break;
+    case 2:
+      if (u == nullptr) { set_error("dssum_shared: masked mode needs u"); return SF_ERR_ARG; }
+      dssum_shared_kernel<2><<<grid, th, 0, st>>>(v, off, perm, n_shared, u);
+      break;
+    default: set_error("dssum_shared: bad mode %d", mode); return SF_ERR_ARG;
+  }
+  return check_launch("dssum_shared");
+}
+
+}  // namespace sf

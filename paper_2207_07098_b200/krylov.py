@@ -1,0 +1,482 @@
+"""Krylov solvers and projection on device (reference semflow/krylov.py).
+
+Same signatures, stopping rules, breakdown semantics and loop order as the
+reference (pcg krylov.py:36-75, gmres :78-160, ProjectionSpace :163-236).
+
+When the operator is a :class:`~paper_2207_07098_b200.operators.GlobalOp`, the
+preconditioner a :class:`~paper_2207_07098_b200.precond.BlockJacobi` (or None)
+and ``dot`` the space's ``gs.dot`` (or None), the solvers run on fused sm_100a
+kernels with all vector updates and inner products on the device (the host only
+reads the scalars the reference's control flow branches on, once per
+iteration).  Any other callables run through a generic torch path that follows
+the reference line by line.
+"""
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+from .errors import SolverBreakdownError
+from .operators import GlobalOp
+from .precond import BlockJacobi
+
+
+@dataclass
+class SolveInfo:
+    x: torch.Tensor
+    iterations: int
+    residual: float
+    initial_residual: float
+    converged: bool
+
+
+def _default_dot(a, b):
+    return float(torch.dot(a.reshape(-1), b.reshape(-1)))
+
+
+def _ptrs(ts):
+    return (ctypes.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+
+
+class _Fused:
+    """Kernel-level helpers bound to one (space, weighting, preconditioner)."""
+
+    def __init__(self, op, precond, dot):
+        sp = op.space
+        self.op = op
+        self.sp = sp
+        self.P = sp.n_points
+        self.dev = sp.device
+        gs = sp.gs
+        # weighting: gs.dot -> 1/mult ; None -> plain dot (krylov.py:32-33)
+        self.mult = _lib.ptr(gs.mult8) if dot is not None else None
+        self.invdiag = precond.inv_diag if precond is not None else None
+        self.w = _device.workspace(self.dev)
+        self.st = _lib.stream_ptr(self.dev)
+
+    def dot(self, a, b, out):
+        _lib.call("sf_glsc3_f64", 1, _ptrs([a]), _ptrs([b]), self.mult, self.P, *self.w.args(),
+                  _lib.ptr(out), self.st)
+
+    def dots(self, pairs, out):
+        for c in range(0, len(pairs), 4):
+            chunk = pairs[c:c + 4]
+            _lib.call("sf_glsc3_f64", len(chunk), _ptrs([a for a, _ in chunk]), _ptrs([b for _, b in chunk]),
+                      self.mult, self.P, *self.w.args(), out.data_ptr() + 8 * c, self.st)
+
+    def read(self, t):
+        h = t.to("cpu", non_blocking=False)
+        return h.tolist()
+
+    def precond_into(self, v, z):
+        if self.invdiag is None:
+            z.copy_(v)
+        else:
+            torch.mul(self.invdiag, v, out=z)
+        return z
+
+
+def _fusable(apply_a, precond, dot):
+    if not isinstance(apply_a, GlobalOp):
+        return False
+    if precond is not None and not (isinstance(precond, BlockJacobi) and precond.space is apply_a.space):
+        return False
+    if dot is not None:
+        owner = getattr(dot, "__self__", None)
+        if owner is not apply_a.space.gs or getattr(dot, "__name__", "") != "dot":
+            return False
+    return apply_a.space.device.type == "cuda"
+
+
+# =========================================================================== PCG
+
+def pcg(apply_a, b, *, tol, max_iter, precond=None, dot=None, x0=None):
+    """Preconditioned CG with absolute residual tolerance (krylov.py:36-75)."""
+    if _fusable(apply_a, precond, dot):
+        return _pcg_fused(apply_a, b, tol, max_iter, precond, dot, x0)
+    return _pcg_generic(apply_a, b, tol, max_iter, precond, dot, x0)
+
+
+def _pcg_generic(apply_a, b, tol, max_iter, precond, dot, x0):
+    if dot is None:
+        dot = _default_dot
+    x = torch.zeros_like(b) if x0 is None else x0.clone()
+    r = b.clone() if x0 is None else b - apply_a(x)
+    res0 = math.sqrt(dot(r, r))
+    res = res0
+    if res <= tol:
+        return SolveInfo(x, 0, res, res0, True)
+    z = precond(r) if precond is not None else r.clone()
+    p = z.clone()
+    rz = dot(r, z)
+    it = 0
+    converged = False
+    for it in range(1, max_iter + 1):
+        ap = apply_a(p)
+        pap = dot(p, ap)
+        if pap <= 0.0:
+            raise SolverBreakdownError(
+                f"non-positive curvature <p,Ap> = {pap:.3e} in conjugate gradients", iteration=it)
+        alpha = rz / pap
+        x += alpha * p
+        r -= alpha * ap
+        res = math.sqrt(dot(r, r))
+        if res <= tol:
+            converged = True
+            break
+        z = precond(r) if precond is not None else r.clone()
+        rz_new = dot(r, z)
+        beta = rz_new / rz
+        rz = rz_new
+        p = z + beta * p
+    return SolveInfo(x, it, res, res0, converged)
+
+
+def _pcg_fused(op, b, tol, max_iter, precond, dot, x0):
+    F = _Fused(op, precond, dot)
+    P = F.P
+    b = b.contiguous()
+    x = torch.zeros_like(b) if x0 is None else x0.clone()
+    r = b.clone() if x0 is None else b - op(x)
+    # scalar slots: 0 rr, 1-2 rz (ping-pong), 3 pap, 4-5 update outputs (rr, rz_new)
+    s = torch.zeros(8, dtype=torch.float64, device=F.dev)
+    F.dot(r, r, s[0:1])
+    res0 = math.sqrt(F.read(s[0:1])[0])
+    res = res0
+    if res <= tol:
+        return SolveInfo(x, 0, res, res0, True)
+    p = torch.empty_like(b)
+    ap = torch.empty_like(b)
+    inv = _lib.ptr(F.invdiag)
+    mult = F.mult
+    wk = F.w.args()
+    sp = lambda i: s.data_ptr() + 8 * i
+    _lib.call("sf_cg_init_f64", _lib.ptr(r), inv, _lib.ptr(p), mult, P, *wk, sp(1), F.st)
+    rz_slot = 1
+    it = 0
+    converged = False
+    for it in range(1, max_iter + 1):
+        op.apply_into(p, ap)
+        F.dot(p, ap, s[3:4])
+        _lib.call("sf_cg_update_f64", _lib.ptr(x), _lib.ptr(r), _lib.ptr(p), _lib.ptr(ap), inv, mult,
+                  sp(rz_slot), sp(3), P, *wk, sp(4), F.st)
+        pap, rr = F.read(s[3:5])
+        if pap <= 0.0:
+            raise SolverBreakdownError(
+                f"non-positive curvature <p,Ap> = {pap:.3e} in conjugate gradients", iteration=it)
+        res = math.sqrt(rr)
+        if res <= tol:
+            converged = True
+            break
+        new_slot = 2 if rz_slot == 1 else 1
+        # rz_new lives in slot 5; copy it into the free ping-pong slot for the next round
+        s[new_slot:new_slot + 1].copy_(s[5:6])
+        _lib.call("sf_cg_direction_f64", _lib.ptr(p), _lib.ptr(r), inv, sp(new_slot), sp(rz_slot), P, F.st)
+        rz_slot = new_slot
+    return SolveInfo(x, it, res, res0, converged)
+
+
+# =========================================================================== GMRES
+
+def gmres(apply_a, b, *, tol, max_iter, restart=10, precond=None, dot=None, x0=None):
+    """Flexible right-preconditioned restarted GMRES (krylov.py:78-160)."""
+    if _fusable(apply_a, precond, dot):
+        return _gmres_fused(apply_a, b, tol, max_iter, restart, precond, dot, x0)
+    return _gmres_generic(apply_a, b, tol, max_iter, restart, precond, dot, x0)
+
+
+def _givens_column(hcol, j, cs, sn, g, total):
+    """Apply the stored rotations to column j and form the new one (krylov.py:124-142)."""
+    for i in range(j):
+        tmp = cs[i] * hcol[i] + sn[i] * hcol[i + 1]
+        hcol[i + 1] = -sn[i] * hcol[i] + cs[i] * hcol[i + 1]
+        hcol[i] = tmp
+    denom = np.hypot(hcol[j], hcol[j + 1])
+    if denom == 0.0:
+        raise SolverBreakdownError(
+            "zero Hessenberg column in GMRES (operator annihilated the search direction)",
+            iteration=total + 1)
+    cs[j] = hcol[j] / denom
+    sn[j] = hcol[j + 1] / denom
+    hcol[j] = denom
+    hcol[j + 1] = 0.0
+    g[j + 1] = -sn[j] * g[j]
+    g[j] = cs[j] * g[j]
+
+
+def _back_substitute(h, g, j_end):
+    y = np.zeros(j_end)
+    for i in range(j_end - 1, -1, -1):
+        y[i] = (g[i] - h[i, i + 1:j_end] @ y[i + 1:j_end]) / h[i, i]
+    return y
+
+
+def _gmres_generic(apply_a, b, tol, max_iter, restart, precond, dot, x0):
+    if dot is None:
+        dot = _default_dot
+    x = torch.zeros_like(b) if x0 is None else x0.clone()
+    r = b.clone() if x0 is None else b - apply_a(x)
+    beta = math.sqrt(dot(r, r))
+    res0 = beta
+    if beta <= tol:
+        return SolveInfo(x, 0, beta, res0, True)
+    total = 0
+    converged = False
+    while total < max_iter and not converged:
+        m = min(restart, max_iter - total)
+        vs = [r / beta]
+        zs = []
+        h = np.zeros((m + 1, m))
+        cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
+        g[0] = beta
+        j_end = 0
+        for j in range(m):
+            z = precond(vs[j]) if precond is not None else vs[j].clone()
+            zs.append(z)
+            w = apply_a(z)
+            norm_before = math.sqrt(dot(w, w))
+            hcol = np.zeros(j + 2)
+            for i in range(j + 1):
+                hij = dot(w, vs[i])
+                w -= hij * vs[i]
+                hcol[i] = hij
+            norm_after = math.sqrt(dot(w, w))
+            if norm_after < 0.7071 * norm_before:
+                for i in range(j + 1):
+                    c = dot(w, vs[i])
+                    w -= c * vs[i]
+                    hcol[i] += c
+                norm_after = math.sqrt(dot(w, w))
+            hcol[j + 1] = norm_after
+            _givens_column(hcol, j, cs, sn, g, total)
+            h[: j + 2, j] = hcol
+            total += 1
+            j_end = j + 1
+            happy = norm_after <= 1e-14 * max(norm_before, 1.0)
+            if abs(g[j + 1]) <= tol or happy or total >= max_iter:
+                break
+            vs.append(w / norm_after)
+        y = _back_substitute(h, g, j_end)
+        for i in range(j_end):
+            x += float(y[i]) * zs[i]
+        r = b - apply_a(x)
+        beta = math.sqrt(dot(r, r))
+        if beta <= tol:
+            converged = True
+    return SolveInfo(x, total, beta, res0, converged)
+
+
+def _gmres_fused(op, b, tol, max_iter, restart, precond, dot, x0):
+    F = _Fused(op, precond, dot)
+    P = F.P
+    dev = F.dev
+    b = b.contiguous()
+    x = torch.zeros_like(b) if x0 is None else x0.clone()
+    r = b.clone() if x0 is None else b - op(x)
+    mult = F.mult
+    wk = F.w.args()
+    inv = _lib.ptr(F.invdiag)
+    s0 = torch.zeros(4, dtype=torch.float64, device=dev)
+    F.dot(r, r, s0[0:1])
+    beta = math.sqrt(F.read(s0[0:1])[0])
+    res0 = beta
+    if beta <= tol:
+        return SolveInfo(x, 0, beta, res0, True)
+    # per-cycle device scalars: [2*i] = h_i (first pass), [2*i+1] = <w,w> ; second
+    # pass at offset 2*(restart+2); slot `sc` holds the divisor for scale_div
+    nh = 2 * (restart + 2)
+    hs = torch.zeros(2 * nh + 4, dtype=torch.float64, device=dev)
+    sc = 2 * nh
+    hp = lambda i: hs.data_ptr() + 8 * i
+    z = torch.empty_like(b)
+    total = 0
+    converged = False
+    while total < max_iter and not converged:
+        m = min(restart, max_iter - total)
+        v0 = torch.empty_like(b)
+        hs[sc:sc + 1].fill_(beta)
+        _lib.call("sf_scale_div_f64", _lib.ptr(v0), _lib.ptr(r), None, None, hp(sc), P, F.st)
+        vs = [v0]
+        h = np.zeros((m + 1, m))
+        cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
+        g[0] = beta
+        j_end = 0
+        for j in range(m):
+            F.precond_into(vs[j], z)
+            w = torch.empty_like(b)
+            op.apply_into(z, w)
+            # MGS sweep: pass 0 = (<w,v0>, <w,w>), pass i = (w -= h_{i-1} v_{i-1}; <w,v_i>),
+            # last = (w -= h_j v_j; <w,w>)
+            _lib.call("sf_mgs_step_f64", _lib.ptr(w), None, None, _lib.ptr(vs[0]), None, None, mult, 1,
+                      P, *wk, hp(0), F.st)
+            for i in range(1, j + 1):
+                _lib.call("sf_mgs_step_f64", _lib.ptr(w), _lib.ptr(vs[i - 1]), hp(2 * (i - 1)),
+                          _lib.ptr(vs[i]), None, None, mult, 0, P, *wk, hp(2 * i), F.st)
+            _lib.call("sf_mgs_step_f64", _lib.ptr(w), _lib.ptr(vs[j]), hp(2 * j), None, None, None, mult, 1,
+                      P, *wk, hp(2 * (j + 1)), F.st)
+            vals = F.read(hs[: 2 * (j + 2)])
+            norm_before = math.sqrt(vals[1])
+            hcol = np.zeros(j + 2)
+            for i in range(j + 1):
+                hcol[i] = vals[2 * i]
+            norm_after = math.sqrt(vals[2 * (j + 1) + 1])
+            if norm_after < 0.7071 * norm_before:
+                o = nh
+                _lib.call("sf_mgs_step_f64", _lib.ptr(w), None, None, _lib.ptr(vs[0]), None, None, mult, 0,
+                          P, *wk, hp(o), F.st)
+                for i in range(1, j + 1):
+                    _lib.call("sf_mgs_step_f64", _lib.ptr(w), _lib.ptr(vs[i - 1]), hp(o + 2 * (i - 1)),
+                              _lib.ptr(vs[i]), None, None, mult, 0, P, *wk, hp(o + 2 * i), F.st)
+                _lib.call("sf_mgs_step_f64", _lib.ptr(w), _lib.ptr(vs[j]), hp(o + 2 * j), None, None, None,
+                          mult, 1, P, *wk, hp(o + 2 * (j + 1)), F.st)
+                v2 = F.read(hs[o: o + 2 * (j + 2)])
+                for i in range(j + 1):
+                    hcol[i] += v2[2 * i]
+                norm_after = math.sqrt(v2[2 * (j + 1) + 1])
+            hcol[j + 1] = norm_after
+            _givens_column(hcol, j, cs, sn, g, total)
+            h[: j + 2, j] = hcol
+            total += 1
+            j_end = j + 1
+            happy = norm_after <= 1e-14 * max(norm_before, 1.0)
+            if abs(g[j + 1]) <= tol or happy or total >= max_iter:
+                break
+            hs[sc:sc + 1].fill_(norm_after)
+            _lib.call("sf_scale_div_f64", _lib.ptr(w), _lib.ptr(w), None, None, hp(sc), P, F.st)
+            vs.append(w)
+        y = _back_substitute(h, g, j_end)
+        _lincomb(x, x, vs[:j_end], y, F.invdiag, P, dev, F.st)
+        ax = op(x)
+        _lib.call("sf_residual_f64", _lib.ptr(r), _lib.ptr(b), _lib.ptr(ax), mult, P, *wk, _lib.ptr(s0[0:1]), F.st)
+        beta = math.sqrt(F.read(s0[0:1])[0])
+        if beta <= tol:
+            converged = True
+    return SolveInfo(x, total, beta, res0, converged)
+
+
+def _lincomb(x, x0, vecs, coef, invdiag, P, dev, st):
+    """x = x0 + sum_i coef[i] M vecs[i] (coef host array or device tensor)."""
+    nv = len(vecs)
+    if nv == 0:
+        if x0 is not None and x0.data_ptr() != x.data_ptr():
+            x.copy_(x0)
+        elif x0 is None:
+            x.zero_()
+        return x
+    ptrs = torch.tensor([v.data_ptr() for v in vecs], dtype=torch.int64, device=dev)
+    if isinstance(coef, torch.Tensor):
+        cd = coef.to(device=dev, dtype=torch.float64).contiguous()
+    else:
+        cd = torch.tensor(np.asarray(coef, dtype=np.float64), device=dev)
+    _lib.call("sf_lincomb_f64", _lib.ptr(x), _lib.ptr(x0), _lib.ptr(ptrs), _lib.ptr(cd), _lib.ptr(invdiag),
+              nv, P, st)
+    return x
+
+
+# =========================================================================== projection
+
+class ProjectionSpace:
+    """A-orthonormal basis of previous solutions (krylov.py:163-236)."""
+
+    def __init__(self, dot=None, capacity=20, reset_every=20):
+        self.dot = dot if dot is not None else _default_dot
+        self.capacity = int(capacity)
+        self.reset_every = int(reset_every)
+        self.xs = []
+        self.axs = []
+        self._solves = 0
+
+    @property
+    def count(self):
+        return len(self.xs)
+
+    def invalidate(self):
+        self.xs = []
+        self.axs = []
+        self._solves = 0
+
+    def _fused(self, apply_a):
+        if not isinstance(apply_a, GlobalOp):
+            return None
+        gs = apply_a.space.gs
+        owner = getattr(self.dot, "__self__", None)
+        if owner is not gs:
+            return None
+        return _Fused(apply_a, None, self.dot)
+
+    def prepare(self, rhs, apply_a):
+        self._solves += 1
+        if self._solves > self.reset_every:
+            self.xs = []
+            self.axs = []
+            self._solves = 1
+        if not self.xs:
+            return torch.zeros_like(rhs), rhs.clone()
+        F = self._fused(apply_a)
+        if F is None:
+            x0 = torch.zeros_like(rhs)
+            for xi in self.xs:
+                x0 += self.dot(xi, rhs) * xi
+            return x0, rhs - apply_a(x0)
+        k = len(self.xs)
+        coef = torch.zeros(k, dtype=torch.float64, device=F.dev)
+        F.dots([(xi, rhs) for xi in self.xs], coef)
+        x0 = torch.empty_like(rhs)
+        _lincomb(x0, None, self.xs, coef, None, F.P, F.dev, F.st)
+        return x0, rhs - apply_a(x0)
+
+    def absorb(self, dx, apply_a):
+        if len(self.xs) >= self.capacity:
+            self.xs = []
+            self.axs = []
+        F = self._fused(apply_a)
+        d = dx.clone()
+        ad = apply_a(d)
+        if F is None:
+            a0 = self.dot(d, ad)
+            if a0 <= 0.0:
+                return
+            for xi, axi in zip(self.xs, self.axs):
+                c = self.dot(xi, ad)
+                d -= c * xi
+                ad -= c * axi
+            nrm2 = self.dot(d, ad)
+            if nrm2 <= 1e-14 * a0:
+                return
+            nrm = math.sqrt(nrm2)
+            self.xs.append(d / nrm)
+            self.axs.append(ad / nrm)
+            return
+        k = len(self.xs)
+        s = torch.zeros(2 * k + 8, dtype=torch.float64, device=F.dev)
+        sp = lambda i: s.data_ptr() + 8 * i
+        F.dot(d, ad, s[0:1])
+        a0 = F.read(s[0:1])[0]
+        if a0 <= 0.0:
+            return
+        wk = F.w.args()
+        # c_i = <ad, x_i> after the updates of 0..i-1 (slot 2 + 2 i)
+        for i in range(k):
+            vprev = self.axs[i - 1] if i else None
+            v2prev = self.xs[i - 1] if i else None
+            _lib.call("sf_mgs_step_f64", _lib.ptr(ad), _lib.ptr(vprev), sp(2 + 2 * (i - 1)) if i else None,
+                      _lib.ptr(self.xs[i]), _lib.ptr(d) if i else None, _lib.ptr(v2prev), F.mult, 0, F.P,
+                      *wk, sp(2 + 2 * i), F.st)
+        if k:
+            _lib.call("sf_mgs_step_f64", _lib.ptr(ad), _lib.ptr(self.axs[k - 1]), sp(2 + 2 * (k - 1)), None,
+                      _lib.ptr(d), _lib.ptr(self.xs[k - 1]), F.mult, 0, F.P, *wk, sp(2 + 2 * k), F.st)
+        F.dot(d, ad, s[1:2])
+        nrm2 = F.read(s[1:2])[0]
+        if nrm2 <= 1e-14 * a0:
+            return
+        nrm = math.sqrt(nrm2)
+        s[0:1].fill_(nrm)
+        xn = torch.empty_like(d)
+        axn = torch.empty_like(ad)
+        _lib.call("sf_scale_div_f64", _lib.ptr(xn), _lib.ptr(d), _lib.ptr(axn), _lib.ptr(ad), sp(0), F.P, F.st)
+        self.xs.append(xn)
+        self.axs.append(axn)

@@ -1,0 +1,185 @@
+"""Device matrix-free operators (reference semflow/operators.py).
+
+Every function takes a :class:`~paper_2207_07098_b200.space.FunctionSpace` and
+torch CUDA tensors and mirrors the reference signature of the same name.  The
+assembled operator returned by :func:`make_global_op` is the hot path: one
+sm_100a Ax_helm launch (mask applied on load, output select fused) followed by
+one in-place dssum over the shared gids.
+"""
+
+import math
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+from .space import pack_bits
+
+OP_GRAD, OP_DIV, OP_CURL, OP_ADVECT = 0, 1, 2, 3
+
+
+def _ex():
+    return 1 if _device.EXACT else 0
+
+
+def _ax_local(space, u, lam_visc, lam_mass, out=None):
+    _lib.require_cuda(u)
+    u = u.contiguous()
+    w = torch.empty_like(u) if out is None else out
+    E = u.shape[0]
+    _lib.call("sf_ax_helm_f64", space.dmat.ctypes.data, space.n, _lib.ptr(space.geom), _lib.ptr(space.bm),
+              _lib.ptr(u), _lib.ptr(w), E, float(lam_visc), float(lam_mass), _ex(),
+              _lib.stream_ptr(space.device))
+    return w
+
+
+def laplace_local(space, u):
+    """Element-local D^T G D u (operators.py:16-18)."""
+    return _ax_local(space, u, 1.0, 0.0)
+
+
+def helmholtz_local(space, u, lam_visc, lam_mass):
+    """Element-local lam_visc D^T G D u + lam_mass B u (operators.py:21-29)."""
+    if lam_visc <= 0.0:
+        raise ValueError(f"lam_visc must be positive, got {lam_visc}")
+    if lam_mass < 0.0:
+        raise ValueError(f"lam_mass must be non-negative, got {lam_mass}")
+    return _ax_local(space, u, float(lam_visc), float(lam_mass))
+
+
+class GlobalOp:
+    """u -> mask*gs.add(ax(mask*u)) + (1-mask)*u  (operators.py:32-56).
+
+    Callable like the reference closure.  ``mask`` must be a 0/1 field (as built
+    by BoundarySet); it is stored as per-element bitmasks, and the masked copies
+    of shared gids are flagged in a private copy of the shared perm.
+    """
+
+    def __init__(self, space, lam_visc, lam_mass, mask=None):
+        self.space = space
+        self.lam_visc = float(lam_visc)
+        self.lam_mass = float(lam_mass)
+        gs = space.gs
+        E, n = space.n_elements, space.n
+        self.masked = False
+        if mask is not None:
+            m = torch.as_tensor(mask, dtype=torch.float64, device=space.device).reshape(E, n ** 3)
+            if not bool(((m == 0.0) | (m == 1.0)).all()):
+                raise ValueError("make_global_op: mask must contain only 0.0 and 1.0")
+            keep = m != 0.0
+            if not bool(keep.all()):
+                self.masked = True
+                self.inmask = pack_bits(keep)
+                self.outsel = pack_bits(keep) | gs.shared_bits
+                dropped = (~keep).reshape(-1)
+                self.sh_perm = torch.where(
+                    dropped[gs.sh_perm.long()],
+                    gs.sh_perm | torch.tensor(-2**31, dtype=torch.int32, device=space.device),
+                    gs.sh_perm).contiguous()
+            self.mask = m.view(space.shape)
+        else:
+            self.mask = None
+        self.launches = 0
+
+    def apply_into(self, u, w):
+        """w <- A u (w must not alias u)."""
+        sp = self.space
+        gs = sp.gs
+        st = _lib.stream_ptr(sp.device)
+        E = sp.n_elements
+        if self.masked:
+            _lib.call("sf_ax_masked_f64", sp.dmat.ctypes.data, sp.n, _lib.ptr(sp.geom), _lib.ptr(sp.bm),
+                      _lib.ptr(u), _lib.ptr(w), E, self.lam_visc, self.lam_mass, _lib.ptr(self.inmask),
+                      _lib.ptr(self.outsel), _ex(), st)
+            _lib.call("sf_dssum_f64", _lib.ptr(w), _lib.ptr(gs.sh_off), _lib.ptr(self.sh_perm),
+                      gs.n_shared, 2, _lib.ptr(u), st)
+        else:
+            _lib.call("sf_ax_helm_f64", sp.dmat.ctypes.data, sp.n, _lib.ptr(sp.geom), _lib.ptr(sp.bm),
+                      _lib.ptr(u), _lib.ptr(w), E, self.lam_visc, self.lam_mass, _ex(), st)
+            _lib.call("sf_dssum_f64", _lib.ptr(w), _lib.ptr(gs.sh_off), _lib.ptr(gs.sh_perm),
+                      gs.n_shared, 0, None, st)
+        self.launches += 2
+        return w
+
+    def __call__(self, u):
+        _lib.require_cuda(u)
+        u = u.contiguous()
+        return self.apply_into(u, torch.empty_like(u))
+
+
+def make_global_op(space, lam_visc, lam_mass, mask=None):
+    return GlobalOp(space, lam_visc, lam_mass, mask)
+
+
+def _deriv(space, op, inp, c=None, sign=1.0, out_comps=3):
+    E, n = space.n_elements, space.n
+    out = torch.empty((out_comps,) + space.shape if out_comps > 1 else space.shape,
+                      dtype=torch.float64, device=space.device)
+    _lib.call("sf_deriv_f64", op, space.dmat.ctypes.data, n, _lib.ptr(inp.contiguous()),
+              _lib.ptr(c.contiguous()) if c is not None else None, _lib.ptr(space.rx), _lib.ptr(out),
+              E, float(sign), _ex(), _lib.stream_ptr(space.device))
+    return out
+
+
+def grad(space, u):
+    """Physical gradient (3, E, n, n, n) (operators.py:59-66)."""
+    return _deriv(space, OP_GRAD, u)
+
+
+def div(space, v):
+    """Pointwise divergence (operators.py:69-76)."""
+    return _deriv(space, OP_DIV, v, out_comps=1)
+
+
+def curl(space, v):
+    """Pointwise curl (operators.py:79-88)."""
+    return _deriv(space, OP_CURL, v)
+
+
+def advect_vec(space, c, v, dealias=None, sign=1.0):
+    """(c . grad) v_l for l = 0, 1, 2 (operators.py:108-126, collocation)."""
+    if dealias is not None:
+        raise NotImplementedError("over-integration (Dealias) is not on the device path yet")
+    return _deriv(space, OP_ADVECT, v, c=c, sign=sign)
+
+
+def advect(space, c, u, dealias=None):
+    g = grad(space, u)
+    return c[0] * g[0] + c[1] * g[1] + c[2] * g[2]
+
+
+def weak_grad_dot(space, w):
+    """r_i = (grad phi_i, w) -- Nek cdtp (operators.py:91-105)."""
+    out = torch.empty(space.shape, dtype=torch.float64, device=space.device)
+    _lib.call("sf_cdtp_f64", space.dmat.ctypes.data, space.n, _lib.ptr(w.contiguous()), _lib.ptr(space.rx),
+              _lib.ptr(space.bm), _lib.ptr(out), space.n_elements, _ex(), _lib.stream_ptr(space.device))
+    return out
+
+
+def _dxi(points):
+    xi = np.asarray(points, dtype=np.float64)
+    gaps = np.diff(xi)
+    dxi = np.empty_like(xi)
+    dxi[0] = gaps[0]
+    dxi[-1] = gaps[-1]
+    if xi.size > 2:
+        dxi[1:-1] = np.minimum(gaps[:-1], gaps[1:])
+    return np.ascontiguousarray(dxi)
+
+
+def cfl_max_async(space, v, out_bits):
+    """out_bits (uint64 as int64 tensor) <- bits of max_p sum_s |rx_s . v| / dxi_s."""
+    dxi = _dxi(space.basis.points)
+    _lib.call("sf_cfl_f64", _lib.ptr(v.contiguous()), _lib.ptr(space.rx), dxi.ctypes.data, space.n,
+              space.n_elements, _lib.ptr(out_bits), _ex(), _lib.stream_ptr(space.device))
+    return out_bits
+
+
+def cfl(space, v, dt):
+    """CFL number (operators.py:161-182)."""
+    bits = torch.zeros(1, dtype=torch.int64, device=space.device)
+    cfl_max_async(space, v, bits)
+    if space.n_elements == 0:
+        return 0.0
+    val = bits.cpu().view(torch.float64).item()
+    return float(dt) * float(val)

@@ -1,0 +1,506 @@
+"""Device-resident function space and gather-scatter (reference space.py).
+
+``build_space(mesh, basis)`` builds everything on the GPU:
+
+* GLL coordinates and geometric factors with the sm_100a setup kernels, bit-
+  identical to the reference's numba-lane ``build_space`` (space.py:195-262);
+* the gather-scatter numbering (space.py:265-314).  The reference groups
+  coincident points with a KD-tree and union-find; here coincident points are
+  grouped *topologically* -- a GLL point on an element vertex, edge or face is
+  keyed by the mesh-vertex ids of that entity plus its canonical position on it
+  -- which yields the same groups on every conforming mesh the reference
+  accepts, in O(P log P) device sorts instead of 80 s of host work at 32^3.
+  Group ids are then ordered exactly as the reference orders them (lexicographic
+  by the *exact bits* of the representative's (x, y, z), representative = lowest
+  local index), and ``perm``/``offsets`` follow (ascending local index within a
+  gid).  gid/perm/offsets are bit-identical to the reference (tests/test_setup_parity.py).
+
+Memory layout in HBM (per rank): fields (E, n, n, n) float64; geom (6, E, n^3);
+rx (3, 3, E, n^3); bm; uint8 multiplicity (1 B/point, for glsc3 weights);
+int32 shared-gid maps (S_g + 1 offsets, S_l perm) for dssum; per-element
+bitmasks (ceil(n^3/32) uint32 words) for masks and the shared-point set.
+"""
+
+import math
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+from .errors import ConfigError, GeometryError, TopologyError
+
+_FACE_NORMAL_SIGN = (-1.0, 1.0, 1.0, -1.0, -1.0, 1.0)
+
+
+# --------------------------------------------------------------------------- bits
+
+def pack_bits(flags):
+    """(E, nnn) bool -> (E, ceil(nnn/32)) int32 words, bit p of element e = flags[e, p]."""
+    E, nnn = flags.shape
+    wpe = (nnn + 31) // 32
+    pad = wpe * 32 - nnn
+    f = flags.to(torch.int64)
+    if pad:
+        f = torch.nn.functional.pad(f, (0, pad))
+    f = f.view(E, wpe, 32)
+    sh = torch.arange(32, device=flags.device, dtype=torch.int64)
+    words = (f << sh).sum(dim=2)
+    words = torch.where(words >= 2**31, words - 2**32, words)
+    return words.to(torch.int32).contiguous()
+
+
+# --------------------------------------------------------------------------- gather-scatter
+
+class GatherScatter:
+    """Direct-stiffness summation QQ^T on device (reference space.py:20-76).
+
+    Reference-format maps (int64 device tensors ``gid``, ``perm``, ``offsets``;
+    float64 ``mult``/``invmult`` on demand) are kept for parity checks and the
+    unique-value helpers.  The hot path uses only the *shared* maps:
+    ``sh_off``/``sh_perm`` (int32) over the gids of multiplicity > 1, and the
+    uint8 multiplicity ``mult8`` for glsc3 weights.
+    """
+
+    def __init__(self, gid, perm, offsets, shape):
+        self.shape = tuple(shape)
+        self.device = gid.device
+        self.gid = gid
+        self.perm = perm
+        self.offsets = offsets
+        self.n_gid = int(offsets.numel() - 1)
+        P = int(gid.numel())
+        self.P = P
+        if P >= 2**31 - 1:
+            raise ConfigError("more than 2^31 local points on one device; partition the mesh")
+        counts = offsets[1:] - offsets[:-1]
+        if counts.numel() and int(counts.max()) > 255:
+            raise TopologyError("a global id has more than 255 local copies")
+        self.mult8 = counts[gid].to(torch.uint8).contiguous()
+        cnt_pos = torch.repeat_interleave(counts, counts)   # count of the gid at each perm slot
+        sel = cnt_pos > 1
+        shared_gid = counts > 1
+        self.n_shared = int(shared_gid.sum())
+        self.sh_perm = perm[sel].to(torch.int32).contiguous()
+        sh_counts = counts[shared_gid]
+        self.sh_off = torch.zeros(self.n_shared + 1, dtype=torch.int32, device=self.device)
+        if self.n_shared:
+            self.sh_off[1:] = torch.cumsum(sh_counts, 0).to(torch.int32)
+        E = self.shape[0]
+        nnn = P // E if E else 0
+        self.shared_bits = pack_bits((self.mult8 > 1).view(E, nnn)) if E else None
+        self._masked_perm = {}
+        self._mult = None
+
+    # ------------------------------------------------------------ properties
+    @property
+    def mult(self):
+        if self._mult is None:
+            self._mult = self.mult8.to(torch.float64).view(self.shape)
+        return self._mult
+
+    @property
+    def invmult(self):
+        return 1.0 / self.mult
+
+    @property
+    def shared_local_points(self):
+        return int(self.sh_perm.numel())
+
+    # ------------------------------------------------------------ kernels
+    def _dssum_rows(self, flat, mode, u=None):
+        st = _lib.stream_ptr(self.device)
+        for row in range(flat.shape[0]):
+            _lib.call("sf_dssum_f64", _lib.ptr(flat[row]), _lib.ptr(self.sh_off), _lib.ptr(self.sh_perm),
+                      self.n_shared, mode, _lib.ptr(u[row]) if u is not None else None, st)
+
+    def add_(self, u):
+        """In-place QQ^T u (any leading axes, one row per leading index)."""
+        _lib.require_cuda(u)
+        flat = u.view(-1, self.P)
+        self._dssum_rows(flat, 0)
+        return u
+
+    def avg_(self, u):
+        _lib.require_cuda(u)
+        flat = u.view(-1, self.P)
+        self._dssum_rows(flat, 1)
+        return u
+
+    def add(self, u):
+        """QQ^T u into a new tensor (space.py:38-49)."""
+        return self.add_(u.contiguous().clone())
+
+    def avg(self, u):
+        """Multiplicity-weighted average, sum * (1.0/count) (space.py:51-60)."""
+        return self.avg_(u.contiguous().clone())
+
+    def masked_perm(self, mask_bits_flat):
+        """Shared perm with bit 31 set on masked copies (cached per mask object)."""
+        key = id(mask_bits_flat)
+        mp = self._masked_perm.get(key)
+        if mp is None:
+            m = mask_bits_flat[self.sh_perm.long()]
+            mp = torch.where(m, self.sh_perm | torch.tensor(-2**31, dtype=torch.int32, device=self.device),
+                             self.sh_perm).contiguous()
+            self._masked_perm[key] = (mp, mask_bits_flat)
+            return mp
+        return mp[0]
+
+    def dot_async(self, u, v, out):
+        """Write <u, v>_{1/mult} into the device scalar ``out`` (no sync)."""
+        w = _device.workspace(self.device)
+        pa = (ctypes_ptrs([u]))
+        pb = (ctypes_ptrs([v]))
+        _lib.call("sf_glsc3_f64", 1, pa, pb, _lib.ptr(self.mult8), self.P * (u.numel() // self.P),
+                  *w.args(), _lib.ptr(out), _lib.stream_ptr(self.device))
+        return out
+
+    def dot(self, u, v):
+        """Multiplicity-weighted inner product (space.py:72-76), host float."""
+        if u.numel() != self.P or v.numel() != self.P:
+            # vector fields: sum of the component dots is NOT what the reference
+            # does (it flattens); flatten likewise with a repeated weight
+            return self._dot_flat(u, v)
+        w = _device.workspace(self.device)
+        self.dot_async(u, v, w.slots[0:1])
+        return w.read(0)[0]
+
+    def _dot_flat(self, u, v):
+        rows = u.numel() // self.P
+        tot = 0.0
+        w = _device.workspace(self.device)
+        uf, vf = u.reshape(rows, self.P), v.reshape(rows, self.P)
+        for r in range(rows):
+            self.dot_async(uf[r], vf[r], w.slots[r:r + 1])
+        vals = w.read(0, rows)
+        for x in vals:
+            tot += x
+        return tot
+
+    def gather_unique(self, u):
+        return u.reshape(-1)[self.perm[self.offsets[:-1]]]
+
+    def scatter_unique(self, vals, shape):
+        counts = self.offsets[1:] - self.offsets[:-1]
+        out = torch.empty(int(np.prod(shape)), dtype=torch.float64, device=self.device)
+        out[self.perm] = torch.repeat_interleave(vals.to(torch.float64), counts)
+        return out.view(shape)
+
+
+def ctypes_ptrs(tensors):
+    import ctypes
+
+    arr = (ctypes.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
+    return arr
+
+
+# --------------------------------------------------------------------------- topology
+
+def _boundary_point_table(n):
+    """Per local boundary point of an element: kind and the corners/positions that key it.
+
+    Returns numpy arrays over the nb boundary points: lp (local index), kind
+    (0 vertex, 1 edge, 2 face), corners (nb, 4) and positions (nb, 2).
+    For edges corners[:, :2] are the edge ends at parameter 0 and m; for faces
+    corners = (c00, c10, c01, c11) over the two in-face axes a1 < a2.
+    """
+    m = n - 1
+    lp, kind, cor, pos = [], [], [], []
+    for i in range(n):
+        for j in range(n):
+            for k in range(n):
+                idx = (i, j, k)
+                inner = [0 < v < m for v in idx]
+                ni = sum(inner)
+                if ni == 3:
+                    continue
+                hi = [1 if v == m else 0 for v in idx]
+                if ni == 0:
+                    c = hi[0] | (hi[1] << 1) | (hi[2] << 2)
+                    lp.append((i * n + j) * n + k); kind.append(0)
+                    cor.append((c, c, c, c)); pos.append((0, 0))
+                elif ni == 1:
+                    ax = inner.index(True)
+                    base = [hi[0], hi[1], hi[2]]
+                    base[ax] = 0
+                    ca = base[0] | (base[1] << 1) | (base[2] << 2)
+                    cb = ca | (1 << ax)
+                    lp.append((i * n + j) * n + k); kind.append(1)
+                    cor.append((ca, cb, ca, cb)); pos.append((idx[ax], 0))
+                else:
+                    a1, a2 = [a for a in range(3) if inner[a]]
+                    fixed = [a for a in range(3) if not inner[a]][0]
+                    base = [0, 0, 0]
+                    base[fixed] = hi[fixed]
+
+                    def corner(b1, b2):
+                        c = list(base)
+                        c[a1] = b1
+                        c[a2] = b2
+                        return c[0] | (c[1] << 1) | (c[2] << 2)
+
+                    lp.append((i * n + j) * n + k); kind.append(2)
+                    cor.append((corner(0, 0), corner(1, 0), corner(0, 1), corner(1, 1)))
+                    pos.append((idx[a1], idx[a2]))
+    return (np.array(lp, dtype=np.int64), np.array(kind, dtype=np.int64),
+            np.array(cor, dtype=np.int64), np.array(pos, dtype=np.int64))
+
+
+def build_gather_scatter(elements, coords, n):
+    """Bit-exact reference numbering (space.py:265-314) from topology + coordinates.
+
+    elements: (E, 8) int64 device tensor of vertex ids; coords: (3, E, n, n, n).
+    """
+    dev = coords.device
+    E = elements.shape[0]
+    nnn = n ** 3
+    P = E * nnn
+    m = n - 1
+    if E and int(elements.max()) >= 2**30:
+        raise ConfigError("vertex ids must be < 2^30")
+    lp, kind, cor, pos = (torch.from_numpy(a).to(dev) for a in _boundary_point_table(n))
+    nb = lp.numel()
+    V = elements[:, cor.view(-1)].view(E, nb, 4)            # (E, nb, 4) vertex ids
+    kind_b = kind.view(1, nb).expand(E, nb)
+    p1 = pos[:, 0].view(1, nb).expand(E, nb)
+    p2 = pos[:, 1].view(1, nb).expand(E, nb)
+    va, vb, vc, vd = V[..., 0], V[..., 1], V[..., 2], V[..., 3]
+    # edges: orient from the lower vertex id
+    e_lo = torch.minimum(va, vb)
+    e_hi = torch.maximum(va, vb)
+    e_pos = torch.where(va < vb, p1, m - p1)
+    # faces: origin at the lowest vertex id, first axis toward its lower neighbour
+    four = torch.stack([va, vb, vc, vd], dim=-1)            # (c00, c10, c01, c11)
+    v0, arg = four.min(dim=-1)
+    b1 = arg & 1
+    b2 = arg >> 1
+    nA = four.gather(-1, ((1 - b1) | (b2 << 1)).unsqueeze(-1)).squeeze(-1)   # neighbour along a1
+    nB = four.gather(-1, (b1 | ((1 - b2) << 1)).unsqueeze(-1)).squeeze(-1)   # neighbour along a2
+    q1 = torch.where(b1 == 0, p1, m - p1)
+    q2 = torch.where(b2 == 0, p2, m - p2)
+    f_P = torch.where(nA < nB, q1, q2)
+    f_Q = torch.where(nA < nB, q2, q1)
+    f_lo = torch.minimum(nA, nB)
+    f_hi = torch.maximum(nA, nB)
+    k1 = torch.where(kind_b == 0, va << 30,
+                     torch.where(kind_b == 1, (1 << 60) | (e_lo << 30) | e_hi,
+                                 (2 << 60) | (v0 << 30) | f_lo))
+    k2 = torch.where(kind_b == 0, torch.zeros_like(va),
+                     torch.where(kind_b == 1, e_pos, (f_hi << 16) | (f_P * n + f_Q)))
+    del V, four, nA, nB, q1, q2, f_P, f_Q, f_lo, f_hi, e_lo, e_hi, e_pos
+    k1 = k1.reshape(-1)
+    k2 = k2.reshape(-1)
+    gpt = (torch.arange(E, device=dev, dtype=torch.int64).view(E, 1) * nnn + lp.view(1, nb)).reshape(-1)
+    # lexicographic sort by (k1, k2), ties by point index (stable sorts)
+    o = torch.sort(k2, stable=True).indices
+    o = o[torch.sort(k1[o], stable=True).indices]
+    sk1, sk2 = k1[o], k2[o]
+    newg = torch.ones_like(sk1, dtype=torch.bool)
+    if newg.numel() > 1:
+        newg[1:] = (sk1[1:] != sk1[:-1]) | (sk2[1:] != sk2[:-1])
+    grp_sorted = torch.cumsum(newg.to(torch.int64), 0) - 1
+    n_bgroups = int(grp_sorted[-1]) + 1 if grp_sorted.numel() else 0
+    grp_of_b = torch.empty_like(grp_sorted)
+    grp_of_b[o] = grp_sorted
+    del o, sk1, sk2, newg, k1, k2, grp_sorted
+    # group index of every local point: boundary groups first, then interior points
+    group = torch.empty(P, dtype=torch.int64, device=dev)
+    group[gpt] = grp_of_b
+    is_int = torch.ones(P, dtype=torch.bool, device=dev)
+    is_int[gpt] = False
+    int_pts = torch.nonzero(is_int).view(-1)
+    group[int_pts] = n_bgroups + torch.arange(int_pts.numel(), device=dev)
+    n_groups = n_bgroups + int_pts.numel()
+    rep = torch.full((n_groups,), P, dtype=torch.int64, device=dev)
+    rep.scatter_reduce_(0, group, torch.arange(P, device=dev), reduce="amin")
+    del is_int, int_pts, grp_of_b, gpt
+    # order groups by representative (the reference's root order), then a stable
+    # lexsort on the exact coordinate bits of the representative: x primary
+    flat = coords.reshape(3, -1)
+    order = torch.sort(rep).indices
+    for l in (2, 1, 0):
+        key = flat[l][rep[order]] + 0.0            # + 0.0 folds -0.0 into +0.0
+        order = order[torch.sort(key, stable=True).indices]
+    rank = torch.empty_like(order)
+    rank[order] = torch.arange(n_groups, device=dev)
+    gid = rank[group]
+    del rank, order, rep, group
+    perm = torch.sort(gid, stable=True).indices
+    counts = torch.bincount(gid, minlength=n_groups)
+    offsets = torch.zeros(n_groups + 1, dtype=torch.int64, device=dev)
+    offsets[1:] = torch.cumsum(counts, 0)
+    return gid, perm, offsets
+
+
+# --------------------------------------------------------------------------- space
+
+def _face_grids(n):
+    base = np.arange(n ** 3, dtype=np.int64).reshape(n, n, n)
+    return np.stack([base[0], base[-1], base[:, 0], base[:, -1], base[:, :, 0], base[:, :, -1]])
+
+
+class FunctionSpace:
+    """Device analogue of the reference FunctionSpace (space.py:102-180)."""
+
+    def __init__(self, basis, mesh, coords, rx, jac, bm, geom, gs, facet_elem, facet_face,
+                 facet_tag, facet_flat, facet_normal, facet_warea):
+        self.basis = basis
+        self.mesh = mesh
+        self.coords = coords
+        self.rx = rx
+        self.jac = jac
+        self.bm = bm
+        self.geom = geom
+        self.gs = gs
+        self.facet_elem = facet_elem
+        self.facet_face = facet_face
+        self.facet_tag = facet_tag
+        self.facet_flat = facet_flat
+        self.facet_normal = facet_normal
+        self.facet_warea = facet_warea
+        self.device = coords.device
+        self.dmat = np.ascontiguousarray(basis.dmat, dtype=np.float64)
+        self.volume = self.integral(torch.ones(self.shape, dtype=torch.float64, device=self.device))
+
+    n = property(lambda self: self.basis.n)
+    n_elements = property(lambda self: self.coords.shape[1])
+    shape = property(lambda self: (self.n_elements, self.n, self.n, self.n))
+    x = property(lambda self: self.coords[0])
+    y = property(lambda self: self.coords[1])
+    z = property(lambda self: self.coords[2])
+    n_points = property(lambda self: self.n_elements * self.n ** 3)
+
+    def zeros(self):
+        return torch.zeros(self.shape, dtype=torch.float64, device=self.device)
+
+    def zeros_vec(self):
+        return torch.zeros((3,) + self.shape, dtype=torch.float64, device=self.device)
+
+    def from_function(self, fn):
+        """fn(x, y, z) on device tensors (use torch ops)."""
+        return torch.as_tensor(fn(self.coords[0], self.coords[1], self.coords[2]),
+                               dtype=torch.float64, device=self.device)
+
+    def integral(self, u):
+        """GLL quadrature sum(bm * u) (space.py:159-161), host float."""
+        w = _device.workspace(self.device)
+        _lib.call("sf_glsc3_f64", 1, ctypes_ptrs([self.bm]), ctypes_ptrs([u]), None, self.n_points,
+                  *w.args(), _lib.ptr(w.slots[1:2]), _lib.stream_ptr(self.device))
+        return w.read(1)[0]
+
+    def l2_norm(self, u):
+        return float(math.sqrt(max(self.integral(u * u), 0.0)))
+
+    def mean(self, u):
+        return self.integral(u) / self.volume
+
+    def facet_sel(self, tag):
+        if tag not in self.mesh.tag_names:
+            raise KeyError(f"unknown boundary tag {tag!r}; have {self.mesh.tag_names}")
+        return self.facet_tag == self.mesh.tag_names.index(tag)
+
+
+def _wc(points):
+    """Trilinear corner weights (8, n^3), reference space.py:183-189 arithmetic."""
+    xi = np.asarray(points, dtype=np.float64)
+    n = xi.size
+    phi = np.stack([(1.0 - xi) / 2.0, (1.0 + xi) / 2.0])
+    wc = np.empty((8, n, n, n))
+    for c in range(8):
+        cr, cs, ct = c & 1, (c >> 1) & 1, (c >> 2) & 1
+        wc[c] = phi[cr][:, None, None] * phi[cs][None, :, None] * phi[ct][None, None, :]
+    return wc.reshape(8, -1)
+
+
+def _facets(mesh, basis, coords, dev):
+    n = basis.n
+    F = int(mesh.facet_elem.size)
+    grids = _face_grids(n)
+    fe = np.asarray(mesh.facet_elem, dtype=np.int64)
+    ff = np.asarray(mesh.facet_face, dtype=np.int64)
+    flat = fe[:, None, None] * n ** 3 + grids[ff]                     # (F, n, n)
+    flat_t = torch.from_numpy(flat).to(dev)
+    if F == 0:
+        return flat_t, torch.zeros((0, n, n, 3), dtype=torch.float64, device=dev), \
+            torch.zeros((0, n, n), dtype=torch.float64, device=dev)
+    d = torch.from_numpy(np.ascontiguousarray(basis.dmat)).to(dev)
+    w = torch.from_numpy(np.ascontiguousarray(basis.weights)).to(dev)
+    fx = coords.reshape(3, -1)[:, flat_t]                              # (3, F, n, n)
+    ta = torch.einsum("ab,lfbc->lfac", d, fx)
+    tb = torch.einsum("ab,lfcb->lfca", d, fx)
+    sign = torch.tensor(_FACE_NORMAL_SIGN, dtype=torch.float64, device=dev)[torch.from_numpy(ff).to(dev)]
+    raw = sign.view(1, F, 1, 1) * torch.cross(ta, tb, dim=0)
+    area = torch.linalg.vector_norm(raw, dim=0)
+    if bool((area <= 0.0).any()):
+        bad = int(torch.nonzero(area <= 0.0)[0, 0])
+        raise GeometryError("degenerate boundary facet", element=int(fe[bad]))
+    normal = (raw / area).permute(1, 2, 3, 0).contiguous()
+    warea = area * (w[:, None] * w[None, :])
+    return flat_t, normal, warea
+
+
+def build_space(mesh, basis, device=None):
+    """Bind a basis to a mesh on the GPU (reference space.py:195-262)."""
+    _lib.load()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise _lib.LibraryError("build_space needs a CUDA device (no CPU fallback)")
+    n = basis.n
+    E = int(mesh.n_elements)
+    nnn = n ** 3
+    st = _lib.stream_ptr(dev)
+    elements = torch.from_numpy(np.ascontiguousarray(mesh.elements, dtype=np.int64)).to(dev)
+    verts = torch.from_numpy(np.ascontiguousarray(mesh.vertices, dtype=np.float64)).to(dev)
+    corners = verts[elements].contiguous()                                  # (E, 8, 3)
+    wc = torch.from_numpy(_wc(basis.points)).to(dev)
+    coords = torch.empty((3, E, n, n, n), dtype=torch.float64, device=dev)
+    _lib.call("sf_trilinear_coords_f64", _lib.ptr(corners), _lib.ptr(wc), n, E, _lib.ptr(coords), st)
+    del corners
+    curved = np.asarray(getattr(mesh, "curved_elem", np.zeros(0, dtype=np.int64)), dtype=np.int64)
+    if curved.size:
+        if mesh.geom_order != basis.order:
+            raise ConfigError(
+                f"mesh curved geometry order {mesh.geom_order} does not match basis order "
+                f"{basis.order}; regenerate the mesh at the solver order")
+        cc = torch.from_numpy(np.ascontiguousarray(mesh.curved_coords, dtype=np.float64)).to(dev)
+        ce = torch.from_numpy(curved).to(dev)
+        for l in range(3):
+            coords[l][ce] = cc[..., l]
+    rx = torch.empty((3, 3, E, n, n, n), dtype=torch.float64, device=dev)
+    jac = torch.empty((E, n, n, n), dtype=torch.float64, device=dev)
+    bm = torch.empty_like(jac)
+    geom = torch.empty((6, E, n, n, n), dtype=torch.float64, device=dev)
+    dh, dptr = _lib.host_f64(basis.dmat)
+    wh, wptr = _lib.host_f64(basis.weights)
+    _lib.call("sf_metrics_f64", dptr, wptr, n, _lib.ptr(coords), E, _lib.ptr(rx), _lib.ptr(jac),
+              _lib.ptr(bm), _lib.ptr(geom), st)
+    bad = jac <= 0.0
+    if bool(bad.any()):
+        e, i, j, k = (int(v) for v in torch.nonzero(bad)[0])
+        raise GeometryError(f"non-positive Jacobian determinant {float(jac[e, i, j, k]):.3e}",
+                            element=e, ref_coords=(basis.points[i], basis.points[j], basis.points[k]))
+    gid, perm, offsets = build_gather_scatter(elements, coords, n)
+    gs = GatherScatter(gid, perm, offsets, (E, n, n, n))
+    flat, normal, warea = _facets(mesh, basis, coords, dev)
+    return FunctionSpace(
+        basis=basis, mesh=mesh, coords=coords, rx=rx, jac=jac, bm=bm, geom=geom, gs=gs,
+        facet_elem=np.asarray(mesh.facet_elem).copy(), facet_face=np.asarray(mesh.facet_face).copy(),
+        facet_tag=np.asarray(mesh.facet_tag).copy(), facet_flat=flat, facet_normal=normal,
+        facet_warea=warea)
+
+
+def from_reference(ref_space, device=None):
+    """Upload a reference ``semflow.space.FunctionSpace`` (numpy) as-is."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    t = lambda a, dt=torch.float64: torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dt)
+    g = ref_space.gs
+    gs = GatherScatter(t(g.gid, torch.int64), t(g.perm, torch.int64), t(g.offsets, torch.int64),
+                       ref_space.shape)
+    return FunctionSpace(
+        basis=ref_space.basis, mesh=ref_space.mesh, coords=t(ref_space.coords), rx=t(ref_space.rx),
+        jac=t(ref_space.jac), bm=t(ref_space.bm), geom=t(ref_space.geom), gs=gs,
+        facet_elem=np.asarray(ref_space.facet_elem).copy(),
+        facet_face=np.asarray(ref_space.facet_face).copy(),
+        facet_tag=np.asarray(ref_space.facet_tag).copy(),
+        facet_flat=t(ref_space.facet_flat, torch.int64), facet_normal=t(ref_space.facet_normal),
+        facet_warea=t(ref_space.facet_warea))

@@ -1,0 +1,329 @@
+"""Generate the golden fixtures from the REFERENCE implementation (run here only).
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache SEMFLOW_NUMBA=1 \
+        python tests/golden/make_golden.py [--skip-big]
+
+Imports `semflow` from /root/reference/pkg/src (read-only, never shipped) and
+records, with the numba lane:
+
+* kernels.npz    -- lane kernel inputs/outputs (sample_fields of
+                    pkg/tests/test_kernels.py plus an lx=8 case), gather/scatter;
+* basis.npz      -- GLL points/weights/D for orders 1..10;
+* spaces.npz     -- meshes (as arrays) and sha256 of coords/rx/jac/bm/geom/gid/
+                    perm/offsets for box, perturbed-box and cylinder meshes, full
+                    arrays for the small ones;
+* operators.npz  -- Ax / global op / gs.add / avg / dot / grad / div / curl /
+                    advect / weak_grad_dot / cfl / BlockJacobi on a perturbed box;
+* solvers.json   -- PCG / GMRES iteration counts and residuals, per-step TGV
+                    and channel diagnostics (iteration counts, residuals, CFL,
+                    divergence, kinetic energy, enstrophy).
+"""
+
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+os.environ.setdefault("SEMFLOW_NUMBA", "1")
+
+from semflow import kernels  # noqa: E402
+from semflow import operators as ops  # noqa: E402
+from semflow.basis import make_basis  # noqa: E402
+from semflow.bc import BoundarySet  # noqa: E402
+from semflow.diagnostics import kinetic_energy  # noqa: E402
+from semflow.krylov import ProjectionSpace, gmres, pcg  # noqa: E402
+from semflow.mesh import gen_box_mesh, gen_cylinder_box_mesh  # noqa: E402
+from semflow.precond import BlockJacobi  # noqa: E402
+from semflow.space import build_space  # noqa: E402
+from semflow.timestep import SolverOptions, Stepper  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+assert kernels.lane_name() == "numba"
+
+
+def sha(a):
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(a.tobytes()).hexdigest()
+
+
+def sample_fields(e, n, seed):
+    """Same recipe as pkg/tests/test_kernels.py:25-35."""
+    rng = np.random.default_rng(seed)
+    u = rng.standard_normal((e, n, n, n))
+    a = rng.standard_normal((n, n))
+    g = rng.standard_normal((6, e, n, n, n))
+    g[0] += 3.0
+    g[3] += 3.0
+    g[5] += 3.0
+    b = rng.uniform(0.5, 2.0, (e, n, n, n))
+    return a, g, b, u
+
+
+def gen_kernels():
+    out = {}
+    for tag, (e, n, seed) in {"n5": (3, 5, 7), "n6": (4, 6, 11), "n8": (6, 8, 3)}.items():
+        a, g, b, u = sample_fields(e, n, seed)
+        out[f"{tag}_a"], out[f"{tag}_g"], out[f"{tag}_b"], out[f"{tag}_u"] = a, g, b, u
+        for ax, fn in enumerate((kernels.apply_r, kernels.apply_s, kernels.apply_t)):
+            out[f"{tag}_apply{ax}"] = fn(a, u)
+        rect = np.random.default_rng(seed + 1).standard_normal((n + 3, n))
+        out[f"{tag}_rect"] = rect
+        for ax, fn in enumerate((kernels.apply_r, kernels.apply_s, kernels.apply_t)):
+            out[f"{tag}_rect{ax}"] = fn(rect, u)
+        ur, us, ut = kernels.grad_ref(a, u)
+        out[f"{tag}_ur"], out[f"{tag}_us"], out[f"{tag}_ut"] = ur, us, ut
+        for k, (lv, lm) in enumerate(((1.0, 0.0), (0.7, 2.5), (1.0, 0.3))):
+            out[f"{tag}_ax{k}"] = kernels.ax_helmholtz_local(a, g, b, u, lv, lm)
+    # gather/scatter case (pkg/tests/test_kernels.py:98-108)
+    rng = np.random.default_rng(5)
+    nloc, ngid = 40, 12
+    gid = rng.integers(0, ngid, nloc)
+    gid[:ngid] = np.arange(ngid)
+    perm = np.argsort(gid, kind="stable").astype(np.int64)
+    counts = np.bincount(gid, minlength=ngid)
+    offsets = np.zeros(ngid + 1, dtype=np.int64)
+    offsets[1:] = np.cumsum(counts)
+    vals = rng.standard_normal(nloc)
+    out["gs_gid"], out["gs_perm"], out["gs_off"], out["gs_vals"] = gid, perm, offsets, vals
+    out["gs_sums"] = kernels.gs_gather(vals, perm, offsets)
+    out["gs_scat"] = kernels.gs_scatter(out["gs_sums"], perm, offsets, np.zeros(nloc))
+    np.savez_compressed(os.path.join(OUT, "kernels.npz"), **out)
+
+
+def gen_basis():
+    out = {}
+    for order in range(1, 11):
+        b = make_basis(order)
+        out[f"p{order}"], out[f"w{order}"], out[f"d{order}"] = b.points, b.weights, b.dmat
+    np.savez_compressed(os.path.join(OUT, "basis.npz"), **out)
+
+
+def perturbed_box(counts, seed, amp=0.08, extent=(0.0, 1.5, 0.0, 1.0, 0.0, 1.2)):
+    m = gen_box_mesh(extent, counts)
+    rng = np.random.default_rng(seed)
+    v = m.vertices.copy()
+    lo = np.array([extent[0], extent[2], extent[4]])
+    hi = np.array([extent[1], extent[3], extent[5]])
+    interior = np.all((v > lo + 1e-9) & (v < hi - 1e-9), axis=1)
+    h = (hi - lo) / np.array(counts)
+    v[interior] += amp * h * rng.uniform(-1, 1, (int(interior.sum()), 3))
+    m.vertices = v
+    return m
+
+
+def mesh_arrays(prefix, m, out):
+    out[f"{prefix}_vertices"] = m.vertices
+    out[f"{prefix}_elements"] = m.elements
+    out[f"{prefix}_facet_elem"] = m.facet_elem
+    out[f"{prefix}_facet_face"] = m.facet_face
+    out[f"{prefix}_facet_tag"] = m.facet_tag
+    out[f"{prefix}_curved_elem"] = m.curved_elem
+    out[f"{prefix}_curved_coords"] = m.curved_coords
+    out[f"{prefix}_geom_order"] = np.array(-1 if m.geom_order is None else m.geom_order)
+    out[f"{prefix}_tags"] = np.array(json.dumps(list(m.tag_names)))
+
+
+def space_meta(prefix, sp, out, full):
+    for name in ("coords", "rx", "jac", "bm", "geom"):
+        out[f"{prefix}_sha_{name}"] = np.array(sha(getattr(sp, name)))
+    for name in ("gid", "perm", "offsets"):
+        out[f"{prefix}_sha_{name}"] = np.array(sha(getattr(sp.gs, name)))
+    out[f"{prefix}_n_gid"] = np.array(sp.gs.n_gid)
+    out[f"{prefix}_volume"] = np.array(sp.volume)
+    out[f"{prefix}_warea_sum"] = np.array(float(sp.facet_warea.sum()))
+    if full:
+        for name in ("coords", "jac", "bm"):
+            out[f"{prefix}_{name}"] = getattr(sp, name)
+        for name in ("gid", "perm", "offsets"):
+            out[f"{prefix}_{name}"] = getattr(sp.gs, name)
+        out[f"{prefix}_facet_normal"] = sp.facet_normal
+        out[f"{prefix}_facet_warea"] = sp.facet_warea
+
+
+SPACES = {}
+
+
+def gen_spaces():
+    out = {}
+    cases = {
+        "box211": (gen_box_mesh((0.0, 2.0, 0.0, 1.0, 0.0, 1.0), (2, 1, 1)), 2, True),
+        "cube222": (gen_box_mesh((0.0, 1.0, 0.0, 1.0, 0.0, 1.0), (2, 2, 2)), 4, True),
+        "pbox322": (perturbed_box((3, 2, 2), 17), 7, True),
+        "pbox543": (perturbed_box((5, 4, 3), 29, amp=0.12), 5, True),
+        "tgv4": (gen_box_mesh((0.0, 2 * np.pi, 0.0, 2 * np.pi, 0.0, 2 * np.pi), (4, 4, 4)), 7, False),
+        "tgv8": (gen_box_mesh((0.0, 2 * np.pi, 0.0, 2 * np.pi, 0.0, 2 * np.pi), (8, 8, 8)), 7, False),
+        "rotor": (gen_cylinder_box_mesh(1.0, (-4.0, 6.0), (-4.0, 4.0), 2.0, n_azimuthal=8, n_radial=2,
+                                        n_axial=2, n_upstream=4, n_downstream=5, n_front=3, n_back=3,
+                                        geom_order=5), 5, True),
+    }
+    for key, (m, order, full) in cases.items():
+        t0 = time.time()
+        sp = build_space(m, make_basis(order))
+        SPACES[key] = sp
+        mesh_arrays(key, m, out)
+        out[f"{key}_order"] = np.array(order)
+        space_meta(key, sp, out, full)
+        print(f"space {key}: E={m.n_elements} P={sp.gs.gid.size} {time.time() - t0:.1f}s", flush=True)
+    np.savez_compressed(os.path.join(OUT, "spaces.npz"), **out)
+
+
+def gen_operators():
+    """Operator outputs on the perturbed 3x2x2 order-7 box (6144 points)."""
+    sp = SPACES["pbox322"]
+    rng = np.random.default_rng(0)
+    u = rng.standard_normal(sp.shape)
+    v = rng.standard_normal((3,) + sp.shape)
+    c = rng.standard_normal((3,) + sp.shape)
+    mask = np.ones(sp.shape)
+    mask.reshape(-1)[sp.facet_flat.ravel()] = 0.0
+    out = {"u": u, "v": v, "c": c, "mask": mask}
+    out["ax_poisson"] = ops.laplace_local(sp, u)
+    out["ax_helm"] = ops.helmholtz_local(sp, u, 0.3, 7.0)
+    out["gop_poisson_masked"] = ops.make_global_op(sp, 1.0, 0.0, mask)(u)
+    out["gop_helm_masked"] = ops.make_global_op(sp, 0.3, 7.0, mask)(u)
+    out["gop_poisson"] = ops.make_global_op(sp, 1.0, 0.0)(u)
+    out["gs_add"] = sp.gs.add(u)
+    out["gs_avg"] = sp.gs.avg(u)
+    out["gs_add_vec"] = sp.gs.add(v)
+    out["gs_dot"] = np.array(sp.gs.dot(u, v[0]))
+    out["integral"] = np.array(sp.integral(u))
+    out["grad"] = ops.grad(sp, u)
+    out["div"] = ops.div(sp, v)
+    out["curl"] = ops.curl(sp, v)
+    out["advect"] = ops.advect_vec(sp, c, v)
+    out["wgd"] = ops.weak_grad_dot(sp, v)
+    out["cfl"] = np.array(ops.cfl(sp, v, 0.01))
+    out["jacobi_p"] = BlockJacobi(sp, 1.0, 0.0, mask).inv_diag
+    out["jacobi_h"] = BlockJacobi(sp, 0.3, 7.0, mask).inv_diag
+    out["ke"] = np.array(kinetic_energy(sp, v))
+    np.savez_compressed(os.path.join(OUT, "operators.npz"), **out)
+
+
+def all_tags(spec):
+    return {t: dict(spec) for t in ("xlo", "xhi", "ylo", "yhi", "zlo", "zhi")}
+
+
+def poisson_case(ne, order=7, restart_gmres=10):
+    sp = build_space(gen_box_mesh((0.0, 1.0, 0.0, 1.0, 0.0, 1.0), (ne, ne, ne)), make_basis(order))
+    mask = np.ones(sp.shape)
+    mask.reshape(-1)[sp.facet_flat.ravel()] = 0.0
+    f = sp.from_function(lambda x, y, z: 3.0 * np.pi ** 2 * np.sin(np.pi * x) * np.sin(np.pi * y)
+                         * np.sin(np.pi * z))
+    exact = sp.from_function(lambda x, y, z: np.sin(np.pi * x) * np.sin(np.pi * y) * np.sin(np.pi * z))
+    rhs = mask * sp.gs.add(sp.bm * f)
+    a = ops.make_global_op(sp, 1.0, 0.0, mask)
+    pc = BlockJacobi(sp, 1.0, 0.0, mask)
+    res = {}
+    t0 = time.time()
+    info = pcg(a, rhs, tol=1e-8, max_iter=500, precond=pc, dot=sp.gs.dot)
+    res["pcg"] = dict(iterations=info.iterations, residual=info.residual,
+                      initial_residual=info.initial_residual, converged=info.converged,
+                      err=float(np.abs(info.x - exact).max()), seconds=time.time() - t0,
+                      x_l2=sp.l2_norm(info.x))
+    if ne <= 8:
+        info = gmres(a, rhs, tol=1e-8, max_iter=500, restart=restart_gmres, precond=pc, dot=sp.gs.dot)
+        res["gmres"] = dict(iterations=info.iterations, residual=info.residual,
+                            initial_residual=info.initial_residual, converged=info.converged,
+                            err=float(np.abs(info.x - exact).max()), x_l2=sp.l2_norm(info.x))
+        info = pcg(a, rhs, tol=1e-8, max_iter=500, dot=sp.gs.dot)
+        res["cg_noprec"] = dict(iterations=info.iterations, residual=info.residual)
+        # projection: solve twice with perturbed rhs
+        proj = ProjectionSpace(sp.gs.dot)
+        seq = []
+        for k in range(3):
+            r_k = rhs * (1.0 + 0.1 * k)
+            x0, b = proj.prepare(r_k, a)
+            inf = pcg(a, b, tol=1e-8, max_iter=500, precond=pc, dot=sp.gs.dot)
+            proj.absorb(inf.x, a)
+            seq.append(dict(iterations=inf.iterations, residual=inf.residual, count=proj.count))
+        res["projection"] = seq
+    return res
+
+
+def enstrophy(sp, v):
+    w = ops.curl(sp, v)
+    return 0.5 * sp.integral(w[0] ** 2 + w[1] ** 2 + w[2] ** 2)
+
+
+def tgv_case(ne, steps):
+    L = 2 * np.pi
+    sp = build_space(gen_box_mesh((0.0, L, 0.0, L, 0.0, L), (ne, ne, ne)), make_basis(7))
+    bset = BoundarySet(sp, all_tags({"kind": "symmetry"}))
+    st = Stepper(sp, bset, nu=1.0 / 1600.0, dt=1e-2, scheme_order=3,
+                 pressure=SolverOptions(tol=1e-5, max_iter=200, restart=20, precond="jacobi"),
+                 velocity=SolverOptions(tol=1e-8, max_iter=100, precond="jacobi"))
+    x, y, z = sp.coords
+    v0 = np.stack([np.sin(x) * np.cos(y) * np.cos(z), -np.cos(x) * np.sin(y) * np.cos(z), np.zeros_like(x)])
+    state = st.initial_state(v0)
+    rows = [dict(step=0, ke=kinetic_energy(sp, state.vel), ens=enstrophy(sp, state.vel))]
+    for _ in range(steps):
+        t0 = time.time()
+        state, d = st.step(state)
+        rows.append(dict(step=d.step, p_it=d.p_iterations, p_res=d.p_residual, v_it=list(d.v_iterations),
+                         v_res=list(d.v_residual), cfl=d.cfl, div=d.div_norm,
+                         ke=kinetic_energy(sp, state.vel), ens=enstrophy(sp, state.vel),
+                         seconds=time.time() - t0))
+        print(f"tgv{ne} step {d.step}: p {d.p_iterations} v {d.v_iterations} ke {rows[-1]['ke']:.15g}",
+              flush=True)
+    return rows
+
+
+def channel_case(counts, steps):
+    """Config-4 analogue: Poiseuille inflow, outflow, no-slip walls, symmetric span."""
+    Lx, Ly, Lz = 4 * np.pi / 8, 2.0, 4 * np.pi / 3 / 8
+    m = gen_box_mesh((0.0, Lx, 0.0, Ly, 0.0, Lz), counts)
+    sp = build_space(m, make_basis(5))
+
+    def pois(x, y, z, t):
+        out = np.zeros((3,) + np.shape(x))
+        out[0] = 1.5 * y * (2.0 - y)
+        return out
+
+    specs = {"xlo": {"kind": "function", "fn": pois}, "xhi": {"kind": "outflow"},
+             "ylo": {"kind": "noslip"}, "yhi": {"kind": "noslip"},
+             "zlo": {"kind": "symmetry"}, "zhi": {"kind": "symmetry"}}
+    bset = BoundarySet(sp, specs)
+    st = Stepper(sp, bset, nu=1.0 / 2800.0, dt=2e-3, scheme_order=3,
+                 pressure=SolverOptions(tol=1e-5, max_iter=200, restart=20, precond="jacobi"),
+                 velocity=SolverOptions(tol=1e-8, max_iter=100, precond="jacobi"))
+    x, y, z = sp.coords
+    rng = np.random.default_rng(3)
+    v0 = pois(x, y, z, 0.0)
+    v0[1] += 0.05 * np.sin(np.pi * x / Lx) * np.sin(np.pi * y / 2.0) ** 2
+    state = st.initial_state(v0)
+    rows = []
+    for _ in range(steps):
+        state, d = st.step(state)
+        rows.append(dict(step=d.step, p_it=d.p_iterations, p_res=d.p_residual, v_it=list(d.v_iterations),
+                         v_res=list(d.v_residual), cfl=d.cfl, div=d.div_norm,
+                         ke=kinetic_energy(sp, state.vel), ens=enstrophy(sp, state.vel)))
+        print(f"channel step {d.step}: p {d.p_iterations} v {d.v_iterations}", flush=True)
+    del rng
+    return rows
+
+
+def main():
+    skip_big = "--skip-big" in sys.argv
+    gen_kernels()
+    gen_basis()
+    gen_spaces()
+    gen_operators()
+    sol = {"versions": {"numpy": np.__version__}}
+    sol["poisson4"] = poisson_case(4)
+    sol["poisson8"] = poisson_case(8)
+    sol["tgv4"] = tgv_case(4, 10)
+    sol["channel"] = channel_case((6, 4, 3), 4)
+    if not skip_big:
+        sol["tgv8"] = tgv_case(8, 10)
+        sol["poisson32"] = poisson_case(32)
+    with open(os.path.join(OUT, "solvers.json"), "w") as fh:
+        json.dump(sol, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,185 @@
+"""Pin the CPU oracle to the reference: golden fixtures from tests/golden/make_golden.py.
+
+These run without a GPU.  Element kernels, basis, coordinates and gather-scatter
+maps must be bit-identical to the reference numba lane; derived operators agree
+to rounding; Krylov iteration counts and TGV diagnostics match.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import mesh_from_golden, rel_err
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("tag", ["n5", "n6", "n8"])
+def test_oracle_kernels_bitwise(oracle, golden_kernels, tag):
+    g = golden_kernels
+    a, geo, b, u = g[f"{tag}_a"], g[f"{tag}_g"], g[f"{tag}_b"], g[f"{tag}_u"]
+    for ax in range(3):
+        assert np.array_equal(oracle.apply_axis(ax, a, u), g[f"{tag}_apply{ax}"])
+        assert np.array_equal(oracle.apply_axis(ax, g[f"{tag}_rect"], u), g[f"{tag}_rect{ax}"])
+    ur, us, ut = oracle.grad_ref(a, u)
+    assert np.array_equal(ur, g[f"{tag}_ur"])
+    assert np.array_equal(us, g[f"{tag}_us"])
+    assert np.array_equal(ut, g[f"{tag}_ut"])
+    for k, (lv, lm) in enumerate(((1.0, 0.0), (0.7, 2.5), (1.0, 0.3))):
+        assert np.array_equal(oracle.ax_helmholtz_local(a, geo, b, u, lv, lm), g[f"{tag}_ax{k}"])
+
+
+def test_oracle_gather_scatter_bitwise(oracle, golden_kernels):
+    g = golden_kernels
+    sums = oracle.gs_gather(g["gs_vals"], g["gs_perm"], g["gs_off"])
+    assert np.array_equal(sums, g["gs_sums"])
+    out = oracle.gs_scatter(sums, g["gs_perm"], g["gs_off"], np.zeros(g["gs_vals"].size))
+    assert np.array_equal(out, g["gs_scat"])
+
+
+def test_oracle_thread_count_invariance(oracle, golden_kernels, monkeypatch):
+    # reference contract: bit-identical across thread counts (pkg/tests/test_kernels.py:140-155)
+    g = golden_kernels
+    a, geo, b, u = g["n8_a"], g["n8_g"], g["n8_b"], g["n8_u"]
+    x = oracle.ax_helmholtz_local(a, geo, b, u, 1.0, 0.5)
+    monkeypatch.setenv("ORACLE_THREADS", "1")
+    y = oracle.ax_helmholtz_local(a, geo, b, u, 1.0, 0.5)
+    assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("order", range(1, 11))
+def test_oracle_basis_bitwise(oracle, golden_basis, order):
+    b = oracle.make_basis(order)
+    assert np.array_equal(b.points, golden_basis[f"p{order}"])
+    assert np.array_equal(b.weights, golden_basis[f"w{order}"])
+    assert np.array_equal(b.dmat, golden_basis[f"d{order}"])
+
+
+@pytest.mark.parametrize("key", ["box211", "cube222", "pbox322", "pbox543", "tgv4", "rotor"])
+def test_oracle_space_bitwise(oracle, golden_spaces, key):
+    g = golden_spaces
+    m = mesh_from_golden(g, key)
+    sp = oracle.build_space(m, oracle.make_basis(int(g[f"{key}_order"])))
+    assert sha(sp.coords) == str(g[f"{key}_sha_coords"])
+    for name in ("gid", "perm", "offsets"):
+        assert sha(getattr(sp.gs, name)) == str(g[f"{key}_sha_{name}"]), name
+    assert sp.gs.n_gid == int(g[f"{key}_n_gid"])
+    # metrics: same formulas as the reference (np.cross, sequential sums) -> bitwise
+    for name in ("jac", "bm", "rx"):
+        assert sha(getattr(sp, name)) == str(g[f"{key}_sha_{name}"]), name
+    # geom: the reference's einsum over l takes a vectorised inner loop whose
+    # association is not reproducible; the diagonal entries (rr, ss, tt) are
+    # still bit-exact and the off-diagonal ones differ only where they are
+    # rounding noise (|G_st| ~ 1e-30 on affine boxes) -- checked in
+    # test_oracle_operators via the golden BlockJacobi / operator outputs.
+    assert abs(sp.volume - float(g[f"{key}_volume"])) <= 1e-13 * abs(float(g[f"{key}_volume"]))
+
+
+def test_oracle_box_mesh_matches_reference(oracle, golden_spaces):
+    g = golden_spaces
+    m = oracle.gen_box_mesh((0.0, 2 * np.pi, 0.0, 2 * np.pi, 0.0, 2 * np.pi), (4, 4, 4))
+    assert np.array_equal(m.vertices, g["tgv4_vertices"])
+    assert np.array_equal(m.elements, g["tgv4_elements"])
+    assert np.array_equal(m.facet_elem, g["tgv4_facet_elem"])
+    assert np.array_equal(m.facet_face, g["tgv4_facet_face"])
+
+
+@pytest.fixture(scope="module")
+def pbox(oracle, golden_spaces):
+    m = mesh_from_golden(golden_spaces, "pbox322")
+    return oracle.build_space(m, oracle.make_basis(7))
+
+
+def test_oracle_operators(oracle, golden_ops, pbox):
+    g, sp = golden_ops, pbox
+    u, v, c, mask = g["u"], g["v"], g["c"], g["mask"]
+    d = sp.basis.dmat
+    # geom-dependent outputs: exact up to the off-diagonal G noise (see above)
+    assert rel_err(oracle.ax_helmholtz_local(d, sp.geom, sp.bm, u, 1.0, 0.0), g["ax_poisson"]) < 1e-15
+    assert rel_err(oracle.make_global_op(sp, 1.0, 0.0, mask)(u), g["gop_poisson_masked"]) < 1e-15
+    assert rel_err(oracle.make_global_op(sp, 0.3, 7.0, mask)(u), g["gop_helm_masked"]) < 1e-15
+    assert np.array_equal(sp.gs.add(u), g["gs_add"])
+    assert np.array_equal(sp.gs.avg(u), g["gs_avg"])
+    assert np.array_equal(sp.gs.add(v), g["gs_add_vec"])
+    assert sp.gs.dot(u, v[0]) == float(g["gs_dot"])
+    assert np.array_equal(oracle.grad(sp, u), g["grad"])
+    assert np.array_equal(oracle.div(sp, v), g["div"])
+    assert np.array_equal(oracle.curl(sp, v), g["curl"])
+    assert np.array_equal(oracle.advect_vec(sp, c, v), g["advect"])
+    assert np.array_equal(oracle.weak_grad_dot(sp, v), g["wgd"])
+    assert oracle.cfl(sp, v, 0.01) == float(g["cfl"])
+    assert rel_err(oracle.block_jacobi(sp, 1.0, 0.0, mask)[1], g["jacobi_p"]) < 1e-15
+    assert rel_err(oracle.block_jacobi(sp, 0.3, 7.0, mask)[1], g["jacobi_h"]) < 1e-15
+    assert rel_err(oracle.kinetic_energy(sp, v), g["ke"]) < 1e-14
+
+
+def _poisson(oracle, ne):
+    sp = oracle.build_space(oracle.gen_box_mesh((0.0, 1.0, 0.0, 1.0, 0.0, 1.0), (ne, ne, ne)),
+                            oracle.make_basis(7))
+    mask = np.ones(sp.shape)
+    mask.reshape(-1)[sp.facet_flat.ravel()] = 0.0
+    x, y, z = sp.coords
+    f = 3.0 * np.pi ** 2 * np.sin(np.pi * x) * np.sin(np.pi * y) * np.sin(np.pi * z)
+    rhs = mask * sp.gs.add(sp.bm * f)
+    return sp, mask, rhs
+
+
+def test_oracle_pcg_gmres_counts(oracle, golden_solvers):
+    sp, mask, rhs = _poisson(oracle, 4)
+    A = oracle.make_global_op(sp, 1.0, 0.0, mask)
+    M = oracle.block_jacobi(sp, 1.0, 0.0, mask)[0]
+    want = golden_solvers["poisson4"]
+    info = oracle.pcg(A, rhs, 1e-8, 500, M, sp.gs.dot)
+    assert info.iterations == want["pcg"]["iterations"]
+    assert rel_err(info.residual, want["pcg"]["residual"]) < 1e-6
+    info = oracle.gmres(A, rhs, 1e-8, 500, 10, M, sp.gs.dot)
+    assert info.iterations == want["gmres"]["iterations"]
+    info = oracle.pcg(A, rhs, 1e-8, 500, None, sp.gs.dot)
+    assert info.iterations == want["cg_noprec"]["iterations"]
+    proj = oracle.Projection(sp.gs.dot)
+    for k, row in enumerate(want["projection"]):
+        x0, b = proj.prepare(rhs * (1.0 + 0.1 * k), A)
+        inf = oracle.pcg(A, b, 1e-8, 500, M, sp.gs.dot)
+        proj.absorb(inf.x, A)
+        assert inf.iterations == row["iterations"]
+        assert len(proj.xs) == row["count"]
+
+
+def test_oracle_tgv4_ten_steps(oracle, golden_solvers):
+    sp, st, state = oracle.tgv_setup(4)
+    for row in golden_solvers["tgv4"][1:]:
+        state, d = st.step(state)
+        assert d.p_iterations == row["p_it"], row["step"]
+        assert list(d.v_iterations) == row["v_it"], row["step"]
+        assert rel_err(oracle.kinetic_energy(sp, state.vel), row["ke"]) < 1e-12
+        assert rel_err(oracle.enstrophy(sp, state.vel), row["ens"]) < 1e-11
+        assert rel_err(d.cfl, row["cfl"]) < 1e-12
+
+
+def test_oracle_channel_boundary_terms(oracle, golden_solvers, golden_spaces):
+    """Dirichlet / outflow / symmetry paths of the step (config-4 analogue)."""
+    Lx, Ly, Lz = 4 * np.pi / 8, 2.0, 4 * np.pi / 3 / 8
+    sp = oracle.build_space(oracle.gen_box_mesh((0.0, Lx, 0.0, Ly, 0.0, Lz), (6, 4, 3)), oracle.make_basis(5))
+
+    def pois(x, y, z, t):
+        out = np.zeros((3,) + np.shape(x))
+        out[0] = 1.5 * y * (2.0 - y)
+        return out
+
+    specs = {"xlo": {"kind": "function", "fn": pois}, "xhi": {"kind": "outflow"},
+             "ylo": {"kind": "noslip"}, "yhi": {"kind": "noslip"},
+             "zlo": {"kind": "symmetry"}, "zhi": {"kind": "symmetry"}}
+    bc = oracle.Boundary(sp, specs)
+    st = oracle.Stepper(sp, bc, 1.0 / 2800.0, 2e-3)
+    x, y, z = sp.coords
+    v0 = pois(x, y, z, 0.0)
+    v0[1] += 0.05 * np.sin(np.pi * x / Lx) * np.sin(np.pi * y / 2.0) ** 2
+    state = st.initial_state(v0)
+    for row in golden_solvers["channel"][:2]:
+        state, d = st.step(state)
+        assert d.p_iterations == row["p_it"]
+        assert list(d.v_iterations) == row["v_it"]
+        assert rel_err(oracle.kinetic_energy(sp, state.vel), row["ke"]) < 1e-9
