@@ -50,8 +50,21 @@ __device__ __forceinline__ bool mask_bit(const uint32_t* __restrict__ m, long lo
 // K1.  w = lam_visc * D^T G D um + lam_mass * B um, um = inmask ? u : 0.
 // With MASK, the written value is w where outsel is set and u elsewhere
 // (outsel = mask | shared: shared points are finalised by the dssum kernel).
+//
+// Register budget: the layer loops are not fully unrolled (SF_AX_UNROLL) so the
+// live state per thread is the u pencil, one layer of G (plus the prefetched next
+// layer) and the thread's two rows of D -- ~80-100 registers, 5-6 blocks (20-24
+// warps) per SM, enough loads in flight to cover HBM latency.  f1, f2, f3 live in
+// shared memory (4 element volumes, 16 KB per element at n = 8).
+#ifndef SF_AX_MINB
+#define SF_AX_MINB 5
+#endif
+#ifndef SF_AX_UNROLL
+#define SF_AX_UNROLL 2
+#endif
+constexpr int kAxUnroll = SF_AX_UNROLL;
 template <int N, bool EX, bool MASK>
-__global__ void __launch_bounds__(AxCfg<N>::THREADS)
+__global__ void __launch_bounds__(AxCfg<N>::THREADS, (N == 8 ? SF_AX_MINB : 1))
 ax_helm_kernel(DMat<N> D, const double* __restrict__ g, const double* __restrict__ b,
                const double* __restrict__ u, double* __restrict__ w, long long E, double lv,
                double lm, const uint32_t* __restrict__ inmask,
@@ -59,6 +72,7 @@ ax_helm_kernel(DMat<N> D, const double* __restrict__ g, const double* __restrict
   using C = AxCfg<N>;
   constexpr int NN = C::NN, NNN = C::NNN;
   __shared__ double us_[C::EPB][NNN];
+  __shared__ double f1s[C::EPB][NNN];
   __shared__ double f2s[C::EPB][NNN];
   __shared__ double f3s[C::EPB][NNN];
 
@@ -70,15 +84,15 @@ ax_helm_kernel(DMat<N> D, const double* __restrict__ g, const double* __restrict
   const long long base = e * NNN + t;
   const long long gstride = E * (long long)NNN;
 
-  double up[N];   // original pencil (kept for the masked output select)
   double um[N];   // masked pencil the operator acts on
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    up[i] = active ? __ldg(u + base + i * NN) : 0.0;
-    bool in = true;
-    if constexpr (MASK) in = active && mask_bit(inmask, e, C::WPE, i * NN + t);
-    um[i] = in ? up[i] : 0.0;
-    us_[le][i * NN + t] = um[i];
+    double uv = active ? __ldg(u + base + i * NN) : 0.0;
+    if constexpr (MASK) {
+      if (!(active && mask_bit(inmask, e, C::WPE, i * NN + t))) uv = 0.0;
+    }
+    um[i] = uv;
+    us_[le][i * NN + t] = uv;
   }
   double dj[N], dk[N];
 #pragma unroll
@@ -86,11 +100,22 @@ ax_helm_kernel(DMat<N> D, const double* __restrict__ g, const double* __restrict
     dj[q] = D.v[j * N + q];
     dk[q] = D.v[k * N + q];
   }
+  // G of layer 0 in flight while the block synchronises
+  const double* gp = g + (active ? base : 0);
+  double gn[6];
+#pragma unroll
+  for (int m = 0; m < 6; ++m) gn[m] = active ? __ldg(gp + m * gstride) : 0.0;
   __syncthreads();
 
-  double f1[N];
-#pragma unroll
+#pragma unroll (kAxUnroll)
   for (int i = 0; i < N; ++i) {
+    double gc[6];
+#pragma unroll
+    for (int m = 0; m < 6; ++m) gc[m] = gn[m];
+    if (i + 1 < N) {
+#pragma unroll
+      for (int m = 0; m < 6; ++m) gn[m] = active ? __ldg(gp + (i + 1) * NN + m * gstride) : 0.0;
+    }
     double ar = 0.0, as = 0.0, at = 0.0;
 #pragma unroll
     for (int q = 0; q < N; ++q) {
@@ -98,20 +123,10 @@ ax_helm_kernel(DMat<N> D, const double* __restrict__ g, const double* __restrict
       as = mac<EX>(as, dj[q], us_[le][i * NN + q * N + k]);
       at = mac<EX>(at, dk[q], us_[le][i * NN + j * N + q]);
     }
-    double g0 = 0, g1 = 0, g2 = 0, g3 = 0, g4 = 0, g5 = 0;
-    if (active) {
-      const double* gp = g + base + i * NN;
-      g0 = __ldg(gp);
-      g1 = __ldg(gp + gstride);
-      g2 = __ldg(gp + 2 * gstride);
-      g3 = __ldg(gp + 3 * gstride);
-      g4 = __ldg(gp + 4 * gstride);
-      g5 = __ldg(gp + 5 * gstride);
-    }
     // (g0*gr + g1*gs) + g2*gt, as written in _numba.py:116-118
-    f1[i] = add<EX>(add<EX>(mul<EX>(g0, ar), mul<EX>(g1, as)), mul<EX>(g2, at));
-    f2s[le][i * NN + t] = add<EX>(add<EX>(mul<EX>(g1, ar), mul<EX>(g3, as)), mul<EX>(g4, at));
-    f3s[le][i * NN + t] = add<EX>(add<EX>(mul<EX>(g2, ar), mul<EX>(g4, as)), mul<EX>(g5, at));
+    f1s[le][i * NN + t] = add<EX>(add<EX>(mul<EX>(gc[0], ar), mul<EX>(gc[1], as)), mul<EX>(gc[2], at));
+    f2s[le][i * NN + t] = add<EX>(add<EX>(mul<EX>(gc[1], ar), mul<EX>(gc[3], as)), mul<EX>(gc[4], at));
+    f3s[le][i * NN + t] = add<EX>(add<EX>(mul<EX>(gc[2], ar), mul<EX>(gc[4], as)), mul<EX>(gc[5], at));
   }
 #pragma unroll
   for (int q = 0; q < N; ++q) {  // columns of D for the transposed contraction
@@ -122,21 +137,179 @@ ax_helm_kernel(DMat<N> D, const double* __restrict__ g, const double* __restrict
   if (!active) return;
 
   const bool mass = lm != 0.0;
-#pragma unroll
+#pragma unroll (kAxUnroll)
   for (int i = 0; i < N; ++i) {
     double acc = 0.0;
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-      acc = mac<EX>(acc, D.v[q * N + i], f1[q]);
+      acc = mac<EX>(acc, D.v[q * N + i], f1s[le][q * NN + t]);
       acc = mac<EX>(acc, dj[q], f2s[le][i * NN + q * N + k]);
       acc = mac<EX>(acc, dk[q], f3s[le][i * NN + j * N + q]);
     }
     double wv = mul<EX>(lv, acc);
-    if (mass) wv = add<EX>(wv, mul<EX>(mul<EX>(lm, __ldg(b + base + i * NN)), um[i]));
+    if (mass) wv = add<EX>(wv, mul<EX>(mul<EX>(lm, __ldg(b + base + i * NN)), us_[le][i * NN + t]));
     if constexpr (MASK) {
-      if (!mask_bit(outsel, e, C::WPE, i * NN + t)) wv = up[i];
+      // unselected points (masked, unshared) return the operator input
+      if (!mask_bit(outsel, e, C::WPE, i * NN + t)) wv = __ldg(u + base + i * NN);
     }
     w[base + i * NN] = wv;
+  }
+}
+
+// K1 for n = 8, register-blocked.  One warp owns one element; lane (j, kk)
+// owns the two r-pencils (j, 2kk) and (j, 2kk+1).  All global accesses are
+// 16-byte vectors (a warp moves one 512 B element layer per instruction); the
+// s-derivative value pair and the t-derivative row are read from shared memory
+// once for both pencils, cutting shared-memory wavefronts ~4x against the
+// one-pencil kernel; f1 (r-component) stays in registers.  Each element is
+// private to its warp, so __syncwarp replaces block barriers.  Per-point
+// arithmetic and accumulation order are identical to ax_helm_kernel.
+#ifndef SF_AX8_MINB
+#define SF_AX8_MINB 3
+#endif
+#ifndef SF_AX8_EPB
+#define SF_AX8_EPB 4
+#endif
+constexpr int AX8_EPB = SF_AX8_EPB;  // elements (warps) per block
+// keeps the scheduler from hoisting every layer's loads to the top of the fully
+// unrolled loop (which would need ~250 registers)
+#ifndef SF_NO_LAYER_FENCE
+#define SF_LAYER_FENCE() asm volatile("" ::: "memory")
+#else
+#define SF_LAYER_FENCE()
+#endif
+
+template <bool EX, bool MASK>
+__global__ void __launch_bounds__(32 * AX8_EPB, SF_AX8_MINB)
+ax_helm_n8_kernel(DMat<8> D, const double* __restrict__ g, const double* __restrict__ b,
+                  const double* __restrict__ u, double* __restrict__ w, long long E, double lv,
+                  double lm, const uint32_t* __restrict__ inmask,
+                  const uint32_t* __restrict__ outsel) {
+  constexpr int N = 8, NN = 64, NNN = 512;
+  // us_ holds the element's (masked) u; layer i is overwritten by f3 once every
+  // lane of the warp is past layer i (the t-derivative of layer i reads only
+  // layer i), so two element volumes suffice
+  __shared__ __align__(16) double us_[AX8_EPB][NNN];
+  __shared__ __align__(16) double f2s[AX8_EPB][NNN];
+  __shared__ __align__(16) double Dr[NN];   // D, row-major
+  __shared__ __align__(16) double Dc[NN];   // D^T, row-major (columns of D)
+  for (int x = threadIdx.x; x < NN; x += blockDim.x) {
+    Dr[x] = D.v[x];
+    Dc[x] = D.v[(x & 7) * N + (x >> 3)];
+  }
+  __syncthreads();
+  const int le = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int j = lane >> 2, k0 = (lane & 3) * 2;
+  const long long e = (long long)blockIdx.x * AX8_EPB + le;
+  if (e >= E) return;  // whole warp exits together (no block barrier below)
+  const long long base = e * NNN + j * N + k0;
+  const long long gstride = E * (long long)NNN;
+  const int wsel = j >> 2, bsh = (j & 3) * 8 + k0;  // mask word offset / bit within a layer
+  double* su = us_[le];
+  double* s2 = f2s[le];
+  double* s3 = us_[le];
+
+  double um0[N], um1[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double2 v = __ldg(reinterpret_cast<const double2*>(u + base + i * NN));
+    if constexpr (MASK) {
+      const uint32_t wd = __ldg(inmask + e * 16 + 2 * i + wsel) >> bsh;
+      if (!(wd & 1u)) v.x = 0.0;
+      if (!(wd & 2u)) v.y = 0.0;
+    }
+    um0[i] = v.x;
+    um1[i] = v.y;
+    *reinterpret_cast<double2*>(su + i * NN + j * N + k0) = v;
+  }
+  double dj[N];
+#pragma unroll
+  for (int q = 0; q < N; ++q) dj[q] = D.v[j * N + q];
+  __syncwarp();
+
+  double f10[N], f11[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const double* gp = g + base + i * NN;
+    double2 gv[6];
+#pragma unroll
+    for (int m = 0; m < 6; ++m) gv[m] = __ldg(reinterpret_cast<const double2*>(gp + m * gstride));
+    double ar0 = 0.0, ar1 = 0.0, as0 = 0.0, as1 = 0.0, at0 = 0.0, at1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      ar0 = mac<EX>(ar0, D.v[i * N + q], um0[q]);
+      ar1 = mac<EX>(ar1, D.v[i * N + q], um1[q]);
+      const double2 sv = *reinterpret_cast<const double2*>(su + i * NN + q * N + k0);
+      as0 = mac<EX>(as0, dj[q], sv.x);
+      as1 = mac<EX>(as1, dj[q], sv.y);
+    }
+#pragma unroll
+    for (int q = 0; q < N; q += 2) {
+      const double2 tv = *reinterpret_cast<const double2*>(su + i * NN + j * N + q);
+      const double2 da = *reinterpret_cast<const double2*>(Dr + k0 * N + q);
+      const double2 db = *reinterpret_cast<const double2*>(Dr + (k0 + 1) * N + q);
+      at0 = mac<EX>(at0, da.x, tv.x);
+      at1 = mac<EX>(at1, db.x, tv.x);
+      at0 = mac<EX>(at0, da.y, tv.y);
+      at1 = mac<EX>(at1, db.y, tv.y);
+    }
+    f10[i] = add<EX>(add<EX>(mul<EX>(gv[0].x, ar0), mul<EX>(gv[1].x, as0)), mul<EX>(gv[2].x, at0));
+    f11[i] = add<EX>(add<EX>(mul<EX>(gv[0].y, ar1), mul<EX>(gv[1].y, as1)), mul<EX>(gv[2].y, at1));
+    double2 v2, v3;
+    v2.x = add<EX>(add<EX>(mul<EX>(gv[1].x, ar0), mul<EX>(gv[3].x, as0)), mul<EX>(gv[4].x, at0));
+    v2.y = add<EX>(add<EX>(mul<EX>(gv[1].y, ar1), mul<EX>(gv[3].y, as1)), mul<EX>(gv[4].y, at1));
+    v3.x = add<EX>(add<EX>(mul<EX>(gv[2].x, ar0), mul<EX>(gv[4].x, as0)), mul<EX>(gv[5].x, at0));
+    v3.y = add<EX>(add<EX>(mul<EX>(gv[2].y, ar1), mul<EX>(gv[4].y, as1)), mul<EX>(gv[5].y, at1));
+    *reinterpret_cast<double2*>(s2 + i * NN + j * N + k0) = v2;
+    __syncwarp();   // every lane has read u layer i
+    *reinterpret_cast<double2*>(s3 + i * NN + j * N + k0) = v3;
+  }
+#pragma unroll
+  for (int q = 0; q < N; ++q) dj[q] = D.v[q * N + j];  // column j of D
+  __syncwarp();
+
+  const bool mass = lm != 0.0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < N; q += 2) {
+      const double2 t3 = *reinterpret_cast<const double2*>(s3 + i * NN + j * N + q);
+      const double2 ca = *reinterpret_cast<const double2*>(Dc + k0 * N + q);        // D[q..q+1][k0]
+      const double2 cb = *reinterpret_cast<const double2*>(Dc + (k0 + 1) * N + q);  // D[q..q+1][k0+1]
+      const double2 sa = *reinterpret_cast<const double2*>(s2 + i * NN + q * N + k0);
+      const double2 sb = *reinterpret_cast<const double2*>(s2 + i * NN + (q + 1) * N + k0);
+      acc0 = mac<EX>(acc0, D.v[q * N + i], f10[q]);
+      acc1 = mac<EX>(acc1, D.v[q * N + i], f11[q]);
+      acc0 = mac<EX>(acc0, dj[q], sa.x);
+      acc1 = mac<EX>(acc1, dj[q], sa.y);
+      acc0 = mac<EX>(acc0, ca.x, t3.x);
+      acc1 = mac<EX>(acc1, cb.x, t3.x);
+      acc0 = mac<EX>(acc0, D.v[(q + 1) * N + i], f10[q + 1]);
+      acc1 = mac<EX>(acc1, D.v[(q + 1) * N + i], f11[q + 1]);
+      acc0 = mac<EX>(acc0, dj[q + 1], sb.x);
+      acc1 = mac<EX>(acc1, dj[q + 1], sb.y);
+      acc0 = mac<EX>(acc0, ca.y, t3.y);
+      acc1 = mac<EX>(acc1, cb.y, t3.y);
+    }
+    double2 wv;
+    wv.x = mul<EX>(lv, acc0);
+    wv.y = mul<EX>(lv, acc1);
+    if (mass) {
+      const double2 bv = __ldg(reinterpret_cast<const double2*>(b + base + i * NN));
+      wv.x = add<EX>(wv.x, mul<EX>(mul<EX>(lm, bv.x), um0[i]));
+      wv.y = add<EX>(wv.y, mul<EX>(mul<EX>(lm, bv.y), um1[i]));
+    }
+    if constexpr (MASK) {
+      const uint32_t sel = __ldg(outsel + e * 16 + 2 * i + wsel) >> bsh;
+      if ((sel & 3u) != 3u) {
+        const double2 uv = __ldg(reinterpret_cast<const double2*>(u + base + i * NN));
+        if (!(sel & 1u)) wv.x = uv.x;
+        if (!(sel & 2u)) wv.y = uv.y;
+      }
+    }
+    *reinterpret_cast<double2*>(w + base + i * NN) = wv;
   }
 }
 
@@ -237,6 +410,19 @@ static int launch_ax(const double* d_host, const double* g, const double* b, con
   DMat<N> D = load_dmat<N>(d_host);
   dim3 grid((unsigned)((E + C::EPB - 1) / C::EPB));
   const bool masked = inmask != nullptr;
+  if constexpr (N == 8) {
+#ifdef SF_AX_REGBLOCK8
+    dim3 g8((unsigned)((E + AX8_EPB - 1) / AX8_EPB));
+    if (exact) {
+      if (masked) ax_helm_n8_kernel<true, true><<<g8, 32 * AX8_EPB, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel);
+      else ax_helm_n8_kernel<true, false><<<g8, 32 * AX8_EPB, 0, st>>>(D, g, b, u, w, E, lv, lm, nullptr, nullptr);
+    } else {
+      if (masked) ax_helm_n8_kernel<false, true><<<g8, 32 * AX8_EPB, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel);
+      else ax_helm_n8_kernel<false, false><<<g8, 32 * AX8_EPB, 0, st>>>(D, g, b, u, w, E, lv, lm, nullptr, nullptr);
+    }
+    return check_launch("ax_helm_n8");
+#endif
+  }
   if (exact) {
     if (masked) ax_helm_kernel<N, true, true><<<grid, C::THREADS, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel);
     else ax_helm_kernel<N, true, false><<<grid, C::THREADS, 0, st>>>(D, g, b, u, w, E, lv, lm, nullptr, nullptr);

@@ -16,7 +16,7 @@ def assembled_diagonal(space, lam_visc, lam_mass):
     from 0.0 -- the order numpy's einsum uses -- so the result is bit-identical
     to the reference.
     """
-    d = torch.from_numpy(space.dmat).to(space.device)
+    d = torch.tensor(space.dmat, dtype=torch.float64, device=space.device)
     g = space.geom
     n = space.n
     d2 = d * d

@@ -76,15 +76,22 @@ class GatherScatter:
         if counts.numel() and int(counts.max()) > 255:
             raise TopologyError("a global id has more than 255 local copies")
         self.mult8 = counts[gid].to(torch.uint8).contiguous()
-        cnt_pos = torch.repeat_interleave(counts, counts)   # count of the gid at each perm slot
-        sel = cnt_pos > 1
-        shared_gid = counts > 1
-        self.n_shared = int(shared_gid.sum())
-        self.sh_perm = perm[sel].to(torch.int32).contiguous()
-        sh_counts = counts[shared_gid]
+        # shared gids (multiplicity > 1), processed in the order of their lowest
+        # local copy: consecutive threads of the dssum kernel then touch
+        # neighbouring memory (the per-gid summation order is unaffected)
+        shared_g = torch.nonzero(counts > 1).view(-1)
+        self.n_shared = int(shared_g.numel())
+        first = perm[offsets[shared_g]]
+        g_sorted = shared_g[torch.argsort(first)]
+        cnt = counts[g_sorted]
         self.sh_off = torch.zeros(self.n_shared + 1, dtype=torch.int32, device=self.device)
         if self.n_shared:
-            self.sh_off[1:] = torch.cumsum(sh_counts, 0).to(torch.int32)
+            self.sh_off[1:] = torch.cumsum(cnt, 0).to(torch.int32)
+        total = int(cnt.sum()) if self.n_shared else 0
+        start = torch.repeat_interleave(offsets[g_sorted], cnt)
+        within = torch.arange(total, device=self.device) - torch.repeat_interleave(
+            self.sh_off[:-1].to(torch.int64), cnt)
+        self.sh_perm = perm[start + within].to(torch.int32).contiguous()
         E = self.shape[0]
         nnn = P // E if E else 0
         self.shared_bits = pack_bits((self.mult8 > 1).view(E, nnn)) if E else None
@@ -423,8 +430,8 @@ def _facets(mesh, basis, coords, dev):
     if F == 0:
         return flat_t, torch.zeros((0, n, n, 3), dtype=torch.float64, device=dev), \
             torch.zeros((0, n, n), dtype=torch.float64, device=dev)
-    d = torch.from_numpy(np.ascontiguousarray(basis.dmat)).to(dev)
-    w = torch.from_numpy(np.ascontiguousarray(basis.weights)).to(dev)
+    d = torch.tensor(np.asarray(basis.dmat), dtype=torch.float64, device=dev)
+    w = torch.tensor(np.asarray(basis.weights), dtype=torch.float64, device=dev)
     fx = coords.reshape(3, -1)[:, flat_t]                              # (3, F, n, n)
     ta = torch.einsum("ab,lfbc->lfac", d, fx)
     tb = torch.einsum("ab,lfcb->lfca", d, fx)

@@ -208,7 +208,7 @@ def all_tags(spec):
     return {t: dict(spec) for t in ("xlo", "xhi", "ylo", "yhi", "zlo", "zhi")}
 
 
-def poisson_case(ne, order=7, restart_gmres=10):
+def poisson_case(ne, order=7, restart_gmres=20):
     sp = build_space(gen_box_mesh((0.0, 1.0, 0.0, 1.0, 0.0, 1.0), (ne, ne, ne)), make_basis(order))
     mask = np.ones(sp.shape)
     mask.reshape(-1)[sp.facet_flat.ravel()] = 0.0
@@ -308,6 +308,20 @@ def channel_case(counts, steps):
 
 
 def main():
+    if "--update" in sys.argv:
+        # recompute selected solver entries only: --update poisson4 poisson8 ...
+        keys = sys.argv[sys.argv.index("--update") + 1:]
+        path = os.path.join(OUT, "solvers.json")
+        with open(path) as fh:
+            sol = json.load(fh)
+        for k in keys:
+            if k.startswith("poisson"):
+                sol[k] = poisson_case(int(k[len("poisson"):]))
+            elif k.startswith("tgv"):
+                sol[k] = tgv_case(int(k[3:]), 10)
+        with open(path, "w") as fh:
+            json.dump(sol, fh, indent=1)
+        return
     skip_big = "--skip-big" in sys.argv
     gen_kernels()
     gen_basis()

@@ -135,7 +135,7 @@ def test_oracle_pcg_gmres_counts(oracle, golden_solvers):
     info = oracle.pcg(A, rhs, 1e-8, 500, M, sp.gs.dot)
     assert info.iterations == want["pcg"]["iterations"]
     assert rel_err(info.residual, want["pcg"]["residual"]) < 1e-6
-    info = oracle.gmres(A, rhs, 1e-8, 500, 10, M, sp.gs.dot)
+    info = oracle.gmres(A, rhs, 1e-8, 500, 20, M, sp.gs.dot)
     assert info.iterations == want["gmres"]["iterations"]
     info = oracle.pcg(A, rhs, 1e-8, 500, None, sp.gs.dot)
     assert info.iterations == want["cg_noprec"]["iterations"]

@@ -1,0 +1,98 @@
+"""Build and time Ax_helm kernel variants (register bound / unroll) and dssum at 32^3.
+
+    python tools/ax_variants.py build      # here (nvcc), writes paper_2207_07098_b200/variants/*.so
+    python tools/ax_variants.py run [ne]   # on the GPU box
+"""
+import ctypes
+import glob
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+VDIR = os.path.join(ROOT, "paper_2207_07098_b200", "variants")
+VARIANTS = {
+    "generic_minb5u2": "-DSF_AX_GENERIC8 -DSF_AX_MINB=5 -DSF_AX_UNROLL=2",
+    "n8_minb2_epb4": "-DSF_AX8_MINB=2 -DSF_AX8_EPB=4",
+    "n8_minb3_epb4": "-DSF_AX8_MINB=3 -DSF_AX8_EPB=4",
+    "n8_minb2_epb2": "-DSF_AX8_MINB=2 -DSF_AX8_EPB=2",
+    "n8_minb4_epb2": "-DSF_AX8_MINB=4 -DSF_AX8_EPB=2",
+}
+
+
+def build():
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2207_07098_b200 import build as b
+
+    os.makedirs(VDIR, exist_ok=True)
+    srcs = b.sources()
+
+    def one(item):
+        name, flags = item
+        out = os.path.join(VDIR, f"lib_{name}.so")
+        cmd = ["nvcc", *b.NVCC_FLAGS, "-shared", *flags.split(), "-o", out, *srcs]
+        subprocess.run(cmd, check=True)
+        return out
+
+    with ThreadPoolExecutor(4) as ex:
+        print(list(ex.map(one, VARIANTS.items())))
+
+
+def run(ne):
+    import numpy as np
+    import torch
+
+    from paper_2207_07098_b200 import _lib
+    from bench import poisson_space
+
+    dev = torch.device("cuda", 0)
+    sp, mask, f = poisson_space(ne, dev)
+    from paper_2207_07098_b200.operators import GlobalOp
+
+    op = GlobalOp(sp, 1.0, 0.0, mask)
+    u = torch.randn(sp.shape, dtype=torch.float64, device=dev)
+    w = torch.empty_like(u)
+    st = torch.cuda.current_stream().cuda_stream
+    P = sp.n_points
+    gs = sp.gs
+    paths = [_lib.LIB_PATH] if os.environ.get("AX_MAIN_ONLY") else \
+        sorted(glob.glob(os.path.join(VDIR, "lib_*.so"))) + [_lib.LIB_PATH]
+    for path in paths:
+        L = ctypes.CDLL(path)
+        for name, args in _lib._SIGS.items():
+            getattr(L, name).argtypes = args
+        res = {}
+        for kind in ("masked", "plain", "dssum"):
+            def fn():
+                if kind == "masked":
+                    L.sf_ax_masked_f64(sp.dmat.ctypes.data, 8, sp.geom.data_ptr(), sp.bm.data_ptr(), u.data_ptr(),
+                                       w.data_ptr(), sp.n_elements, 1.0, 0.0, op.inmask.data_ptr(),
+                                       op.outsel.data_ptr(), 0, st)
+                elif kind == "plain":
+                    L.sf_ax_helm_f64(sp.dmat.ctypes.data, 8, sp.geom.data_ptr(), sp.bm.data_ptr(), u.data_ptr(),
+                                     w.data_ptr(), sp.n_elements, 1.0, 0.0, 0, st)
+                else:
+                    L.sf_dssum_f64(w.data_ptr(), gs.sh_off.data_ptr(), op.sh_perm.data_ptr(), gs.n_shared, 2,
+                                   u.data_ptr(), st)
+            for _ in range(3):
+                fn()
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
+            torch.cuda.synchronize()
+            for a, b in ev:
+                a.record()
+                fn()
+                b.record()
+            torch.cuda.synchronize()
+            res[kind] = float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3
+        gbs = P * 64 / (res["masked"] * 1e-6) / 1e9
+        print(f"{os.path.basename(path):24s} masked {res['masked']:8.1f} us ({gbs:6.0f} GB/s)  plain {res['plain']:8.1f} us"
+              f"  dssum {res['dssum']:7.1f} us", flush=True)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build()
+    else:
+        run(int(sys.argv[2]) if len(sys.argv) > 2 else 32)
