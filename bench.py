@@ -305,13 +305,113 @@ def bench_poisson(args, world, rank, dev):
     return line
 
 
+def cpu_tgv_sample(steps=None, warmup=None, budget=20.0):
+    """Oracle (CPU port of the reference) TGV Re=1600 on the 8^3 lx=8 box: mean step time
+    over the first steps (config 1, the reference's own CPU-runnable case)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import semflow_oracle as O
+
+    sp, st, state = O.tgv_setup(8)
+    P = int(np.prod(sp.shape))
+    for _ in range(warmup or 0):
+        state, _d = st.step(state)
+    times, its = [], []
+    t_all = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        state, d = st.step(state)
+        times.append(time.perf_counter() - t0)
+        its.append(d.p_iterations)
+        if (steps is not None and len(times) >= steps) or (steps is None and time.perf_counter() - t_all > budget):
+            break
+    t = float(np.mean(times))
+    first = (warmup or 0) + 1
+    return {"value": P / t / 1e9, "unit": "GDOF/s", "cores": O.num_threads(), "kind": "port",
+            "sample": f"oracle TGV Re=1600 8^3 lx=8 ({P} points), steps {first}-{first + len(times) - 1} "
+                      f"(pressure its {its}), mean {t:.2f} s/step"}
+
+
+def bench_tgv(args, world, rank, dev):
+    import torch
+
+    from paper_2207_07098_b200 import _lib
+    from paper_2207_07098_b200.timestep import FlowState, kinetic_energy, tgv_problem
+
+    ne = args.ne or 32
+    sp, st, state = tgv_problem(ne, device=dev)
+    P = sp.n_points
+    for _ in range(args.warmup):
+        state, d = st.step(state)
+    stream = torch.cuda.current_stream()
+    clk = ClockSampler(torch.cuda.current_device())
+    clk.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    l0 = _lib.LAUNCHES
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    p_its, v_its = [], []
+    for _ in range(args.steps):
+        state, d = st.step(state)
+        p_its.append(d.p_iterations)
+        v_its.append(list(d.v_iterations))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = _lib.LAUNCHES - l0
+    clk.stop()
+    t = barrier_max(e0.elapsed_time(e1) * 1e-3, world)
+    value = world * P * args.steps / t / 1e9
+    ke = kinetic_energy(sp, state.vel)
+    # end to end through the public API with host buffers: per step the velocity
+    # field arrives from pinned host memory and the new velocity is read back
+    vel_h = state.vel.cpu().pin_memory()
+    out_h = torch.empty_like(vel_h).pin_memory()
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v = vel_h.to(dev, non_blocking=True)
+        state = FlowState(state.time, state.nsteps, [v] + state.vel_hist[1:], state.curl_hist, state.nl_hist,
+                          state.prs, state.primed)
+        state, d = st.step(state)
+        out_h.copy_(state.vel, non_blocking=True)
+        torch.cuda.synchronize()
+        vel_h.copy_(out_h)
+    te = barrier_max(time.perf_counter() - t0, world)
+    e2e = {"value": world * P * args.steps / te / 1e9, "unit": "GDOF/s",
+           "h2d_bytes_per_step": vel_h.numel() * 8, "d2h_bytes_per_step": out_h.numel() * 8}
+    op = st.apply_p
+    kt = time_kernels(sp, op, torch.randn(sp.shape, dtype=torch.float64, device=dev))
+    pk, src = peaks()
+    nbytes = ax_dssum_bytes(sp, op.masked)
+    achieved = nbytes / (kt["ax"] + kt["dssum"]) / 1e9
+    return {
+        "metric": "GDOF/s per time step (TGV, lx=8)",
+        "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"TGV Re=1600 {ne}^3 elements lx=8 (config {'3' if ne == 64 else '1' if ne == 8 else '1/3 analogue'}),"
+                               " symmetry box, Jacobi-GMRES(20) p 1e-5, Jacobi-PCG v 1e-8, projection on",
+                   "points": P, "steps_timed": f"{args.warmup + 1}-{args.warmup + args.steps}",
+                   "p_iterations": p_its, "v_iterations": v_its, "ke_end": ke,
+                   "l2": "inputs larger than L2" if P * 8 * 6 > 126e6 else "working set may be L2-resident",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                     "kernel": "ax_helm+dssum (pressure Poisson operator)", "algorithmic_bytes": nbytes,
+                     "ax_us": kt["ax"] * 1e6, "dssum_us": kt["dssum"] * 1e6, "peak_source": src},
+        "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+    }
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--workload", default="poisson", choices=("poisson",))
+    ap.add_argument("--workload", default="tgv", choices=("tgv", "poisson"))
     ap.add_argument("--ne", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -320,11 +420,16 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        base = cpu_poisson_sample()
-        line = {"impl": "reference", "metric": "GDOF/s per PCG iteration (config 2: Poisson Ax+dssum+Jacobi-CG, 32^3 lx=8)",
+        if args.workload == "tgv":
+            base = cpu_tgv_sample(steps=args.steps, warmup=args.warmup)
+            metric = "GDOF/s per time step (TGV, lx=8)"
+        else:
+            base = cpu_poisson_sample()
+            metric = "GDOF/s per PCG iteration (config 2: Poisson Ax+dssum+Jacobi-CG, 32^3 lx=8)"
+        line = {"impl": "reference", "metric": metric,
                 "value": base["value"], "unit": "GDOF/s", "n_gpus": args.gpus, "steps": args.steps,
                 "warmup": args.warmup, "higher_is_better": True, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": "poisson (bounded CPU sample, see cpu_baseline.sample)"},
+                "config": {"workload": f"{args.workload} (bounded CPU sample, see cpu_baseline.sample)"},
                 "cpu_baseline": base, "e2e": {"value": base["value"], "unit": "GDOF/s",
                                               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -333,10 +438,10 @@ def main():
 
     world, rank, local = dist_setup()
     dev = torch.device("cuda", torch.cuda.current_device())
-    line = bench_poisson(args, world, rank, dev)
+    line = (bench_tgv if args.workload == "tgv" else bench_poisson)(args, world, rank, dev)
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_poisson_sample()
+            line["cpu_baseline"] = cpu_tgv_sample() if args.workload == "tgv" else cpu_poisson_sample()
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

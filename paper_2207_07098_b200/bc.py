@@ -1,0 +1,163 @@
+"""Boundary conditions on device (reference semflow/bc.py).
+
+Masks and per-step boundary terms for the kinds the hot path uses:
+``noslip``, ``velocity``, ``function`` (Dirichlet), ``symmetry`` and
+``outflow`` (bc.py:159-270).  Dirichlet evaluators are called with host numpy
+coordinates of the constrained points -- the same call the reference makes
+(bc.py:218-229), so user functions written for the reference work unchanged --
+and only those boundary values cross to the device.
+
+Surface terms (``pressure_surface_rhs``, ``surface_flux_rhs``) reproduce the
+reference's ``np.add.at`` accumulation order: contributions are added group by
+group (tag order), and inside a group in facet-point order, one "round" per
+repeated target so every local point sums its contributions sequentially.
+"""
+
+import numpy as np
+import torch
+
+from .errors import ConfigError
+
+DIRICHLET_KINDS = ("noslip", "velocity", "function")
+
+
+def _const_fn(value):
+    v = np.asarray(value, dtype=np.float64)
+    if v.shape != (3,):
+        raise ConfigError(f"constant velocity must have 3 components, got {v.shape}")
+
+    def fn(x, y, z, t):
+        return np.broadcast_to(v.reshape((3,) + (1,) * np.ndim(x)), (3,) + np.shape(x)).copy()
+
+    return fn
+
+
+class _Scatter:
+    """Ordered scatter-add of per-facet-point values into a local field."""
+
+    def __init__(self, targets):
+        # targets: (K,) int64 device tensor of local point indices in reference order
+        self.targets = targets
+        order = torch.sort(targets, stable=True).indices
+        st = targets[order]
+        first = torch.ones_like(st, dtype=torch.bool)
+        if st.numel() > 1:
+            first[1:] = st[1:] != st[:-1]
+        grp_start = torch.cummax(torch.where(first, torch.arange(st.numel(), device=st.device),
+                                             torch.zeros_like(st)), 0).values
+        occ_sorted = torch.arange(st.numel(), device=st.device) - grp_start
+        occ = torch.empty_like(occ_sorted)
+        occ[order] = occ_sorted
+        nround = int(occ.max()) + 1 if occ.numel() else 0
+        self.rounds = [torch.nonzero(occ == r).view(-1) for r in range(nround)]
+
+    def add_into(self, out_flat, vals):
+        for sel in self.rounds:
+            out_flat.index_add_(0, self.targets[sel], vals[sel])
+
+
+class BoundarySet:
+    """Compiled boundary conditions for one device FunctionSpace (bc.py:159-203)."""
+
+    def __init__(self, space, specs):
+        self.space = space
+        dev = space.device
+        self.vel_mask = torch.ones((3,) + space.shape, dtype=torch.float64, device=dev)
+        self.prs_mask = torch.ones(space.shape, dtype=torch.float64, device=dev)
+        self.dirichlet = []   # (tag, facet indices (host), evaluator, flat points (device), host coords)
+        self.symmetry = []    # (facet indices, axis, flat points)
+        seen = set()
+        coords_h = None
+        ftag = np.asarray(space.facet_tag)
+        for tag, spec in sorted(specs.items()):
+            if tag not in space.mesh.tag_names:
+                raise ConfigError(f"boundary condition references unknown tag {tag!r}; "
+                                  f"mesh has {space.mesh.tag_names}")
+            kind = spec["kind"]
+            params = {k: v for k, v in spec.items() if k != "kind"}
+            idx = np.nonzero(ftag == space.mesh.tag_names.index(tag))[0]
+            if idx.size == 0:
+                raise ConfigError(f"tag {tag!r} has no facets on this mesh")
+            seen.add(tag)
+            it = torch.from_numpy(idx).to(dev)
+            flat = space.facet_flat[it].reshape(-1)
+            if kind in DIRICHLET_KINDS:
+                fn = {"noslip": lambda: _const_fn((0.0, 0.0, 0.0)), "velocity": lambda: _const_fn(params["value"]),
+                      "function": lambda: params["fn"]}[kind]()
+                if coords_h is None:
+                    coords_h = space.coords.reshape(3, -1)
+                xs = coords_h[:, flat].cpu().numpy()
+                self.dirichlet.append((tag, it, fn, flat, xs))
+            elif kind == "symmetry":
+                self.symmetry.append((it, self._symmetry_axis(tag, it), flat))
+            elif kind == "outflow":
+                self.prs_mask.view(-1)[flat] = 0.0
+            else:
+                raise ConfigError(f"boundary kind {kind!r} for tag {tag!r} is not supported on the device path")
+        missing = set(space.mesh.tag_names) - seen
+        if missing:
+            raise ConfigError(f"no boundary condition given for tags {sorted(missing)}")
+        for _, axis, flat in self.symmetry:
+            self.vel_mask[axis].view(-1)[flat] = 0.0
+        for _, _, _, flat, _ in self.dirichlet:
+            for l in range(3):
+                self.vel_mask[l].view(-1)[flat] = 0.0
+        self.has_pressure_dirichlet = bool((self.prs_mask == 0.0).any())
+        self.has_dirichlet = bool(self.dirichlet)
+        self._neumann = [it for _, it, _, _, _ in self.dirichlet] + [it for it, _, _ in self.symmetry]
+        self._neu_scatter = [_Scatter(space.facet_flat[it].reshape(-1)) for it in self._neumann]
+        self._dir_scatter = [_Scatter(flat) for _, _, _, flat, _ in self.dirichlet]
+
+    def _symmetry_axis(self, tag, it):
+        nrm = self.space.facet_normal[it].abs()          # (k, n, n, 3)
+        axis = int(torch.argmax(nrm.reshape(-1, 3).mean(dim=0)))
+        comp = nrm[..., axis]
+        others = torch.cat([nrm[..., a:a + 1] for a in range(3) if a != axis], dim=-1)
+        if bool((comp < 1.0 - 1e-8).any()) or bool((others > 1e-8).any()):
+            raise ConfigError(f"symmetry tag {tag!r} lies on a non-axis-aligned surface; "
+                              "only coordinate-plane symmetry is supported")
+        return axis
+
+    def _values(self, fn, xs, t):
+        g = np.asarray(fn(xs[0], xs[1], xs[2], t), dtype=np.float64)
+        return torch.from_numpy(np.ascontiguousarray(g.reshape(3, -1))).to(self.space.device)
+
+    def apply_dirichlet(self, vel, t):
+        """Overwrite constrained velocity points with boundary values (bc.py:218-229)."""
+        flat = vel.view(3, -1)
+        for _, axis, pts in self.symmetry:
+            flat[axis][pts] = 0.0
+        for _, _, fn, pts, xs in self.dirichlet:
+            g = self._values(fn, xs, t)
+            for l in range(3):
+                flat[l][pts] = g[l]
+        return vel
+
+    def dirichlet_field(self, t):
+        g = torch.zeros((3,) + self.space.shape, dtype=torch.float64, device=self.space.device)
+        self.apply_dirichlet(g, t)
+        return g
+
+    def pressure_surface_rhs(self, t):
+        """sum over Dirichlet facets of phi_i (g . n) dA (bc.py:237-253)."""
+        sp = self.space
+        out = torch.zeros(sp.n_points, dtype=torch.float64, device=sp.device)
+        for (_, it, fn, pts, xs), sc in zip(self.dirichlet, self._dir_scatter):
+            g = self._values(fn, xs, t).view(3, *sp.facet_flat[it].shape)
+            nrm = sp.facet_normal[it].permute(3, 0, 1, 2)
+            gn = (g[0] * nrm[0] + g[1] * nrm[1] + g[2] * nrm[2]) * sp.facet_warea[it]
+            sc.add_into(out, gn.reshape(-1))
+        return out.view(sp.shape)
+
+    def surface_flux_rhs(self, field):
+        """sum over velocity-BC facets of phi_i (F . n) dA (bc.py:255-270)."""
+        sp = self.space
+        out = torch.zeros(sp.n_points, dtype=torch.float64, device=sp.device)
+        flat = field.reshape(3, -1)
+        for it, sc in zip(self._neumann, self._neu_scatter):
+            pts = sp.facet_flat[it]
+            f = flat[:, pts.reshape(-1)].view(3, *pts.shape)
+            nrm = sp.facet_normal[it].permute(3, 0, 1, 2)
+            fn = (f[0] * nrm[0] + f[1] * nrm[1] + f[2] * nrm[2]) * sp.facet_warea[it]
+            sc.add_into(out, fn.reshape(-1))
+        return out.view(sp.shape)

@@ -1,0 +1,89 @@
+"""Device BDF3/EXT3 step vs the reference's per-step diagnostics (golden) -- needs a B200.
+
+Bars: identical pressure (GMRES) and velocity (PCG) iteration counts on every
+step; kinetic energy and enstrophy within 1e-9 relative after N steps.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("ne", [4, 8])
+def test_tgv_steps_match_reference(cuda, golden_solvers, ne):
+    from paper_2207_07098_b200.timestep import enstrophy, kinetic_energy, tgv_problem
+
+    sp, st, state = tgv_problem(ne, device=cuda)
+    rows = golden_solvers[f"tgv{ne}"]
+    assert rel_err(kinetic_energy(sp, state.vel), rows[0]["ke"]) < 1e-12
+    assert rel_err(enstrophy(sp, state.vel), rows[0]["ens"]) < 1e-12
+    for row in rows[1:]:
+        state, d = st.step(state)
+        assert d.p_iterations == row["p_it"], (row["step"], d.p_iterations, row["p_it"])
+        assert list(d.v_iterations) == row["v_it"], (row["step"], d.v_iterations, row["v_it"])
+        assert rel_err(d.cfl, row["cfl"]) < 1e-10
+        assert rel_err(d.div_norm, row["div"]) < 1e-6
+        assert rel_err(kinetic_energy(sp, state.vel), row["ke"]) < 1e-9, row["step"]
+        assert rel_err(enstrophy(sp, state.vel), row["ens"]) < 1e-9, row["step"]
+
+
+def test_channel_boundary_paths(cuda, golden_solvers):
+    """Config-4 analogue: function (Poiseuille) inflow, outflow, no-slip, symmetry."""
+    from paper_2207_07098_b200.basis import make_basis
+    from paper_2207_07098_b200.bc import BoundarySet
+    from paper_2207_07098_b200.mesh import gen_box_mesh
+    from paper_2207_07098_b200.space import build_space
+    from paper_2207_07098_b200.timestep import SolverOptions, Stepper, kinetic_energy
+
+    Lx, Ly, Lz = 4 * np.pi / 8, 2.0, 4 * np.pi / 3 / 8
+    sp = build_space(gen_box_mesh((0.0, Lx, 0.0, Ly, 0.0, Lz), (6, 4, 3)), make_basis(5), device=cuda)
+
+    def pois(x, y, z, t):
+        out = np.zeros((3,) + np.shape(x))
+        out[0] = 1.5 * y * (2.0 - y)
+        return out
+
+    specs = {"xlo": {"kind": "function", "fn": pois}, "xhi": {"kind": "outflow"},
+             "ylo": {"kind": "noslip"}, "yhi": {"kind": "noslip"},
+             "zlo": {"kind": "symmetry"}, "zhi": {"kind": "symmetry"}}
+    bset = BoundarySet(sp, specs)
+    st = Stepper(sp, bset, nu=1.0 / 2800.0, dt=2e-3, scheme_order=3,
+                 pressure=SolverOptions(tol=1e-5, max_iter=200, restart=20, precond="jacobi"),
+                 velocity=SolverOptions(tol=1e-8, max_iter=100, precond="jacobi"))
+    x, y, z = sp.coords.cpu().numpy()
+    v0 = pois(x, y, z, 0.0)
+    v0[1] += 0.05 * np.sin(np.pi * x / Lx) * np.sin(np.pi * y / 2.0) ** 2
+    state = st.initial_state(torch.from_numpy(v0).to(cuda))
+    for row in golden_solvers["channel"][:3]:
+        state, d = st.step(state)
+        assert d.p_iterations == row["p_it"]
+        assert list(d.v_iterations) == row["v_it"], (d.v_iterations, row["v_it"])
+        assert rel_err(kinetic_energy(sp, state.vel), row["ke"]) < 1e-9
+
+
+def test_zero_state_is_fixed_point(cuda):
+    """Reference tests/test_timestep.py:89-100: zero velocity stays zero, no iterations."""
+    from paper_2207_07098_b200.timestep import tgv_problem
+
+    sp, st, _ = tgv_problem(2, device=cuda)
+    state = st.initial_state(torch.zeros((3,) + sp.shape, dtype=torch.float64, device=cuda))
+    for _ in range(3):
+        state, d = st.step(state)
+        assert d.p_iterations == 0 and d.cfl == 0.0
+    assert float(state.vel.abs().max()) == 0.0
+
+
+def test_order_ramp(cuda):
+    from paper_2207_07098_b200.timestep import scheme_coeffs, tgv_problem
+
+    assert scheme_coeffs(3)[0] == 11.0 / 6.0
+    sp, st, state = tgv_problem(2, device=cuda)
+    orders = []
+    for _ in range(4):
+        state, d = st.step(state)
+        orders.append(st._last_order)
+    assert orders == [1, 2, 3, 3]
