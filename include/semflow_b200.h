@@ -96,9 +96,20 @@ int sf_ax_masked_f64(const double* d_host, int n, const double* g, const double*
  * mode 2: masked operator finalisation (operators.py:53-54): copies whose perm
  *         entry is negative (bit 31 set) receive u[idx] instead of the sum.
  * Each shared gid is summed by one thread in reference order: bit-identical to
- * gs_gather + gs_scatter, atomics-free. */
+ * gs_gather + gs_scatter, atomics-free.
+ * Multi-GPU: perm entries >= n_local name copies owned by other ranks, whose raw
+ * values are read from recv[entry - n_local] and never written (recv == NULL:
+ * single rank, n_local ignored).  Summation stays in global copy order, so the
+ * result is bitwise independent of the rank count. */
 int sf_dssum_f64(double* v, const int* offsets, const int* perm, int n_shared, int mode,
-                 const double* u, void* stream);
+                 const double* u, const double* recv, int n_local, void* stream);
+
+/* out[i] = v[idx[i]] -- packs a rank's interface values for the halo exchange. */
+int sf_gather_f64(double* out, const double* v, const int* idx, long long n, void* stream);
+
+/* out[j] = buf[0*k+j] + buf[1*k+j] + ... (rank order): finishes an all-gather
+ * based, deterministic allreduce of k glsc3 partials over `world` ranks. */
+int sf_rank_sum_f64(const double* buf, int world, int k, double* out, void* stream);
 
 /* glsc3: out[k] = sum_p (a_k[p] / mult[p]) * b_k[p] for K = 1..4 pairs
  * (GatherScatter.dot, space.py:72-76).  a, b are HOST arrays of K device

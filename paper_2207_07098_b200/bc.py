@@ -75,10 +75,13 @@ class BoundarySet:
                                   f"mesh has {space.mesh.tag_names}")
             kind = spec["kind"]
             params = {k: v for k, v in spec.items() if k != "kind"}
-            idx = np.nonzero(ftag == space.mesh.tag_names.index(tag))[0]
-            if idx.size == 0:
+            tix = space.mesh.tag_names.index(tag)
+            idx = np.nonzero(ftag == tix)[0]
+            if not np.any(np.asarray(space.mesh.facet_tag) == tix):
                 raise ConfigError(f"tag {tag!r} has no facets on this mesh")
             seen.add(tag)
+            if idx.size == 0:
+                continue      # the tag's facets live on other ranks' elements
             it = torch.from_numpy(idx).to(dev)
             flat = space.facet_flat[it].reshape(-1)
             if kind in DIRICHLET_KINDS:
@@ -102,7 +105,7 @@ class BoundarySet:
         for _, _, _, flat, _ in self.dirichlet:
             for l in range(3):
                 self.vel_mask[l].view(-1)[flat] = 0.0
-        self.has_pressure_dirichlet = bool((self.prs_mask == 0.0).any())
+        self.has_pressure_dirichlet = space.comm.any(bool((self.prs_mask == 0.0).any()))
         self.has_dirichlet = bool(self.dirichlet)
         self._neumann = [it for _, it, _, _, _ in self.dirichlet] + [it for it, _, _ in self.symmetry]
         self._neu_scatter = [_Scatter(space.facet_flat[it].reshape(-1)) for it in self._neumann]

@@ -39,7 +39,10 @@ int grad_ref(const double*, int, const double*, double*, double*, double*, long 
 int apply_axis(int, const double*, int, int, const double*, double*, long long, int, cudaStream_t);
 int gs_gather(const double*, const long long*, const long long*, long long, double*, cudaStream_t);
 int gs_scatter(const double*, const long long*, const long long*, long long, double*, cudaStream_t);
-int dssum_shared(double*, const int*, const int*, int, int, const double*, cudaStream_t);
+int dssum_shared(double*, const int*, const int*, int, int, const double*, const double*, int,
+                 cudaStream_t);
+int gather(double*, const double*, const int*, long long, cudaStream_t);
+int rank_sum(const double*, int, int, double*, cudaStream_t);
 int dot_multi(int, const double* const*, const double* const*, const uint8_t*, long long, RedWork,
               double*, cudaStream_t);
 int cg_init(const double*, const double*, double*, const uint8_t*, long long, RedWork, double*,
@@ -118,8 +121,16 @@ int sf_ax_masked_f64(const double* d_host, int n, const double* g, const double*
 }
 
 int sf_dssum_f64(double* v, const int* offsets, const int* perm, int n_shared, int mode,
-                 const double* u, void* stream) {
-  return dssum_shared(v, offsets, perm, n_shared, mode, u, as_stream(stream));
+                 const double* u, const double* recv, int n_local, void* stream) {
+  return dssum_shared(v, offsets, perm, n_shared, mode, u, recv, n_local, as_stream(stream));
+}
+
+int sf_gather_f64(double* out, const double* v, const int* idx, long long n, void* stream) {
+  return gather(out, v, idx, n, as_stream(stream));
+}
+
+int sf_rank_sum_f64(const double* buf, int world, int k, double* out, void* stream) {
+  return rank_sum(buf, world, k, out, as_stream(stream));
 }
 
 int sf_glsc3_f64(int K, const double* const* a, const double* const* b, const uint8_t* mult,

@@ -39,20 +39,22 @@ __global__ void gs_scatter_kernel(const double* __restrict__ sums, const long lo
 }
 
 // MODE 0: add (QQ^T).  MODE 1: avg (sum * (1.0/count)).  MODE 2: masked-operator
-// finalisation (negative perm entry -> write u[idx]).  MODE 3: add, but write the
-// sum only to the copies (the caller guarantees the output already holds the
-// right values at unshared points) -- identical to MODE 0, kept for clarity.
+// finalisation (negative perm entry -> write u[idx]).
+// Entries >= n_local refer to copies owned by another rank: their raw values
+// were received into `recv` (entry - n_local), they are summed in place in the
+// global order and never written (their owner finalises them).
 template <int MODE>
 __global__ void dssum_shared_kernel(double* __restrict__ v, const int* __restrict__ off,
                                     const int* __restrict__ perm, int n_shared,
-                                    const double* __restrict__ u) {
+                                    const double* __restrict__ u, const double* __restrict__ recv,
+                                    int n_local) {
   int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n_shared) return;
   const int o0 = __ldg(off + g), o1 = __ldg(off + g + 1);
   double acc = 0.0;
   for (int o = o0; o < o1; ++o) {
-    int p = __ldg(perm + o) & 0x7fffffff;
-    acc = __dadd_rn(acc, v[p]);
+    const int p = __ldg(perm + o) & 0x7fffffff;
+    acc = __dadd_rn(acc, p < n_local ? v[p] : __ldg(recv + (p - n_local)));
   }
   if (MODE == 1) acc = __dmul_rn(acc, __drcp_rn((double)(o1 - o0)));
   for (int o = o0; o < o1; ++o) {
@@ -60,10 +62,27 @@ __global__ void dssum_shared_kernel(double* __restrict__ v, const int* __restric
     if (MODE == 2 && p < 0) {
       p &= 0x7fffffff;
       v[p] = u[p];
-    } else {
+    } else if (p < n_local) {
       v[p] = acc;
     }
   }
+}
+
+__global__ void gather_kernel(double* __restrict__ out, const double* __restrict__ v,
+                              const int* __restrict__ idx, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = v[idx[i]];
+}
+
+// out[j] = buf[0*k + j] + buf[1*k + j] + ... in rank order (deterministic allreduce)
+__global__ void rank_sum_kernel(const double* __restrict__ buf, int world, int k,
+                                double* __restrict__ out) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  double acc = 0.0;
+  for (int r = 0; r < world; ++r) acc = __dadd_rn(acc, buf[r * k + j]);
+  out[j] = acc;
 }
 
 int gs_gather(const double* vals, const long long* perm, const long long* off, long long n_gid,
@@ -83,20 +102,35 @@ int gs_scatter(const double* sums, const long long* perm, const long long* off, 
 }
 
 int dssum_shared(double* v, const int* off, const int* perm, int n_shared, int mode,
-                 const double* u, cudaStream_t st) {
+                 const double* u, const double* recv, int n_local, cudaStream_t st) {
   if (n_shared <= 0) return SF_OK;
+  if (recv == nullptr) n_local = 0x7fffffff;
   int th = 256;
   unsigned grid = (unsigned)((n_shared + th - 1) / th);
   switch (mode) {
-    case 0: dssum_shared_kernel<0><<<grid, th, 0, st>>>(v, off, perm, n_shared, nullptr); break;
-    case 1: dssum_shared_kernel<1><<<grid, th, 0, st>>>(v, off, perm, n_shared, nullptr); break;
+    case 0: dssum_shared_kernel<0><<<grid, th, 0, st>>>(v, off, perm, n_shared, nullptr, recv, n_local); break;
+    case 1: dssum_shared_kernel<1><<<grid, th, 0, st>>>(v, off, perm, n_shared, nullptr, recv, n_local); break;
     case 2:
       if (u == nullptr) { set_error("dssum_shared: masked mode needs u"); return SF_ERR_ARG; }
-      dssum_shared_kernel<2><<<grid, th, 0, st>>>(v, off, perm, n_shared, u);
+      dssum_shared_kernel<2><<<grid, th, 0, st>>>(v, off, perm, n_shared, u, recv, n_local);
       break;
     default: set_error("dssum_shared: bad mode %d", mode); return SF_ERR_ARG;
   }
   return check_launch("dssum_shared");
+}
+
+int gather(double* out, const double* v, const int* idx, long long n, cudaStream_t st) {
+  if (n <= 0) return SF_OK;
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  gather_kernel<<<(unsigned)blocks, 256, 0, st>>>(out, v, idx, n);
+  return check_launch("gather");
+}
+
+int rank_sum(const double* buf, int world, int k, double* out, cudaStream_t st) {
+  if (k <= 0) return SF_OK;
+  rank_sum_kernel<<<(k + 127) / 128, 128, 0, st>>>(buf, world, k, out);
+  return check_launch("rank_sum");
 }
 
 }  // namespace sf

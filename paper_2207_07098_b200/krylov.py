@@ -57,16 +57,24 @@ class _Fused:
         self.invdiag = precond.inv_diag if precond is not None else None
         self.w = _device.workspace(self.dev)
         self.st = _lib.stream_ptr(self.dev)
+        self.comm = sp.comm
 
     def dot(self, a, b, out):
         _lib.call("sf_glsc3_f64", 1, _ptrs([a]), _ptrs([b]), self.mult, self.P, *self.w.args(),
                   _lib.ptr(out), self.st)
+        self.comm.sum_(out)
 
     def dots(self, pairs, out):
         for c in range(0, len(pairs), 4):
             chunk = pairs[c:c + 4]
             _lib.call("sf_glsc3_f64", len(chunk), _ptrs([a for a, _ in chunk]), _ptrs([b for _, b in chunk]),
                       self.mult, self.P, *self.w.args(), out.data_ptr() + 8 * c, self.st)
+        self.comm.sum_(out[:len(pairs)])
+
+    def mgs(self, out, *args):
+        """sf_mgs_step_f64 writing 2 partials to `out` (a 2-slot view), then allreduce."""
+        _lib.call("sf_mgs_step_f64", *args, self.P, *self.w.args(), _lib.ptr(out), self.st)
+        self.comm.sum_(out)
 
     def read(self, t):
         h = t.to("cpu", non_blocking=False)
@@ -156,6 +164,7 @@ def _pcg_fused(op, b, tol, max_iter, precond, dot, x0):
     wk = F.w.args()
     sp = lambda i: s.data_ptr() + 8 * i
     _lib.call("sf_cg_init_f64", _lib.ptr(r), inv, _lib.ptr(p), mult, P, *wk, sp(1), F.st)
+    F.comm.sum_(s[1:2])
     rz_slot = 1
     it = 0
     converged = False
@@ -164,6 +173,7 @@ def _pcg_fused(op, b, tol, max_iter, precond, dot, x0):
         F.dot(p, ap, s[3:4])
         _lib.call("sf_cg_update_f64", _lib.ptr(x), _lib.ptr(r), _lib.ptr(p), _lib.ptr(ap), inv, mult,
                   sp(rz_slot), sp(3), P, *wk, sp(4), F.st)
+        F.comm.sum_(s[4:6])
         pap, rr = F.read(s[3:5])
         if pap <= 0.0:
             raise SolverBreakdownError(
@@ -311,13 +321,12 @@ def _gmres_fused(op, b, tol, max_iter, restart, precond, dot, x0):
             op.apply_into(z, w)
             # MGS sweep: pass 0 = (<w,v0>, <w,w>), pass i = (w -= h_{i-1} v_{i-1}; <w,v_i>),
             # last = (w -= h_j v_j; <w,w>)
-            _lib.call("sf_mgs_step_f64", _lib.ptr(w), None, None, _lib.ptr(vs[0]), None, None, mult, 1,
-                      P, *wk, hp(0), F.st)
+            F.mgs(hs[0:2], _lib.ptr(w), None, None, _lib.ptr(vs[0]), None, None, mult, 1)
             for i in range(1, j + 1):
-                _lib.call("sf_mgs_step_f64", _lib.ptr(w), _lib.ptr(vs[i - 1]), hp(2 * (i - 1)),
-                          _lib.ptr(vs[i]), None, None, mult, 0, P, *wk, hp(2 * i), F.st)
-            _lib.call("sf_mgs_step_f64", _lib.ptr(w), _lib.ptr(vs[j]), hp(2 * j), None, None, None, mult, 1,
-                      P, *wk, hp(2 * (j + 1)), F.st)
+                F.mgs(hs[2 * i:2 * i + 2], _lib.ptr(w), _lib.ptr(vs[i - 1]), hp(2 * (i - 1)),
+                      _lib.ptr(vs[i]), None, None, mult, 0)
+            F.mgs(hs[2 * (j + 1):2 * (j + 2)], _lib.ptr(w), _lib.ptr(vs[j]), hp(2 * j), None, None, None,
+                  mult, 1)
             vals = F.read(hs[: 2 * (j + 2)])
             norm_before = math.sqrt(vals[1])
             hcol = np.zeros(j + 2)
@@ -326,13 +335,12 @@ def _gmres_fused(op, b, tol, max_iter, restart, precond, dot, x0):
             norm_after = math.sqrt(vals[2 * (j + 1) + 1])
             if norm_after < 0.7071 * norm_before:
                 o = nh
-                _lib.call("sf_mgs_step_f64", _lib.ptr(w), None, None, _lib.ptr(vs[0]), None, None, mult, 0,
-                          P, *wk, hp(o), F.st)
+                F.mgs(hs[o:o + 2], _lib.ptr(w), None, None, _lib.ptr(vs[0]), None, None, mult, 0)
                 for i in range(1, j + 1):
-                    _lib.call("sf_mgs_step_f64", _lib.ptr(w), _lib.ptr(vs[i - 1]), hp(o + 2 * (i - 1)),
-                              _lib.ptr(vs[i]), None, None, mult, 0, P, *wk, hp(o + 2 * i), F.st)
-                _lib.call("sf_mgs_step_f64", _lib.ptr(w), _lib.ptr(vs[j]), hp(o + 2 * j), None, None, None,
-                          mult, 1, P, *wk, hp(o + 2 * (j + 1)), F.st)
+                    F.mgs(hs[o + 2 * i:o + 2 * i + 2], _lib.ptr(w), _lib.ptr(vs[i - 1]), hp(o + 2 * (i - 1)),
+                          _lib.ptr(vs[i]), None, None, mult, 0)
+                F.mgs(hs[o + 2 * (j + 1):o + 2 * (j + 2)], _lib.ptr(w), _lib.ptr(vs[j]), hp(o + 2 * j), None,
+                      None, None, mult, 1)
                 v2 = F.read(hs[o: o + 2 * (j + 2)])
                 for i in range(j + 1):
                     hcol[i] += v2[2 * i]
@@ -352,6 +360,7 @@ def _gmres_fused(op, b, tol, max_iter, restart, precond, dot, x0):
         _lincomb(x, x, vs[:j_end], y, F.invdiag, P, dev, F.st)
         ax = op(x)
         _lib.call("sf_residual_f64", _lib.ptr(r), _lib.ptr(b), _lib.ptr(ax), mult, P, *wk, _lib.ptr(s0[0:1]), F.st)
+        F.comm.sum_(s0[0:1])
         beta = math.sqrt(F.read(s0[0:1])[0])
         if beta <= tol:
             converged = True
@@ -463,9 +472,8 @@ class ProjectionSpace:
         for i in range(k):
             vprev = self.axs[i - 1] if i else None
             v2prev = self.xs[i - 1] if i else None
-            _lib.call("sf_mgs_step_f64", _lib.ptr(ad), _lib.ptr(vprev), sp(2 + 2 * (i - 1)) if i else None,
-                      _lib.ptr(self.xs[i]), _lib.ptr(d) if i else None, _lib.ptr(v2prev), F.mult, 0, F.P,
-                      *wk, sp(2 + 2 * i), F.st)
+            F.mgs(s[2 + 2 * i:4 + 2 * i], _lib.ptr(ad), _lib.ptr(vprev), sp(2 + 2 * (i - 1)) if i else None,
+                  _lib.ptr(self.xs[i]), _lib.ptr(d) if i else None, _lib.ptr(v2prev), F.mult, 0)
         if k:
             _lib.call("sf_mgs_step_f64", _lib.ptr(ad), _lib.ptr(self.axs[k - 1]), sp(2 + 2 * (k - 1)), None,
                       _lib.ptr(d), _lib.ptr(self.xs[k - 1]), F.mult, 0, F.P, *wk, sp(2 + 2 * k), F.st)

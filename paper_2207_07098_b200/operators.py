@@ -71,11 +71,7 @@ class GlobalOp:
                 self.masked = True
                 self.inmask = pack_bits(keep)
                 self.outsel = pack_bits(keep) | gs.shared_bits
-                dropped = (~keep).reshape(-1)
-                self.sh_perm = torch.where(
-                    dropped[gs.sh_perm.long()],
-                    gs.sh_perm | torch.tensor(-2**31, dtype=torch.int32, device=space.device),
-                    gs.sh_perm).contiguous()
+                self.sh_perm = gs.masked_perm(keep.reshape(-1))
             self.mask = m.view(space.shape)
         else:
             self.mask = None
@@ -91,13 +87,11 @@ class GlobalOp:
             _lib.call("sf_ax_masked_f64", sp.dmat.ctypes.data, sp.n, _lib.ptr(sp.geom), _lib.ptr(sp.bm),
                       _lib.ptr(u), _lib.ptr(w), E, self.lam_visc, self.lam_mass, _lib.ptr(self.inmask),
                       _lib.ptr(self.outsel), _ex(), st)
-            _lib.call("sf_dssum_f64", _lib.ptr(w), _lib.ptr(gs.sh_off), _lib.ptr(self.sh_perm),
-                      gs.n_shared, 2, _lib.ptr(u), st)
+            gs.dssum_into(w, 2, u=u, perm=self.sh_perm)
         else:
             _lib.call("sf_ax_helm_f64", sp.dmat.ctypes.data, sp.n, _lib.ptr(sp.geom), _lib.ptr(sp.bm),
                       _lib.ptr(u), _lib.ptr(w), E, self.lam_visc, self.lam_mass, _ex(), st)
-            _lib.call("sf_dssum_f64", _lib.ptr(w), _lib.ptr(gs.sh_off), _lib.ptr(gs.sh_perm),
-                      gs.n_shared, 0, None, st)
+            gs.dssum_into(w, 0)
         self.launches += 2
         return w
 
@@ -179,7 +173,6 @@ def cfl(space, v, dt):
     """CFL number (operators.py:161-182)."""
     bits = torch.zeros(1, dtype=torch.int64, device=space.device)
     cfl_max_async(space, v, bits)
-    if space.n_elements == 0:
-        return 0.0
+    space.comm.max_(bits)          # non-negative doubles order like their bit patterns
     val = bits.cpu().view(torch.float64).item()
     return float(dt) * float(val)

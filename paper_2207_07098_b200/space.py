@@ -61,20 +61,46 @@ class GatherScatter:
     uint8 multiplicity ``mult8`` for glsc3 weights.
     """
 
-    def __init__(self, gid, perm, offsets, shape):
+    def __init__(self, gid, perm, offsets, shape, comm=None, starts=None):
+        """gid/perm/offsets: the GLOBAL reference-format numbering.  With a
+        multi-rank ``comm``, this rank owns elements starts[rank]..starts[rank+1]
+        and its dssum reads the other ranks' copies through a halo exchange."""
+        from . import dist as _dist
+
         self.shape = tuple(shape)
         self.device = gid.device
-        self.gid = gid
-        self.perm = perm
-        self.offsets = offsets
+        self.comm = comm if comm is not None else _dist.single()
         self.n_gid = int(offsets.numel() - 1)
-        P = int(gid.numel())
+        E = self.shape[0]
+        P = E * int(np.prod(self.shape[1:])) if len(self.shape) > 1 else int(gid.numel())
         self.P = P
         if P >= 2**31 - 1:
             raise ConfigError("more than 2^31 local points on one device; partition the mesh")
         counts = offsets[1:] - offsets[:-1]
         if counts.numel() and int(counts.max()) > 255:
             raise TopologyError("a global id has more than 255 local copies")
+        self.plan = None
+        if self.comm.world > 1:
+            nnn = P // E
+            r = self.comm.rank
+            g0 = starts[r] * nnn
+            self.gid = gid[g0:g0 + P].clone()
+            self.perm = self.offsets = None      # global maps are not kept per rank
+            self.mult8 = counts[self.gid].to(torch.uint8).contiguous()
+            plan = _dist.build_halo_plan(gid, perm, offsets, starts, r, nnn)
+            self.plan = plan
+            self.n_shared = plan.n_shared
+            self.sh_off = plan.sh_off.contiguous()
+            self.sh_perm = plan.sh_perm.contiguous()
+            self.shared_bits = pack_bits((self.mult8 > 1).view(E, nnn))
+            self._sendbuf = torch.empty(int(plan.send_all.numel()), dtype=torch.float64, device=self.device)
+            self._recvbuf = torch.empty(max(plan.n_recv_total, 1), dtype=torch.float64, device=self.device)
+            self._masked_perm = {}
+            self._mult = None
+            return
+        self.gid = gid
+        self.perm = perm
+        self.offsets = offsets
         self.mult8 = counts[gid].to(torch.uint8).contiguous()
         # shared gids (multiplicity > 1), processed in the order of their lowest
         # local copy: consecutive threads of the dssum kernel then touch
@@ -114,11 +140,31 @@ class GatherScatter:
         return int(self.sh_perm.numel())
 
     # ------------------------------------------------------------ kernels
-    def _dssum_rows(self, flat, mode, u=None):
+    def halo_exchange(self, v):
+        """Send this rank's interface copies of field v, receive the peers' (raw values).
+        Returns the receive buffer (None on a single rank)."""
+        plan = self.plan
+        if plan is None or not plan.peers:
+            return None
         st = _lib.stream_ptr(self.device)
+        _lib.call("sf_gather_f64", _lib.ptr(self._sendbuf), _lib.ptr(v), _lib.ptr(plan.send_all),
+                  int(plan.send_all.numel()), st)
+        sends = {q: self._sendbuf[plan.send_off[q]:plan.send_off[q] + int(plan.send_idx[q].numel())]
+                 for q in plan.send_idx}
+        recvs = {q: self._recvbuf[plan.recv_off[q]:plan.recv_off[q] + plan.n_recv[q]] for q in plan.n_recv}
+        self.comm.exchange(sends, recvs)
+        return self._recvbuf
+
+    def dssum_into(self, v, mode, u=None, perm=None):
+        """In-place dssum of one scalar row v (mode 0 add / 1 avg / 2 masked with u)."""
+        recv = self.halo_exchange(v)
+        _lib.call("sf_dssum_f64", _lib.ptr(v), _lib.ptr(self.sh_off),
+                  _lib.ptr(self.sh_perm if perm is None else perm), self.n_shared, mode, _lib.ptr(u),
+                  _lib.ptr(recv), self.P, _lib.stream_ptr(self.device))
+
+    def _dssum_rows(self, flat, mode, u=None):
         for row in range(flat.shape[0]):
-            _lib.call("sf_dssum_f64", _lib.ptr(flat[row]), _lib.ptr(self.sh_off), _lib.ptr(self.sh_perm),
-                      self.n_shared, mode, _lib.ptr(u[row]) if u is not None else None, st)
+            self.dssum_into(flat[row], mode, u[row] if u is not None else None)
 
     def add_(self, u):
         """In-place QQ^T u (any leading axes, one row per leading index)."""
@@ -141,53 +187,40 @@ class GatherScatter:
         """Multiplicity-weighted average, sum * (1.0/count) (space.py:51-60)."""
         return self.avg_(u.contiguous().clone())
 
-    def masked_perm(self, mask_bits_flat):
-        """Shared perm with bit 31 set on masked copies (cached per mask object)."""
-        key = id(mask_bits_flat)
-        mp = self._masked_perm.get(key)
-        if mp is None:
-            m = mask_bits_flat[self.sh_perm.long()]
-            mp = torch.where(m, self.sh_perm | torch.tensor(-2**31, dtype=torch.int32, device=self.device),
-                             self.sh_perm).contiguous()
-            self._masked_perm[key] = (mp, mask_bits_flat)
-            return mp
-        return mp[0]
+    def masked_perm(self, keep_flat):
+        """Shared perm with bit 31 set on the local copies whose mask is 0."""
+        loc = self.sh_perm.long()
+        is_local = loc < self.P
+        dropped = torch.zeros_like(is_local)
+        dropped[is_local] = ~keep_flat[loc[is_local]]
+        return torch.where(dropped, self.sh_perm | torch.tensor(-2**31, dtype=torch.int32, device=self.device),
+                           self.sh_perm).contiguous()
 
     def dot_async(self, u, v, out):
-        """Write <u, v>_{1/mult} into the device scalar ``out`` (no sync)."""
+        """Write <u, v>_{1/mult} (summed over ranks) into the device scalar ``out``."""
         w = _device.workspace(self.device)
-        pa = (ctypes_ptrs([u]))
-        pb = (ctypes_ptrs([v]))
-        _lib.call("sf_glsc3_f64", 1, pa, pb, _lib.ptr(self.mult8), self.P * (u.numel() // self.P),
+        _lib.call("sf_glsc3_f64", 1, ctypes_ptrs([u]), ctypes_ptrs([v]), _lib.ptr(self.mult8), self.P,
                   *w.args(), _lib.ptr(out), _lib.stream_ptr(self.device))
+        self.comm.sum_(out)
         return out
 
     def dot(self, u, v):
-        """Multiplicity-weighted inner product (space.py:72-76), host float."""
+        """Multiplicity-weighted inner product of scalar fields (space.py:72-76), host float."""
         if u.numel() != self.P or v.numel() != self.P:
-            # vector fields: sum of the component dots is NOT what the reference
-            # does (it flattens); flatten likewise with a repeated weight
-            return self._dot_flat(u, v)
+            raise ValueError("GatherScatter.dot takes scalar fields (the reference's invmult "
+                             "weighting does not broadcast over vector fields)")
         w = _device.workspace(self.device)
-        self.dot_async(u, v, w.slots[0:1])
+        self.dot_async(u.contiguous(), v.contiguous(), w.slots[0:1])
         return w.read(0)[0]
 
-    def _dot_flat(self, u, v):
-        rows = u.numel() // self.P
-        tot = 0.0
-        w = _device.workspace(self.device)
-        uf, vf = u.reshape(rows, self.P), v.reshape(rows, self.P)
-        for r in range(rows):
-            self.dot_async(uf[r], vf[r], w.slots[r:r + 1])
-        vals = w.read(0, rows)
-        for x in vals:
-            tot += x
-        return tot
-
     def gather_unique(self, u):
+        if self.perm is None:
+            raise NotImplementedError("gather_unique on a partitioned space")
         return u.reshape(-1)[self.perm[self.offsets[:-1]]]
 
     def scatter_unique(self, vals, shape):
+        if self.perm is None:
+            raise NotImplementedError("scatter_unique on a partitioned space")
         counts = self.offsets[1:] - self.offsets[:-1]
         out = torch.empty(int(np.prod(shape)), dtype=torch.float64, device=self.device)
         out[self.perm] = torch.repeat_interleave(vals.to(torch.float64), counts)
@@ -350,7 +383,11 @@ class FunctionSpace:
     """Device analogue of the reference FunctionSpace (space.py:102-180)."""
 
     def __init__(self, basis, mesh, coords, rx, jac, bm, geom, gs, facet_elem, facet_face,
-                 facet_tag, facet_flat, facet_normal, facet_warea):
+                 facet_tag, facet_flat, facet_normal, facet_warea, comm=None, e_range=None):
+        from . import dist as _dist
+
+        self.comm = comm if comm is not None else _dist.single()
+        self.e_range = e_range if e_range is not None else (0, coords.shape[1])
         self.basis = basis
         self.mesh = mesh
         self.coords = coords
@@ -391,8 +428,9 @@ class FunctionSpace:
     def integral(self, u):
         """GLL quadrature sum(bm * u) (space.py:159-161), host float."""
         w = _device.workspace(self.device)
-        _lib.call("sf_glsc3_f64", 1, ctypes_ptrs([self.bm]), ctypes_ptrs([u]), None, self.n_points,
-                  *w.args(), _lib.ptr(w.slots[1:2]), _lib.stream_ptr(self.device))
+        _lib.call("sf_glsc3_f64", 1, ctypes_ptrs([self.bm]), ctypes_ptrs([u.contiguous()]), None,
+                  self.n_points, *w.args(), _lib.ptr(w.slots[1:2]), _lib.stream_ptr(self.device))
+        self.comm.sum_(w.slots[1:2])
         return w.read(1)[0]
 
     def l2_norm(self, u):
@@ -446,8 +484,11 @@ def _facets(mesh, basis, coords, dev):
     return flat_t, normal, warea
 
 
-def build_space(mesh, basis, device=None):
-    """Bind a basis to a mesh on the GPU (reference space.py:195-262)."""
+def build_space(mesh, basis, device=None, comm=None):
+    """Bind a basis to a mesh on the GPU (reference space.py:195-262).
+
+    With a multi-rank ``comm`` (paper_2207_07098_b200.dist.Comm) the returned
+    space holds this rank's contiguous element range only."""
     _lib.load()
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     if dev.type != "cuda":
@@ -473,27 +514,48 @@ def build_space(mesh, basis, device=None):
         ce = torch.from_numpy(curved).to(dev)
         for l in range(3):
             coords[l][ce] = cc[..., l]
-    rx = torch.empty((3, 3, E, n, n, n), dtype=torch.float64, device=dev)
-    jac = torch.empty((E, n, n, n), dtype=torch.float64, device=dev)
+    # the gather-scatter numbering is global (every rank builds it; it depends on
+    # the exact coordinates of all elements), everything else is per rank
+    gid, perm, offsets = build_gather_scatter(elements, coords, n)
+    from . import dist as _dist
+
+    comm = comm if comm is not None else _dist.single()
+    starts = _dist.element_ranges(E, comm.world)
+    e0, e1 = starts[comm.rank], starts[comm.rank + 1]
+    El = e1 - e0
+    if comm.world > 1:
+        coords = coords[:, e0:e1].contiguous()
+        torch.cuda.empty_cache()
+    rx = torch.empty((3, 3, El, n, n, n), dtype=torch.float64, device=dev)
+    jac = torch.empty((El, n, n, n), dtype=torch.float64, device=dev)
     bm = torch.empty_like(jac)
-    geom = torch.empty((6, E, n, n, n), dtype=torch.float64, device=dev)
+    geom = torch.empty((6, El, n, n, n), dtype=torch.float64, device=dev)
     dh, dptr = _lib.host_f64(basis.dmat)
     wh, wptr = _lib.host_f64(basis.weights)
-    _lib.call("sf_metrics_f64", dptr, wptr, n, _lib.ptr(coords), E, _lib.ptr(rx), _lib.ptr(jac),
+    _lib.call("sf_metrics_f64", dptr, wptr, n, _lib.ptr(coords), El, _lib.ptr(rx), _lib.ptr(jac),
               _lib.ptr(bm), _lib.ptr(geom), st)
     bad = jac <= 0.0
     if bool(bad.any()):
         e, i, j, k = (int(v) for v in torch.nonzero(bad)[0])
         raise GeometryError(f"non-positive Jacobian determinant {float(jac[e, i, j, k]):.3e}",
-                            element=e, ref_coords=(basis.points[i], basis.points[j], basis.points[k]))
-    gid, perm, offsets = build_gather_scatter(elements, coords, n)
-    gs = GatherScatter(gid, perm, offsets, (E, n, n, n))
-    flat, normal, warea = _facets(mesh, basis, coords, dev)
+                            element=e + e0, ref_coords=(basis.points[i], basis.points[j], basis.points[k]))
+    gs = GatherScatter(gid, perm, offsets, (El, n, n, n), comm=comm, starts=starts)
+    del gid, perm, offsets
+    fe = np.asarray(mesh.facet_elem, dtype=np.int64)
+    sel = (fe >= e0) & (fe < e1)
+    lmesh = _LocalFacets(fe[sel] - e0, np.asarray(mesh.facet_face)[sel])
+    flat, normal, warea = _facets(lmesh, basis, coords, dev)
     return FunctionSpace(
         basis=basis, mesh=mesh, coords=coords, rx=rx, jac=jac, bm=bm, geom=geom, gs=gs,
-        facet_elem=np.asarray(mesh.facet_elem).copy(), facet_face=np.asarray(mesh.facet_face).copy(),
-        facet_tag=np.asarray(mesh.facet_tag).copy(), facet_flat=flat, facet_normal=normal,
-        facet_warea=warea)
+        facet_elem=fe[sel] - e0, facet_face=np.asarray(mesh.facet_face)[sel].copy(),
+        facet_tag=np.asarray(mesh.facet_tag)[sel].copy(), facet_flat=flat, facet_normal=normal,
+        facet_warea=warea, comm=comm, e_range=(e0, e1))
+
+
+class _LocalFacets:
+    def __init__(self, facet_elem, facet_face):
+        self.facet_elem = facet_elem
+        self.facet_face = facet_face
 
 
 def from_reference(ref_space, device=None):

@@ -1,0 +1,82 @@
+"""Multi-GPU parity check, run under torchrun (one rank per GPU):
+
+    torchrun --standalone --nproc-per-node 2 tests/mgpu_check.py [ne] [steps]
+
+1. partitioned dssum (add / avg / masked Poisson operator) on a random field is
+   bitwise identical to the single-GPU result, on every rank;
+2. partitioned glsc3 equals the single-GPU value to rounding;
+3. the TGV step on the partitioned mesh reproduces the reference's iteration
+   counts and kinetic energy (tests/golden/solvers.json) when ne is 4 or 8.
+Rank 0 prints one JSON line and exits nonzero on failure.
+"""
+
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+
+def main():
+    from paper_2207_07098_b200 import dist, operators as ops
+    from paper_2207_07098_b200.basis import make_basis
+    from paper_2207_07098_b200.mesh import gen_box_mesh
+    from paper_2207_07098_b200.space import build_space
+    from paper_2207_07098_b200.timestep import enstrophy, kinetic_energy, tgv_problem
+
+    ne = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
+    comm = dist.init_from_env()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    r, W = comm.rank, comm.world
+    L = 2 * np.pi
+    mesh = gen_box_mesh((0, L, 0, L, 0, L), (ne, ne, ne))
+    basis = make_basis(7)
+    full = build_space(mesh, basis, device=dev)                 # single-GPU reference on each rank
+    part = build_space(mesh, basis, device=dev, comm=comm)
+    e0, e1 = part.e_range
+    g = torch.Generator(device="cpu").manual_seed(5)
+    u_full = torch.randn(full.shape, generator=g, dtype=torch.float64).to(dev)
+    u = u_full[e0:e1].contiguous()
+    ok = {}
+    ok["dssum_add"] = bool(torch.equal(part.gs.add(u), full.gs.add(u_full)[e0:e1]))
+    ok["dssum_avg"] = bool(torch.equal(part.gs.avg(u), full.gs.avg(u_full)[e0:e1]))
+    mask_f = torch.ones(full.shape, dtype=torch.float64, device=dev)
+    mask_f.view(-1)[full.facet_flat.reshape(-1)] = 0.0
+    mask_p = mask_f[e0:e1].contiguous()
+    a_f = ops.make_global_op(full, 1.0 / 1600, 183.3, mask_f)(u_full)[e0:e1]
+    a_p = ops.make_global_op(part, 1.0 / 1600, 183.3, mask_p)(u)
+    ok["masked_op"] = bool(torch.equal(a_p, a_f))
+    d_f = full.gs.dot(u_full, ops.make_global_op(full, 1.0, 0.0)(u_full))
+    d_p = part.gs.dot(u, ops.make_global_op(part, 1.0, 0.0)(u))
+    ok["glsc3"] = abs(d_p - d_f) <= 1e-13 * abs(d_f)
+    del full
+    torch.cuda.empty_cache()
+    res = {"world": W, "ne": ne, "checks": ok}
+    if ne in (4, 8):
+        with open(os.path.join(ROOT, "tests", "golden", "solvers.json")) as fh:
+            rows = json.load(fh)[f"tgv{ne}"]
+        sp, st, state = tgv_problem(ne, device=dev, comm=comm)
+        its, kes = [], []
+        for row in rows[1:steps + 1]:
+            state, d = st.step(state)
+            ke = kinetic_energy(sp, state.vel)
+            ens = enstrophy(sp, state.vel)
+            its.append((d.p_iterations, list(d.v_iterations), row["p_it"], row["v_it"]))
+            kes.append((ke, row["ke"], ens, row["ens"]))
+        ok["tgv_counts"] = all(a == c and b == dd for a, b, c, dd in its)
+        ok["tgv_ke"] = all(abs(k - kr) <= 1e-9 * abs(kr) and abs(e - er) <= 1e-9 * abs(er) for k, kr, e, er in kes)
+        res["tgv"] = {"iterations": its, "ke": kes}
+    res["ok"] = all(ok.values())
+    if r == 0:
+        print(json.dumps(res), flush=True)
+    torch.distributed.destroy_process_group()
+    sys.exit(0 if res["ok"] else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -45,7 +45,7 @@ def test_library_targets_sm100a():
 def test_error_path_without_gpu(lib):
     # an argument error is reported through the status code and sf_last_error,
     # before any device work is attempted
-    st = lib.sf_dssum_f64(None, None, None, 5, 7, None, None)
+    st = lib.sf_dssum_f64(None, None, None, 5, 7, None, None, 0, None)
     assert st == 1
     assert b"bad mode" in lib.sf_last_error()
     st = lib.sf_ax_helm_f64((ctypes.c_double * 1)(), 13, None, None, None, None, 4, 1.0, 0.0, 0, None)

@@ -75,7 +75,7 @@ def run(ne):
                                      w.data_ptr(), sp.n_elements, 1.0, 0.0, 0, st)
                 else:
                     L.sf_dssum_f64(w.data_ptr(), gs.sh_off.data_ptr(), op.sh_perm.data_ptr(), gs.n_shared, 2,
-                                   u.data_ptr(), st)
+                                   u.data_ptr(), None, 0, st)
             for _ in range(3):
                 fn()
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
