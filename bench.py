@@ -396,6 +396,7 @@ def bench_tgv(args, world, rank, dev):
                                " symmetry box, Jacobi-GMRES(20) p 1e-5, Jacobi-PCG v 1e-8, projection on",
                    "points": P, "steps_timed": f"{args.warmup + 1}-{args.warmup + args.steps}",
                    "p_iterations": p_its, "v_iterations": v_its, "ke_end": ke,
+                   "peak_mem_gb_rank0": torch.cuda.max_memory_allocated() / 1e9,
                    "l2": "inputs larger than L2" if P * 8 * 6 / world > 126e6 else "working set may be L2-resident",
                    "parallelism": (f"element partition x{world} (z-slabs), NCCL halo exchange + allgather dots"
                                    if world > 1 else "single")},
