@@ -49,6 +49,6 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // block to finish combines the per-block partials in block order.  The result is
 // a pure function of the inputs and P (never of scheduling).
 constexpr int RED_THREADS = 256;
-constexpr int RED_BLOCKS = 148 * 4;
+constexpr int RED_BLOCKS = 148 * 8;
 
 }  // namespace sf

@@ -190,13 +190,28 @@ struct BdfExtOp {
   double a_dt[3];
   double beta[3];
   int order;
+  struct In { double v[3], n[3], c[3]; };
   __device__ void prologue() {}
-  __device__ __forceinline__ void point(long long p, const double*, double (&)[1]) const {
+  __device__ __forceinline__ In load(long long p, const double*) const {
+    In in;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const bool on = q < order;
+      in.v[q] = on ? __ldg(vel[q] + p) : 0.0;
+      in.n[q] = on ? __ldg(nl[q] + p) : 0.0;
+      in.c[q] = on ? __ldg(crl[q] + p) : 0.0;
+    }
+    return in;
+  }
+  __device__ __forceinline__ void finish(long long p, const In& in, double (&)[1]) const {
     double vh = 0.0, om = 0.0;
-    for (int q = 0; q < order; ++q) {
-      vh = __dadd_rn(vh, __dmul_rn(a_dt[q], vel[q][p]));
-      vh = __dadd_rn(vh, __dmul_rn(beta[q], nl[q][p]));
-      om = __dadd_rn(om, __dmul_rn(beta[q], crl[q][p]));
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      if (q < order) {
+        vh = __dadd_rn(vh, __dmul_rn(a_dt[q], in.v[q]));
+        vh = __dadd_rn(vh, __dmul_rn(beta[q], in.n[q]));
+        om = __dadd_rn(om, __dmul_rn(beta[q], in.c[q]));
+      }
     }
     vhat[p] = vh;
     omega[p] = om;

@@ -14,6 +14,10 @@
 // pointers, so the host never has to round-trip them.  Every division that the
 // reference performs on host floats (alpha = rz / pap, ...) is performed by each
 // thread with the same IEEE operation, so all threads see the same value.
+//
+// Each Op splits its per-point work into load() (all global reads) and finish()
+// (arithmetic, stores, partial sums) so map_reduce_kernel can keep several
+// points' loads in flight per thread.
 #include "reduce.cuh"
 
 namespace sf {
@@ -24,6 +28,11 @@ __device__ __forceinline__ double wgt(const uint8_t* __restrict__ mult, long lon
   return mult ? im_tab[__ldg(mult + p)] : 1.0;
 }
 
+// z = M r with M = diag(invdiag) (BlockJacobi, precond.py:58-59) or identity.
+__device__ __forceinline__ double ldprec(const double* __restrict__ invdiag, long long p) {
+  return invdiag ? __ldg(invdiag + p) : 1.0;
+}
+
 // ---------------------------------------------------------------- dots
 // out[k] = sum_p (a_k[p] * w[p]) * b_k[p] for up to 4 (a, b) pairs
 template <int KK>
@@ -32,13 +41,23 @@ struct DotOp {
   const double* a[4];
   const double* b[4];
   const uint8_t* mult;
+  struct In { double a[KK], b[KK], w; };
   __device__ void prologue() {}
-  __device__ __forceinline__ void point(long long p, const double* im_tab, double (&acc)[K]) const {
-    const double w = wgt(mult, p, im_tab);
+  __device__ __forceinline__ In load(long long p, const double* im_tab) const {
+    In in;
+    in.w = wgt(mult, p, im_tab);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      double aw = mult ? __ldg(a[k] + p) * w : __ldg(a[k] + p);
-      acc[k] = fma(aw, __ldg(b[k] + p), acc[k]);
+      in.a[k] = __ldg(a[k] + p);
+      in.b[k] = __ldg(b[k] + p);
+    }
+    return in;
+  }
+  __device__ __forceinline__ void finish(long long, const In& in, double (&acc)[K]) const {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const double aw = mult ? in.a[k] * in.w : in.a[k];
+      acc[k] = fma(aw, in.b[k], acc[k]);
     }
   }
 };
@@ -60,11 +79,6 @@ int dot_multi(int K, const double* const* a, const double* const* b, const uint8
 }
 
 // ---------------------------------------------------------------- PCG
-// z = M r with M = diag(invdiag) (BlockJacobi, precond.py:58-59) or identity.
-__device__ __forceinline__ double prec(const double* __restrict__ invdiag, double r, long long p) {
-  return invdiag ? __ldg(invdiag + p) * r : r;
-}
-
 // p = M r ; out[0] = <r, p>_w                      (krylov.py:48-50)
 struct CgInitOp {
   static constexpr int K = 1;
@@ -72,12 +86,15 @@ struct CgInitOp {
   const double* invdiag;
   double* pv;
   const uint8_t* mult;
+  struct In { double r, d, w; };
   __device__ void prologue() {}
-  __device__ __forceinline__ void point(long long p, const double* im_tab, double (&acc)[K]) const {
-    const double rv = r[p];
-    const double z = prec(invdiag, rv, p);
+  __device__ __forceinline__ In load(long long p, const double* im_tab) const {
+    return In{r[p], ldprec(invdiag, p), wgt(mult, p, im_tab)};
+  }
+  __device__ __forceinline__ void finish(long long p, const In& in, double (&acc)[K]) const {
+    const double z = invdiag ? in.d * in.r : in.r;
     pv[p] = z;
-    acc[0] = fma(rv * wgt(mult, p, im_tab), z, acc[0]);
+    acc[0] = fma(in.r * in.w, z, acc[0]);
   }
 };
 
@@ -95,14 +112,18 @@ struct CgUpdateOp {
   const double* rz;
   const double* pap;
   double alpha;
+  struct In { double x, r, p, ap, d, w; };
   __device__ void prologue() { alpha = *rz / *pap; }
-  __device__ __forceinline__ void point(long long p, const double* im_tab, double (&acc)[K]) const {
-    x[p] = fma(alpha, pv[p], x[p]);
-    const double rv = fma(-alpha, ap[p], r[p]);
+  __device__ __forceinline__ In load(long long p, const double* im_tab) const {
+    return In{x[p], r[p], pv[p], ap[p], ldprec(invdiag, p), wgt(mult, p, im_tab)};
+  }
+  __device__ __forceinline__ void finish(long long p, const In& in, double (&acc)[K]) const {
+    x[p] = fma(alpha, in.p, in.x);
+    const double rv = fma(-alpha, in.ap, in.r);
     r[p] = rv;
-    const double rw = rv * wgt(mult, p, im_tab);
+    const double rw = rv * in.w;
     acc[0] = fma(rw, rv, acc[0]);
-    acc[1] = fma(rw, prec(invdiag, rv, p), acc[1]);
+    acc[1] = fma(rw, invdiag ? in.d * rv : rv, acc[1]);
   }
 };
 
@@ -115,9 +136,13 @@ struct CgDirOp {
   const double* rz_new;
   const double* rz;
   double beta;
+  struct In { double p, r, d; };
   __device__ void prologue() { beta = *rz_new / *rz; }
-  __device__ __forceinline__ void point(long long p, const double*, double (&)[1]) const {
-    pv[p] = fma(beta, pv[p], prec(invdiag, r[p], p));
+  __device__ __forceinline__ In load(long long p, const double*) const {
+    return In{pv[p], r[p], ldprec(invdiag, p)};
+  }
+  __device__ __forceinline__ void finish(long long p, const In& in, double (&)[1]) const {
+    pv[p] = fma(beta, in.p, invdiag ? in.d * in.r : in.r);
   }
 };
 
@@ -159,16 +184,27 @@ struct MgsOp {
   const uint8_t* mult;
   int want_norm;
   double h;
+  struct In { double w, vp, vn, w2, v2p, m; };
   __device__ void prologue() { h = vprev ? *hprev : 0.0; }
-  __device__ __forceinline__ void point(long long p, const double* im_tab, double (&acc)[K]) const {
-    double wv = w[p];
+  __device__ __forceinline__ In load(long long p, const double* im_tab) const {
+    In in;
+    in.w = w[p];
+    in.vp = vprev ? __ldg(vprev + p) : 0.0;
+    in.vn = vnext ? __ldg(vnext + p) : 0.0;
+    in.w2 = w2 ? w2[p] : 0.0;
+    in.v2p = w2 ? __ldg(v2prev + p) : 0.0;
+    in.m = wgt(mult, p, im_tab);
+    return in;
+  }
+  __device__ __forceinline__ void finish(long long p, const In& in, double (&acc)[K]) const {
+    double wv = in.w;
     if (vprev) {
-      wv = fma(-h, vprev[p], wv);
+      wv = fma(-h, in.vp, wv);
       w[p] = wv;
     }
-    if (w2) w2[p] = fma(-h, v2prev[p], w2[p]);
-    const double ww = wv * wgt(mult, p, im_tab);
-    if (vnext) acc[0] = fma(ww, __ldg(vnext + p), acc[0]);
+    if (w2) w2[p] = fma(-h, in.v2p, in.w2);
+    const double ww = wv * in.m;
+    if (vnext) acc[0] = fma(ww, in.vn, acc[0]);
     if (want_norm) acc[1] = fma(ww, wv, acc[1]);
   }
 };
@@ -183,27 +219,45 @@ int mgs_step(double* w, const double* vprev, const double* hprev, const double* 
 // x = x0 + sum_i coef[i] * M v_i, accumulated in i order (krylov.py:153-154 for
 // GMRES with zs[i] = M v_i recomputed bit-identically; krylov.py:207-209 for the
 // projection guess with M = I and x0 = 0).  x0 may alias x; x0 == nullptr -> 0.
-struct LinCombOp {
-  static constexpr int K = 0;
-  double* x;
-  const double* x0;
-  const double* const* v;  // device array of nv pointers
-  const double* coef;      // device array of nv scalars
-  const double* invdiag;
-  int nv;
-  __device__ void prologue() {}
-  __device__ __forceinline__ void point(long long p, const double*, double (&)[1]) const {
-    double acc = x0 ? x0[p] : 0.0;
-    for (int i = 0; i < nv; ++i) acc = fma(coef[i], prec(invdiag, __ldg(v[i] + p), p), acc);
-    x[p] = acc;
+// Each thread carries 4 independent points through the i loop so 4 loads of
+// every basis vector are in flight at once.
+__global__ void __launch_bounds__(RED_THREADS)
+lincomb_kernel(double* x, const double* x0, const double* const* __restrict__ v,
+               const double* __restrict__ coef, const double* __restrict__ invdiag, int nv,
+               long long P) {
+  const long long stride = (long long)gridDim.x * RED_THREADS;
+  for (long long p0 = (long long)blockIdx.x * RED_THREADS + threadIdx.x; p0 < P; p0 += 4 * stride) {
+    double acc[4], d[4];
+    bool ok[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const long long p = p0 + q * stride;
+      ok[q] = p < P;
+      acc[q] = (ok[q] && x0) ? x0[p] : 0.0;
+      d[q] = (ok[q] && invdiag) ? __ldg(invdiag + p) : 1.0;
+    }
+    for (int i = 0; i < nv; ++i) {
+      const double c = __ldg(coef + i);
+      const double* vi = v[i];
+      double vv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) vv[q] = ok[q] ? __ldg(vi + p0 + q * stride) : 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(c, invdiag ? d[q] * vv[q] : vv[q], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (ok[q]) x[p0 + q * stride] = acc[q];
   }
-};
+}
 
 int lincomb(double* x, const double* x0, const double* const* v, const double* coef,
             const double* invdiag, int nv, long long P, cudaStream_t st) {
-  LinCombOp op{x, x0, v, coef, invdiag, nv};
-  RedWork none{nullptr, nullptr};
-  return launch_map_reduce(op, P, none, nullptr, st, "lincomb");
+  if (P <= 0) return SF_OK;
+  long long need = (P + 4LL * RED_THREADS - 1) / (4LL * RED_THREADS);
+  unsigned blocks = (unsigned)(need < RED_BLOCKS ? (need > 0 ? need : 1) : RED_BLOCKS);
+  lincomb_kernel<<<blocks, RED_THREADS, 0, st>>>(x, x0, v, coef, invdiag, nv, P);
+  return check_launch("lincomb");
 }
 
 // r = b - ax ; out[0] = <r, r>_w                   (krylov.py:155-157)
@@ -213,11 +267,15 @@ struct ResidualOp {
   const double* b;
   const double* ax;
   const uint8_t* mult;
+  struct In { double b, ax, w; };
   __device__ void prologue() {}
-  __device__ __forceinline__ void point(long long p, const double* im_tab, double (&acc)[K]) const {
-    const double rv = b[p] - ax[p];
+  __device__ __forceinline__ In load(long long p, const double* im_tab) const {
+    return In{b[p], ax[p], wgt(mult, p, im_tab)};
+  }
+  __device__ __forceinline__ void finish(long long p, const In& in, double (&acc)[K]) const {
+    const double rv = in.b - in.ax;
     r[p] = rv;
-    acc[0] = fma(rv * wgt(mult, p, im_tab), rv, acc[0]);
+    acc[0] = fma(rv * in.w, rv, acc[0]);
   }
 };
 
@@ -237,10 +295,14 @@ struct ScaleDivOp {
   const double* x2;
   const double* s;
   double sv;
+  struct In { double x, x2; };
   __device__ void prologue() { sv = *s; }
-  __device__ __forceinline__ void point(long long p, const double*, double (&)[1]) const {
-    y[p] = x[p] / sv;
-    if (y2) y2[p] = x2[p] / sv;
+  __device__ __forceinline__ In load(long long p, const double*) const {
+    return In{x[p], y2 ? x2[p] : 0.0};
+  }
+  __device__ __forceinline__ void finish(long long p, const In& in, double (&)[1]) const {
+    y[p] = in.x / sv;
+    if (y2) y2[p] = in.x2 / sv;
   }
 };
 
