@@ -94,17 +94,23 @@ __global__ void __launch_bounds__(RED_THREADS) map_reduce_kernel(Op op, long lon
   double acc[K > 0 ? K : 1];
 #pragma unroll
   for (int k = 0; k < (K > 0 ? K : 1); ++k) acc[k] = 0.0;
-  const long long stride = (long long)gridDim.x * RED_THREADS;
-  for (long long p0 = (long long)blockIdx.x * RED_THREADS + threadIdx.x; p0 < P; p0 += RED_UNR * stride) {
+  // a warp walks contiguous spans of 32*RED_UNR points (each load instruction is a
+  // fully coalesced 256 B run and the warp's RED_UNR runs are adjacent: good DRAM
+  // locality); warps stride over the array
+  const int lane = threadIdx.x & 31;
+  const long long gwarp = ((long long)blockIdx.x * RED_THREADS + threadIdx.x) >> 5;
+  const long long span = 32LL * RED_UNR;
+  const long long wstride = (long long)gridDim.x * (RED_THREADS / 32) * span;
+  for (long long base = gwarp * span + lane; base < P; base += wstride) {
     typename Op::In in[RED_UNR];
 #pragma unroll
     for (int q = 0; q < RED_UNR; ++q) {
-      const long long p = p0 + q * stride;
+      const long long p = base + 32 * q;
       if (p < P) in[q] = o.load(p, im_tab);
     }
 #pragma unroll
     for (int q = 0; q < RED_UNR; ++q) {
-      const long long p = p0 + q * stride;
+      const long long p = base + 32 * q;
       if (p < P) o.finish(p, in[q], acc);
     }
   }

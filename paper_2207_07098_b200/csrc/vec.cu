@@ -225,8 +225,11 @@ __global__ void __launch_bounds__(RED_THREADS)
 lincomb_kernel(double* x, const double* x0, const double* const* __restrict__ v,
                const double* __restrict__ coef, const double* __restrict__ invdiag, int nv,
                long long P) {
-  const long long stride = (long long)gridDim.x * RED_THREADS;
-  for (long long p0 = (long long)blockIdx.x * RED_THREADS + threadIdx.x; p0 < P; p0 += 4 * stride) {
+  const int lane = threadIdx.x & 31;
+  const long long gwarp = ((long long)blockIdx.x * RED_THREADS + threadIdx.x) >> 5;
+  const long long wstride = (long long)gridDim.x * (RED_THREADS / 32) * 128;
+  const long long stride = 32;
+  for (long long p0 = gwarp * 128 + lane; p0 < P; p0 += wstride) {
     double acc[4], d[4];
     bool ok[4];
 #pragma unroll
