@@ -173,6 +173,7 @@ int cg_direction(double* pv, const double* r, const double* invdiag, const doubl
 //   out[1] = <w, w>_w       if want_norm     (norm_before / norm_after)
 // A second pair (w2, v2prev) lets the projection basis update ad and d together
 // (krylov.py:230-231): w2 -= (*hprev) * v2prev.
+template <bool PREV, bool NEXT, bool NORM, bool W2>
 struct MgsOp {
   static constexpr int K = 2;
   double* w;
@@ -182,38 +183,61 @@ struct MgsOp {
   double* w2;
   const double* v2prev;
   const uint8_t* mult;
-  int want_norm;
   double h;
   struct In { double w, vp, vn, w2, v2p, m; };
-  __device__ void prologue() { h = vprev ? *hprev : 0.0; }
+  __device__ void prologue() { h = PREV ? *hprev : 0.0; }
   __device__ __forceinline__ In load(long long p, const double* im_tab) const {
-    In in;
+    In in{};
     in.w = w[p];
-    in.vp = vprev ? __ldg(vprev + p) : 0.0;
-    in.vn = vnext ? __ldg(vnext + p) : 0.0;
-    in.w2 = w2 ? w2[p] : 0.0;
-    in.v2p = w2 ? __ldg(v2prev + p) : 0.0;
-    in.m = wgt(mult, p, im_tab);
+    if constexpr (PREV) in.vp = __ldg(vprev + p);
+    if constexpr (NEXT) in.vn = __ldg(vnext + p);
+    if constexpr (W2) {
+      in.w2 = w2[p];
+      in.v2p = __ldg(v2prev + p);
+    }
+    if constexpr (NEXT || NORM) in.m = wgt(mult, p, im_tab);
     return in;
   }
   __device__ __forceinline__ void finish(long long p, const In& in, double (&acc)[K]) const {
     double wv = in.w;
-    if (vprev) {
+    if constexpr (PREV) {
       wv = fma(-h, in.vp, wv);
       w[p] = wv;
     }
-    if (w2) w2[p] = fma(-h, in.v2p, in.w2);
-    const double ww = wv * in.m;
-    if (vnext) acc[0] = fma(ww, in.vn, acc[0]);
-    if (want_norm) acc[1] = fma(ww, wv, acc[1]);
+    if constexpr (W2) w2[p] = fma(-h, in.v2p, in.w2);
+    if constexpr (NEXT || NORM) {
+      const double ww = wv * in.m;
+      if constexpr (NEXT) acc[0] = fma(ww, in.vn, acc[0]);
+      if constexpr (NORM) acc[1] = fma(ww, wv, acc[1]);
+    }
   }
 };
+
+template <bool PREV, bool NEXT, bool NORM, bool W2>
+static int mgs_launch(double* w, const double* vprev, const double* hprev, const double* vnext,
+                      double* w2, const double* v2prev, const uint8_t* mult, long long P,
+                      RedWork wk, double* out, cudaStream_t st) {
+  MgsOp<PREV, NEXT, NORM, W2> op{w, vprev, hprev, vnext, w2, v2prev, mult, 0.0};
+  return launch_map_reduce(op, P, wk, out, st, "mgs_step");
+}
 
 int mgs_step(double* w, const double* vprev, const double* hprev, const double* vnext, double* w2,
              const double* v2prev, const uint8_t* mult, int want_norm, long long P, RedWork wk,
              double* out, cudaStream_t st) {
-  MgsOp op{w, vprev, hprev, vnext, w2, v2prev, mult, want_norm, 0.0};
-  return launch_map_reduce(op, P, wk, out, st, "mgs_step");
+  if (w2 && !vprev) w2 = nullptr;  // w2 is only ever updated together with w
+  const int code = (vprev ? 8 : 0) | (vnext ? 4 : 0) | (want_norm ? 2 : 0) | (w2 ? 1 : 0);
+  switch (code) {
+#define C(CODE, A, B, N, W) \
+  case CODE: return mgs_launch<A, B, N, W>(w, vprev, hprev, vnext, w2, v2prev, mult, P, wk, out, st);
+    C(0, false, false, false, false) C(2, false, false, true, false)
+    C(4, false, true, false, false) C(6, false, true, true, false)
+    C(8, true, false, false, false) C(9, true, false, false, true)
+    C(10, true, false, true, false) C(11, true, false, true, true)
+    C(12, true, true, false, false) C(13, true, true, false, true)
+    C(14, true, true, true, false) C(15, true, true, true, true)
+#undef C
+    default: set_error("mgs_step: bad argument combination"); return SF_ERR_ARG;
+  }
 }
 
 // x = x0 + sum_i coef[i] * M v_i, accumulated in i order (krylov.py:153-154 for
