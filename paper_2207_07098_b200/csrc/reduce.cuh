@@ -10,6 +10,8 @@
 // kernels/__init__.py:19-22) -- but they are not the OpenBLAS `np.dot` order
 // (space.py:76), which no parallel reduction can reproduce.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace sf {
@@ -82,10 +84,18 @@ __device__ __forceinline__ void finish_reduce(double (&acc)[K], RedWork wk, doub
 // aliasing) and stalled at ~5 TB/s.
 constexpr int RED_UNR = 4;
 
+// per-Op unroll depth: Op::UNR when declared (read-only ops carry few registers
+// per point and want more bytes in flight), RED_UNR otherwise
+template <class Op, class = void>
+struct UnrOf { static constexpr int value = RED_UNR; };
+template <class Op>
+struct UnrOf<Op, std::void_t<decltype(Op::UNR)>> { static constexpr int value = Op::UNR; };
+
 template <class Op>
 __global__ void __launch_bounds__(RED_THREADS) map_reduce_kernel(Op op, long long P, RedWork wk,
                                                                  double* __restrict__ out) {
   constexpr int K = Op::K;
+  constexpr int U = UnrOf<Op>::value;
   __shared__ double im_tab[256];
   init_im_tab(im_tab);
   __syncthreads();
@@ -99,17 +109,17 @@ __global__ void __launch_bounds__(RED_THREADS) map_reduce_kernel(Op op, long lon
   // locality); warps stride over the array
   const int lane = threadIdx.x & 31;
   const long long gwarp = ((long long)blockIdx.x * RED_THREADS + threadIdx.x) >> 5;
-  const long long span = 32LL * RED_UNR;
+  const long long span = 32LL * U;
   const long long wstride = (long long)gridDim.x * (RED_THREADS / 32) * span;
   for (long long base = gwarp * span + lane; base < P; base += wstride) {
-    typename Op::In in[RED_UNR];
+    typename Op::In in[U];
 #pragma unroll
-    for (int q = 0; q < RED_UNR; ++q) {
+    for (int q = 0; q < U; ++q) {
       const long long p = base + 32 * q;
       if (p < P) in[q] = o.load(p, im_tab);
     }
 #pragma unroll
-    for (int q = 0; q < RED_UNR; ++q) {
+    for (int q = 0; q < U; ++q) {
       const long long p = base + 32 * q;
       if (p < P) o.finish(p, in[q], acc);
     }

@@ -213,10 +213,91 @@ struct MgsOp {
   }
 };
 
+// Vectorised MGS pass: 16-byte loads of point pairs (each warp instruction moves
+// a contiguous 512 B run), 4 pairs per lane in flight.  Same per-point arithmetic
+// as MgsOp; used when P is even and every array is 16-byte aligned.
+template <bool PREV, bool NEXT, bool NORM, bool W2>
+__global__ void __launch_bounds__(RED_THREADS)
+mgs2_kernel(double* __restrict__ w, const double* __restrict__ vprev, const double* __restrict__ hprev,
+            const double* __restrict__ vnext, double* __restrict__ w2, const double* __restrict__ v2prev,
+            const uint8_t* __restrict__ mult, long long P2, RedWork wk, double* __restrict__ out) {
+  constexpr int U = 4;
+  __shared__ double im_tab[256];
+  init_im_tab(im_tab);
+  __syncthreads();
+  const double h = PREV ? *hprev : 0.0;
+  double acc[2] = {0.0, 0.0};
+  const int lane = threadIdx.x & 31;
+  const long long gwarp = ((long long)blockIdx.x * RED_THREADS + threadIdx.x) >> 5;
+  const long long span = 32LL * U;
+  const long long wstride = (long long)gridDim.x * (RED_THREADS / 32) * span;
+  double2* w_2 = reinterpret_cast<double2*>(w);
+  double2* w2_2 = reinterpret_cast<double2*>(w2);
+  for (long long base = gwarp * span + lane; base < P2; base += wstride) {
+    double2 wv[U], vp[U], vn[U], x2[U], v2[U];
+    double m0[U], m1[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const long long i = base + 32 * q;
+      if (i < P2) {
+        wv[q] = w_2[i];
+        if constexpr (PREV) vp[q] = __ldg(reinterpret_cast<const double2*>(vprev) + i);
+        if constexpr (NEXT) vn[q] = __ldg(reinterpret_cast<const double2*>(vnext) + i);
+        if constexpr (W2) {
+          x2[q] = w2_2[i];
+          v2[q] = __ldg(reinterpret_cast<const double2*>(v2prev) + i);
+        }
+        if constexpr (NEXT || NORM) {
+          const uchar2 mm = __ldg(reinterpret_cast<const uchar2*>(mult) + i);
+          m0[q] = im_tab[mm.x];
+          m1[q] = im_tab[mm.y];
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const long long i = base + 32 * q;
+      if (i < P2) {
+        double a = wv[q].x, b = wv[q].y;
+        if constexpr (PREV) {
+          a = fma(-h, vp[q].x, a);
+          b = fma(-h, vp[q].y, b);
+          w_2[i] = make_double2(a, b);
+        }
+        if constexpr (W2) w2_2[i] = make_double2(fma(-h, v2[q].x, x2[q].x), fma(-h, v2[q].y, x2[q].y));
+        if constexpr (NEXT || NORM) {
+          const double wa = a * m0[q], wb = b * m1[q];
+          if constexpr (NEXT) {
+            acc[0] = fma(wa, vn[q].x, acc[0]);
+            acc[0] = fma(wb, vn[q].y, acc[0]);
+          }
+          if constexpr (NORM) {
+            acc[1] = fma(wa, a, acc[1]);
+            acc[1] = fma(wb, b, acc[1]);
+          }
+        }
+      }
+    }
+  }
+  finish_reduce<2>(acc, wk, out);
+}
+
 template <bool PREV, bool NEXT, bool NORM, bool W2>
 static int mgs_launch(double* w, const double* vprev, const double* hprev, const double* vnext,
                       double* w2, const double* v2prev, const uint8_t* mult, long long P,
                       RedWork wk, double* out, cudaStream_t st) {
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool vec = (P % 2 == 0) && mult && al(w) && (!PREV || al(vprev)) && (!NEXT || al(vnext)) &&
+                   (!W2 || (al(w2) && al(v2prev))) && ((reinterpret_cast<uintptr_t>(mult) & 1) == 0);
+  if (vec) {
+    const long long P2 = P / 2;
+    unsigned blocks = RED_BLOCKS;
+    long long need = (P2 + RED_THREADS - 1) / RED_THREADS;
+    if (need < (long long)blocks) blocks = (unsigned)(need > 0 ? need : 1);
+    mgs2_kernel<PREV, NEXT, NORM, W2><<<blocks, RED_THREADS, 0, st>>>(w, vprev, hprev, vnext, w2, v2prev,
+                                                                      mult, P2, wk, out);
+    return check_launch("mgs_step");
+  }
   MgsOp<PREV, NEXT, NORM, W2> op{w, vprev, hprev, vnext, w2, v2prev, mult, 0.0};
   return launch_map_reduce(op, P, wk, out, st, "mgs_step");
 }
