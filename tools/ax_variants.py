@@ -13,11 +13,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2207_07098_b200", "variants")
 VARIANTS = {
-    "generic_minb5u2": "-DSF_AX_GENERIC8 -DSF_AX_MINB=5 -DSF_AX_UNROLL=2",
-    "n8_minb2_epb4": "-DSF_AX8_MINB=2 -DSF_AX8_EPB=4",
-    "n8_minb3_epb4": "-DSF_AX8_MINB=3 -DSF_AX8_EPB=4",
-    "n8_minb2_epb2": "-DSF_AX8_MINB=2 -DSF_AX8_EPB=2",
-    "n8_minb4_epb2": "-DSF_AX8_MINB=4 -DSF_AX8_EPB=2",
+    "padded_minb4": "-DSF_AX_MINB=4",
+    "padded_minb5u1": "-DSF_AX_MINB=5 -DSF_AX_UNROLL=1",
+    "padded_minb6": "-DSF_AX_MINB=6",
 }
 
 
