@@ -198,6 +198,43 @@ def time_kernels(sp, op, u, reps=20):
     return res
 
 
+#: dram__bytes_read.sum + dram__bytes_write.sum per launch of the MGS pass, from
+#: the ncu --set full capture committed under profiles/ (keyed by mesh size)
+MGS_TRAFFIC = {}
+
+
+def time_mgs(sp, w0, reps=20):
+    """CUDA-event time of one GMRES MGS pass (w -= h v_prev; <w, v_next>_1/mult)
+    on full-size fields; returns (seconds, algorithmic bytes = P * 33)."""
+    import torch
+
+    from paper_2207_07098_b200 import _device, _lib
+
+    st = torch.cuda.current_stream()
+    w = w0.clone()
+    vp = torch.randn_like(w0)
+    vn = torch.randn_like(w0)
+    h = torch.tensor([1e-9, 0.0], dtype=torch.float64, device=w0.device)
+    out = torch.zeros(2, dtype=torch.float64, device=w0.device)
+    wk = _device.workspace(w0.device)
+    P = sp.n_points
+
+    def fn():
+        _lib.call("sf_mgs_step_f64", _lib.ptr(w), _lib.ptr(vp), _lib.ptr(h), _lib.ptr(vn), None, None,
+                  _lib.ptr(sp.gs.mult8), 0, P, *wk.args(), _lib.ptr(out), st.cuda_stream)
+
+    for _ in range(3):
+        fn()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    torch.cuda.synchronize()
+    for a, b in evs:
+        a.record(st)
+        fn()
+        b.record(st)
+    torch.cuda.synchronize()
+    return float(np.mean([a.elapsed_time(b) for a, b in evs])) * 1e-3, P * 33
+
+
 # ----------------------------------------------------------------------------- CPU baseline
 
 def cpu_poisson_sample():
@@ -389,10 +426,15 @@ def bench_tgv(args, world, rank, dev):
     e2e = {"value": P * args.steps / te / 1e9, "unit": "GDOF/s",
            "h2d_bytes_per_step": P * 3 * 8, "d2h_bytes_per_step": P * 3 * 8}
     op = st.apply_p
-    kt = time_kernels(sp, op, torch.randn(sp.shape, dtype=torch.float64, device=dev))
+    probe = torch.randn(sp.shape, dtype=torch.float64, device=dev)
+    kt = time_kernels(sp, op, probe)
     pk, src = peaks()
     nbytes = ax_dssum_bytes(sp, op.masked)
     achieved = nbytes / (kt["ax"] + kt["dssum"]) / 1e9
+    # dominant kernel of the step: the GMRES modified-Gram-Schmidt pass
+    # (w -= h v_{i-1}; <w, v_i>) -- ~70 % of the step at 64^3 (profiles/)
+    t_mgs, mgs_bytes = time_mgs(sp, probe)
+    mgs_gbs = mgs_bytes / t_mgs / 1e9
     return {
         "metric": "GDOF/s per time step (TGV, lx=8)",
         "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -406,10 +448,14 @@ def bench_tgv(args, world, rank, dev):
                    "l2": "inputs larger than L2" if P * 8 * 6 / world > 126e6 else "working set may be L2-resident",
                    "parallelism": (f"element partition x{world} (z-slabs), NCCL halo exchange + allgather dots"
                                    if world > 1 else "single")},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm_gbs"], "traffic": None,
-                     "kernel": "ax_helm+dssum (pressure Poisson operator, rank 0)", "algorithmic_bytes": nbytes,
-                     "ax_us": kt["ax"] * 1e6, "dssum_us": kt["dssum"] * 1e6, "peak_source": src},
+        "roofline": {"bound": "hbm", "achieved": mgs_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": mgs_gbs / pk["hbm_gbs"], "traffic": MGS_TRAFFIC.get(ne),
+                     "kernel": "mgs2_kernel<true,true,false,false> (GMRES MGS pass, rank 0)",
+                     "algorithmic_bytes": mgs_bytes, "us": t_mgs * 1e6, "peak_source": src,
+                     "ax_dssum": {"achieved": achieved, "frac": achieved / pk["hbm_gbs"],
+                                  "algorithmic_bytes": nbytes, "ax_us": kt["ax"] * 1e6,
+                                  "dssum_us": kt["dssum"] * 1e6,
+                                  "kernel": "ax_helm + dssum (pressure Poisson operator)"}},
         "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
     }
 
