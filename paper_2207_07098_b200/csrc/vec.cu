@@ -216,12 +216,18 @@ struct MgsOp {
 // Vectorised MGS pass: 16-byte loads of point pairs (each warp instruction moves
 // a contiguous 512 B run), 4 pairs per lane in flight.  Same per-point arithmetic
 // as MgsOp; used when P is even and every array is 16-byte aligned.
+#ifndef SF_MGS_MINB
+#define SF_MGS_MINB 4
+#endif
+#ifndef SF_MGS_U
+#define SF_MGS_U 2
+#endif
 template <bool PREV, bool NEXT, bool NORM, bool W2>
-__global__ void __launch_bounds__(RED_THREADS)
+__global__ void __launch_bounds__(RED_THREADS, SF_MGS_MINB)
 mgs2_kernel(double* __restrict__ w, const double* __restrict__ vprev, const double* __restrict__ hprev,
             const double* __restrict__ vnext, double* __restrict__ w2, const double* __restrict__ v2prev,
             const uint8_t* __restrict__ mult, long long P2, RedWork wk, double* __restrict__ out) {
-  constexpr int U = 4;
+  constexpr int U = SF_MGS_U;
   __shared__ double im_tab[256];
   init_im_tab(im_tab);
   __syncthreads();

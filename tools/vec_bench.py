@@ -31,7 +31,8 @@ def main():
 
     P = int(float(sys.argv[1]) * 1e6) if len(sys.argv) > 1 else 134217728
     dev = torch.device("cuda", 0)
-    _lib.load()
+    _lib.load(os.environ.get("SF_LIB", _lib.LIB_PATH))
+    print("library:", os.environ.get("SF_LIB", _lib.LIB_PATH))
     w = torch.randn(P, dtype=torch.float64, device=dev)
     v1 = torch.randn(P, dtype=torch.float64, device=dev)
     v2 = torch.randn(P, dtype=torch.float64, device=dev)
