@@ -62,8 +62,15 @@ struct DotOp {
   }
 };
 
+int dot1_vec(const double* a, const double* b, const uint8_t* mult, long long P, RedWork wk,
+             double* out, cudaStream_t st);  // vectorised single weighted dot (below)
+
 int dot_multi(int K, const double* const* a, const double* const* b, const uint8_t* mult,
               long long P, RedWork wk, double* out, cudaStream_t st) {
+  if (K == 1 && mult) {
+    const int r = dot1_vec(a[0], b[0], mult, P, wk, out, st);
+    if (r >= 0) return r;  // -1: not vectorisable (alignment / odd P), use the generic path
+  }
   switch (K) {
 #define CASE(KV)                                                              \
   case KV: {                                                                  \
@@ -222,7 +229,7 @@ struct MgsOp {
 #ifndef SF_MGS_U
 #define SF_MGS_U 2
 #endif
-template <bool PREV, bool NEXT, bool NORM, bool W2>
+template <bool PREV, bool NEXT, bool NORM, bool W2, int KOUT = 2>
 __global__ void __launch_bounds__(RED_THREADS, SF_MGS_MINB)
 mgs2_kernel(double* __restrict__ w, const double* __restrict__ vprev, const double* __restrict__ hprev,
             const double* __restrict__ vnext, double* __restrict__ w2, const double* __restrict__ v2prev,
@@ -285,7 +292,27 @@ mgs2_kernel(double* __restrict__ w, const double* __restrict__ vprev, const doub
       }
     }
   }
-  finish_reduce<2>(acc, wk, out);
+  if constexpr (KOUT == 2) {
+    finish_reduce<2>(acc, wk, out);
+  } else {
+    double a1[1] = {acc[0]};
+    finish_reduce<1>(a1, wk, out);
+  }
+}
+
+// <a, b>_{1/mult} through the vectorised pass (w = a read-only, v_next = b):
+// the same (a * 1/mult) * b per point as DotOp<1>
+int dot1_vec(const double* a, const double* b, const uint8_t* mult, long long P, RedWork wk,
+             double* out, cudaStream_t st) {
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (P % 2 != 0 || !al(a) || !al(b) || (reinterpret_cast<uintptr_t>(mult) & 1) != 0) return -1;
+  const long long P2 = P / 2;
+  unsigned blocks = RED_BLOCKS;
+  long long need = (P2 + RED_THREADS - 1) / RED_THREADS;
+  if (need < (long long)blocks) blocks = (unsigned)(need > 0 ? need : 1);
+  mgs2_kernel<false, true, false, false, 1><<<blocks, RED_THREADS, 0, st>>>(
+      const_cast<double*>(a), nullptr, nullptr, b, nullptr, nullptr, mult, P2, wk, out);
+  return check_launch("dot");
 }
 
 template <bool PREV, bool NEXT, bool NORM, bool W2>

@@ -263,4 +263,6 @@ def test_generic_solver_path_matches_fused(cuda):
     fused = krylov.pcg(A, rhs, tol=1e-8, max_iter=500, precond=M, dot=sp.gs.dot)
     generic = krylov.pcg(lambda v: A(v), rhs, tol=1e-8, max_iter=500, precond=lambda r: M(r), dot=sp.gs.dot)
     assert fused.iterations == generic.iterations
-    assert rel_err(fused.x.cpu().numpy(), generic.x.cpu().numpy()) < 1e-10
+    # the generic path rounds x += alpha p in two steps (torch), the fused one
+    # uses DFMA: after 44 iterations the iterates differ at the ~1e-10 level
+    assert rel_err(fused.x.cpu().numpy(), generic.x.cpu().numpy()) < 1e-8
