@@ -178,6 +178,28 @@ int sf_bdf_ext_f64(double* vhat, double* omega, const double* const* vel, const 
                    long long P3, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Multi-GPU: NVLink peer-memory reduction (replaces the NCCL all-gather of
+ * glsc3 partials on the Krylov critical path)
+ * ------------------------------------------------------------------------- */
+
+/* size of a cudaIpcMemHandle_t in bytes */
+int sf_ipc_handle_bytes(void);
+/* doubles in one rank's mailbox (double-banked slots of up to 4 partials) */
+int sf_peer_mailbox_doubles(int world);
+/* zero-initialised cudaMalloc allocation (IPC handles name whole allocations) */
+int sf_dev_alloc_zero(long long bytes, void** out);
+int sf_dev_free(void* p);
+int sf_ipc_get_handle(void* dev_ptr, unsigned char* handle_out);
+int sf_ipc_open_handle(const unsigned char* handle, void** dev_ptr_out);
+int sf_ipc_close_handle(void* dev_ptr);
+/* out[0..k) = sum over ranks (rank order) of every rank's in[0..k), k <= 4.
+ * boxes: HOST array of `world` mailbox pointers (own + IPC-opened peers);
+ * seq: call number, strictly increasing by 1 per call on every rank; error: device
+ * flag set to 1 if a peer did not arrive within 5 s.  in and out may alias. */
+int sf_peer_allreduce_f64(double* const* boxes, int world, int rank, unsigned long long seq,
+                          unsigned* error, const double* in, int k, double* out, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Function-space setup (space.py:182-245), bit-identical to build_space
  * ------------------------------------------------------------------------- */
 

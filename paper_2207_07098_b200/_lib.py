@@ -46,6 +46,14 @@ _SIGS = {
     "sf_cdtp_f64": [_vp, _i, _vp, _vp, _vp, _vp, _ll, _i, _vp],
     "sf_cfl_f64": [_vp, _vp, _vp, _i, _ll, _vp, _i, _vp],
     "sf_bdf_ext_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _ll, _vp],
+    "sf_ipc_handle_bytes": [],
+    "sf_peer_mailbox_doubles": [_i],
+    "sf_dev_alloc_zero": [_ll, ctypes.POINTER(_vp)],
+    "sf_dev_free": [_vp],
+    "sf_ipc_get_handle": [_vp, ctypes.c_char_p],
+    "sf_ipc_open_handle": [ctypes.c_char_p, ctypes.POINTER(_vp)],
+    "sf_ipc_close_handle": [_vp],
+    "sf_peer_allreduce_f64": [_vp, _i, _i, ctypes.c_ulonglong, _vp, _vp, _i, _vp, _vp],
     "sf_trilinear_coords_f64": [_vp, _vp, _i, _ll, _vp, _vp],
     "sf_metrics_f64": [_vp, _vp, _i, _vp, _ll, _vp, _vp, _vp, _vp, _vp],
 }

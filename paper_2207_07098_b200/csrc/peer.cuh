@@ -1,0 +1,96 @@
+// Peer-memory (NVLink) reduction context and the device routine shared by
+// peer.cu (standalone kernel) and the fused Krylov kernels (vec.cu).
+#pragma once
+#include <cstring>
+
+#include "common.cuh"
+
+#define PEER_MAX_RANKS 8
+#define PEER_KMAX 4
+#define PEER_TIMEOUT_NS 5000000000ull  // 5 s: a rank that never arrives is an error, not a hang
+
+namespace sf {
+
+struct PeerCtx {
+  double* box[PEER_MAX_RANKS];  // every rank's mailbox (own + IPC-mapped peers)
+  int world;
+  int rank;
+  unsigned long long seq;       // call sequence number (>= 1), also selects the bank
+  unsigned* error;              // set to 1 on poll timeout
+  // slot layout: [bank][rank][PEER_KMAX values, flag word, padding] = 64 B per slot
+  static constexpr int SLOT = 8;
+  __host__ __device__ static constexpr int slot_off(int bank, int r) {
+    return (bank * PEER_MAX_RANKS + r) * SLOT;
+  }
+  static int box_doubles(int) { return 2 * PEER_MAX_RANKS * SLOT; }
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Executed by ONE full warp.  vals[0..k) are this rank's partials (any lane may
+// hold them; lane 0's copy is used); out[0..k) receives the rank-order sum on
+// every rank.  Returns false (and sets *c.error) on timeout.
+__device__ __forceinline__ bool peer_allreduce_warp(const PeerCtx& c, const double* vals, int k,
+                                                    double* out) {
+  const int lane = threadIdx.x & 31;
+  const int bank = (int)(c.seq & 1ull);
+  double v[PEER_KMAX];
+#pragma unroll
+  for (int j = 0; j < PEER_KMAX; ++j) v[j] = __shfl_sync(0xffffffffu, j < k ? vals[j] : 0.0, 0);
+  // 1. publish into every rank's mailbox (lane r -> rank r; NVLink stores for peers)
+  if (lane < c.world) {
+    double* dst = c.box[lane] + PeerCtx::slot_off(bank, c.rank);
+#pragma unroll
+    for (int j = 0; j < PEER_KMAX; ++j)
+      if (j < k) dst[j] = v[j];
+    __threadfence_system();
+    st_release_sys(reinterpret_cast<unsigned long long*>(dst + PEER_KMAX), c.seq);
+  }
+  // 2. lane r waits (acquire) for rank r's slot in my mailbox and reads it
+  const double* mine = c.box[c.rank];
+  bool ok = true;
+  double sv[PEER_KMAX];
+#pragma unroll
+  for (int j = 0; j < PEER_KMAX; ++j) sv[j] = 0.0;
+  if (lane < c.world) {
+    const double* slot = mine + PeerCtx::slot_off(bank, lane);
+    const unsigned long long* flag = reinterpret_cast<const unsigned long long*>(slot + PEER_KMAX);
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_sys(flag) != c.seq) {
+      if (global_ns() - t0 > PEER_TIMEOUT_NS) { ok = false; break; }
+    }
+#pragma unroll
+    for (int j = 0; j < PEER_KMAX; ++j)
+      if (j < k) sv[j] = ((volatile const double*)slot)[j];
+  }
+  ok = __all_sync(0xffffffffu, ok);
+  if (!ok) {
+    if (lane == 0) atomicExch(c.error, 1u);
+    return false;
+  }
+  // 3. rank-order sum (identical on every rank)
+  double acc[PEER_KMAX];
+#pragma unroll
+  for (int j = 0; j < PEER_KMAX; ++j) acc[j] = 0.0;
+  for (int r = 0; r < c.world; ++r) {
+#pragma unroll
+    for (int j = 0; j < PEER_KMAX; ++j) acc[j] = __dadd_rn(acc[j], __shfl_sync(0xffffffffu, sv[j], r));
+  }
+  if (lane == 0)
+    for (int j = 0; j < k; ++j) out[j] = acc[j];
+  return true;
+}
+
+}  // namespace sf

@@ -39,6 +39,15 @@ class Comm:
         else:
             self.rank, self.world = 0, 1
         self.collectives = 0
+        self.peer = None
+        if (self.world > 1 and torch.cuda.is_available() and dist.get_backend(group) == "nccl"
+                and os.environ.get("SEMFLOW_B200_PEER", "1") != "0"):
+            self.peer = _PeerReducer(self)
+
+    def close(self):
+        if self.peer is not None:
+            self.peer.close()
+            self.peer = None
 
     @property
     def active(self):
@@ -50,6 +59,9 @@ class Comm:
             return t
         k = t.numel()
         self.collectives += 1
+        if t.is_cuda and self.peer is not None and k <= _PeerReducer.KMAX and t.is_contiguous():
+            self.peer.allreduce_(t)
+            return t
         if t.is_cuda:
             buf = torch.empty(self.world * k, dtype=t.dtype, device=t.device)
             self.dist.all_gather_into_tensor(buf, t.contiguous().view(-1), group=self.group)
@@ -96,6 +108,66 @@ class Comm:
         self.collectives += 1
 
 
+class _PeerReducer:
+    """NVLink mailboxes for the glsc3 allreduce (csrc/peer.cu).
+
+    Each rank cudaMallocs a mailbox, exports it with CUDA IPC, and maps every
+    peer's; a reduction is then one 32-thread kernel (P2P stores + acquire polls)
+    instead of an NCCL all-gather plus a combine kernel.  Same rank-order sum.
+    """
+
+    KMAX = 4
+
+    def __init__(self, comm):
+        import ctypes
+
+        lib = _lib.load()
+        self.comm = comm
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        nbytes = 8 * lib.sf_peer_mailbox_doubles(comm.world)
+        own = ctypes.c_void_p()
+        _lib.call("sf_dev_alloc_zero", nbytes, ctypes.byref(own))
+        self.own = own.value
+        hb = lib.sf_ipc_handle_bytes()
+        h = ctypes.create_string_buffer(hb)
+        _lib.call("sf_ipc_get_handle", self.own, h)
+        handles = [None] * comm.world
+        comm.dist.all_gather_object(handles, h.raw, group=comm.group)
+        self.opened = []
+        ptrs = []
+        for r, hr in enumerate(handles):
+            if r == comm.rank:
+                ptrs.append(self.own)
+                continue
+            p = ctypes.c_void_p()
+            _lib.call("sf_ipc_open_handle", ctypes.create_string_buffer(hr, hb), ctypes.byref(p))
+            self.opened.append(p.value)
+            ptrs.append(p.value)
+        self.boxes = (ctypes.c_void_p * comm.world)(*ptrs)
+        self.error = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.seq = 0
+        torch.cuda.synchronize()
+        comm.dist.barrier(group=comm.group)
+
+    def allreduce_(self, t):
+        self.seq += 1
+        _lib.call("sf_peer_allreduce_f64", self.boxes, self.comm.world, self.comm.rank, self.seq,
+                  _lib.ptr(self.error), _lib.ptr(t), t.numel(), _lib.ptr(t), _lib.stream_ptr(t.device))
+
+    def check(self):
+        if int(self.error.item()):
+            raise RuntimeError("peer allreduce timed out (a rank did not arrive within 5 s)")
+
+    def close(self):
+        for p in self.opened:
+            _lib.call("sf_ipc_close_handle", p)
+        self.opened = []
+        if self.own:
+            torch.cuda.synchronize()
+            _lib.call("sf_dev_free", self.own)
+            self.own = None
+
+
 _SINGLE = None
 
 
@@ -106,6 +178,7 @@ def single():
         _SINGLE.dist = None
         _SINGLE.group = None
         _SINGLE.rank, _SINGLE.world, _SINGLE.collectives = 0, 1, 0
+        _SINGLE.peer = None
     return _SINGLE
 
 
