@@ -24,9 +24,10 @@ namespace sf {
 
 __global__ void peer_allreduce_kernel(PeerCtx c, const double* __restrict__ in, int k,
                                       double* __restrict__ out) {
-  double v[PEER_KMAX];
-  for (int j = 0; j < k; ++j) v[j] = in[j];
-  peer_allreduce_warp(c, v, k, out);
+  const int lane = threadIdx.x & 31;
+  const double mine = lane < k ? in[lane] : 0.0;
+  __syncwarp();  // every lane has read `in` before lane 0 may overwrite it (in == out)
+  peer_allreduce_warp(c, mine, k, out);
 }
 
 int peer_allreduce(const PeerCtx& c, const double* in, int k, double* out, cudaStream_t st) {

@@ -39,16 +39,16 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
-// Executed by ONE full warp.  vals[0..k) are this rank's partials (any lane may
-// hold them; lane 0's copy is used); out[0..k) receives the rank-order sum on
-// every rank.  Returns false (and sets *c.error) on timeout.
-__device__ __forceinline__ bool peer_allreduce_warp(const PeerCtx& c, const double* vals, int k,
+// Executed by ONE full warp.  Lane j (< k) holds this rank's partial j in
+// `mine_j`; out[0..k) receives the rank-order sum on every rank (written by lane
+// 0).  Returns false (and sets *c.error) on timeout.
+__device__ __forceinline__ bool peer_allreduce_warp(const PeerCtx& c, double mine_j, int k,
                                                     double* out) {
   const int lane = threadIdx.x & 31;
   const int bank = (int)(c.seq & 1ull);
   double v[PEER_KMAX];
 #pragma unroll
-  for (int j = 0; j < PEER_KMAX; ++j) v[j] = __shfl_sync(0xffffffffu, j < k ? vals[j] : 0.0, 0);
+  for (int j = 0; j < PEER_KMAX; ++j) v[j] = __shfl_sync(0xffffffffu, mine_j, j);
   // 1. publish into every rank's mailbox (lane r -> rank r; NVLink stores for peers)
   if (lane < c.world) {
     double* dst = c.box[lane] + PeerCtx::slot_off(bank, c.rank);
