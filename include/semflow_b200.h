@@ -199,6 +199,19 @@ int sf_ipc_close_handle(void* dev_ptr);
 int sf_peer_allreduce_f64(double* const* boxes, int world, int rank, unsigned long long seq,
                           unsigned* error, const double* in, int k, double* out, void* stream);
 
+/* Fused compute + collective: sf_mgs_step_f64 / the weighted glsc3 whose last
+ * thread block publishes the rank's partials to every peer over NVLink and
+ * returns the rank-order global sums in `out` (no separate collective).  The
+ * peer arguments are those of sf_peer_allreduce_f64. */
+int sf_mgs_step_peer_f64(double* w, const double* vprev, const double* hprev, const double* vnext,
+                         double* w2, const double* v2prev, const uint8_t* mult, int want_norm,
+                         long long P, double* partials, unsigned* counter, double* out,
+                         double* const* boxes, int world, int rank, unsigned long long seq,
+                         unsigned* error, void* stream);
+int sf_glsc3_peer_f64(const double* a, const double* b, const uint8_t* mult, long long P,
+                      double* partials, unsigned* counter, double* out, double* const* boxes,
+                      int world, int rank, unsigned long long seq, unsigned* error, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Function-space setup (space.py:182-245), bit-identical to build_space
  * ------------------------------------------------------------------------- */

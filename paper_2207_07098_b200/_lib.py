@@ -54,6 +54,9 @@ _SIGS = {
     "sf_ipc_open_handle": [ctypes.c_char_p, ctypes.POINTER(_vp)],
     "sf_ipc_close_handle": [_vp],
     "sf_peer_allreduce_f64": [_vp, _i, _i, ctypes.c_ulonglong, _vp, _vp, _i, _vp, _vp],
+    "sf_mgs_step_peer_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _ll, _vp, _vp, _vp,
+                             _vp, _i, _i, ctypes.c_ulonglong, _vp, _vp],
+    "sf_glsc3_peer_f64": [_vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp, _i, _i, ctypes.c_ulonglong, _vp, _vp],
     "sf_trilinear_coords_f64": [_vp, _vp, _i, _ll, _vp, _vp],
     "sf_metrics_f64": [_vp, _vp, _i, _vp, _ll, _vp, _vp, _vp, _vp, _vp],
 }

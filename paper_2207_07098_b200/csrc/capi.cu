@@ -8,6 +8,7 @@
 
 #include "common.cuh"
 #include "reduce.cuh"
+#include "peer.cuh"
 
 #include "../../include/semflow_b200.h"
 
@@ -52,7 +53,10 @@ int cg_update(double*, double*, const double*, const double*, const double*, con
 int cg_direction(double*, const double*, const double*, const double*, const double*, long long,
                  cudaStream_t);
 int mgs_step(double*, const double*, const double*, const double*, double*, const double*,
-             const uint8_t*, int, long long, RedWork, double*, cudaStream_t);
+             const uint8_t*, int, long long, RedWork, double*, cudaStream_t, const PeerCtx*);
+int dot1_vec(const double*, const double*, const uint8_t*, long long, RedWork, double*, cudaStream_t,
+             const PeerCtx*);
+int peer_allreduce(const PeerCtx&, const double*, int, double*, cudaStream_t);
 int lincomb(double*, const double*, const double* const*, const double*, const double*, int,
             long long, cudaStream_t);
 int residual(double*, const double*, const double*, const uint8_t*, long long, RedWork, double*,
@@ -160,7 +164,50 @@ int sf_mgs_step_f64(double* w, const double* vprev, const double* hprev, const d
                     double* w2, const double* v2prev, const uint8_t* mult, int want_norm,
                     long long P, double* partials, unsigned* counter, double* out, void* stream) {
   return mgs_step(w, vprev, hprev, vnext, w2, v2prev, mult, want_norm, P,
-                  RedWork{partials, counter}, out, as_stream(stream));
+                  RedWork{partials, counter}, out, as_stream(stream), nullptr);
+}
+
+static int make_peer(PeerCtx& c, double* const* boxes, int world, int rank, unsigned long long seq,
+                     unsigned* error) {
+  if (world < 1 || world > PEER_MAX_RANKS || rank < 0 || rank >= world) {
+    set_error("peer context: bad world/rank %d/%d", world, rank);
+    return SF_ERR_ARG;
+  }
+  c = PeerCtx{};
+  for (int r = 0; r < world; ++r) c.box[r] = boxes[r];
+  c.world = world;
+  c.rank = rank;
+  c.seq = seq;
+  c.error = error;
+  return SF_OK;
+}
+
+int sf_mgs_step_peer_f64(double* w, const double* vprev, const double* hprev, const double* vnext,
+                         double* w2, const double* v2prev, const uint8_t* mult, int want_norm,
+                         long long P, double* partials, unsigned* counter, double* out,
+                         double* const* boxes, int world, int rank, unsigned long long seq,
+                         unsigned* error, void* stream) {
+  PeerCtx c;
+  int st = make_peer(c, boxes, world, rank, seq, error);
+  if (st != SF_OK) return st;
+  return mgs_step(w, vprev, hprev, vnext, w2, v2prev, mult, want_norm, P,
+                  RedWork{partials, counter}, out, as_stream(stream), &c);
+}
+
+int sf_glsc3_peer_f64(const double* a, const double* b, const uint8_t* mult, long long P,
+                      double* partials, unsigned* counter, double* out, double* const* boxes,
+                      int world, int rank, unsigned long long seq, unsigned* error, void* stream) {
+  PeerCtx c;
+  int st = make_peer(c, boxes, world, rank, seq, error);
+  if (st != SF_OK) return st;
+  const int r = mult ? dot1_vec(a, b, mult, P, RedWork{partials, counter}, out, as_stream(stream), &c)
+                     : -1;
+  if (r >= 0) return r;
+  const double* pa[1] = {a};
+  const double* pb[1] = {b};
+  st = dot_multi(1, pa, pb, mult, P, RedWork{partials, counter}, out, as_stream(stream));
+  if (st != SF_OK) return st;
+  return peer_allreduce(c, out, 1, out, as_stream(stream));
 }
 
 int sf_lincomb_f64(double* x, const double* x0, const double* const* v, const double* coef,

@@ -13,6 +13,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "peer.cuh"
 
 namespace sf {
 
@@ -29,8 +30,10 @@ __device__ __forceinline__ void init_im_tab(double* tab) {
 }
 
 template <int K>
-__device__ __forceinline__ void finish_reduce(double (&acc)[K], RedWork wk, double* __restrict__ out) {
+__device__ __forceinline__ void finish_reduce(double (&acc)[K], RedWork wk, double* __restrict__ out,
+                                              const PeerCtx* peer = nullptr) {
   __shared__ double red[RED_THREADS / 32][K];
+  __shared__ double fin[K];
   __shared__ bool am_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -71,9 +74,18 @@ __device__ __forceinline__ void finish_reduce(double (&acc)[K], RedWork wk, doub
     for (int k = 0; k < K; ++k) {
       double v = 0.0;
       for (int w = 0; w < RED_THREADS / 32; ++w) v += red[w][k];
-      out[k] = v;
+      fin[k] = v;
     }
     *wk.counter = 0u;
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  if (peer != nullptr && peer->world > 1) {
+    // fused cross-GPU reduction over NVLink peer memory (peer.cuh): the rank's
+    // partials leave the kernel already summed over all ranks
+    peer_allreduce_warp(*peer, lane < K ? fin[lane] : 0.0, K, out);
+  } else if (lane < K) {
+    out[lane] = fin[lane];
   }
 }
 

@@ -21,6 +21,10 @@
 #include "reduce.cuh"
 
 namespace sf {
+int peer_allreduce(const PeerCtx& c, const double* in, int k, double* out, cudaStream_t st);
+}
+
+namespace sf {
 
 // weight 1/mult for point p, or 1 when no multiplicity is given (plain dot)
 __device__ __forceinline__ double wgt(const uint8_t* __restrict__ mult, long long p,
@@ -63,12 +67,12 @@ struct DotOp {
 };
 
 int dot1_vec(const double* a, const double* b, const uint8_t* mult, long long P, RedWork wk,
-             double* out, cudaStream_t st);  // vectorised single weighted dot (below)
+             double* out, cudaStream_t st, const PeerCtx* peer);  // vectorised weighted dot (below)
 
 int dot_multi(int K, const double* const* a, const double* const* b, const uint8_t* mult,
               long long P, RedWork wk, double* out, cudaStream_t st) {
   if (K == 1 && mult) {
-    const int r = dot1_vec(a[0], b[0], mult, P, wk, out, st);
+    const int r = dot1_vec(a[0], b[0], mult, P, wk, out, st, nullptr);
     if (r >= 0) return r;  // -1: not vectorisable (alignment / odd P), use the generic path
   }
   switch (K) {
@@ -233,7 +237,8 @@ template <bool PREV, bool NEXT, bool NORM, bool W2, int KOUT = 2>
 __global__ void __launch_bounds__(RED_THREADS, SF_MGS_MINB)
 mgs2_kernel(double* __restrict__ w, const double* __restrict__ vprev, const double* __restrict__ hprev,
             const double* __restrict__ vnext, double* __restrict__ w2, const double* __restrict__ v2prev,
-            const uint8_t* __restrict__ mult, long long P2, RedWork wk, double* __restrict__ out) {
+            const uint8_t* __restrict__ mult, long long P2, RedWork wk, double* __restrict__ out,
+            PeerCtx peer) {
   constexpr int U = SF_MGS_U;
   __shared__ double im_tab[256];
   init_im_tab(im_tab);
@@ -293,17 +298,17 @@ mgs2_kernel(double* __restrict__ w, const double* __restrict__ vprev, const doub
     }
   }
   if constexpr (KOUT == 2) {
-    finish_reduce<2>(acc, wk, out);
+    finish_reduce<2>(acc, wk, out, &peer);
   } else {
     double a1[1] = {acc[0]};
-    finish_reduce<1>(a1, wk, out);
+    finish_reduce<1>(a1, wk, out, &peer);
   }
 }
 
 // <a, b>_{1/mult} through the vectorised pass (w = a read-only, v_next = b):
 // the same (a * 1/mult) * b per point as DotOp<1>
 int dot1_vec(const double* a, const double* b, const uint8_t* mult, long long P, RedWork wk,
-             double* out, cudaStream_t st) {
+             double* out, cudaStream_t st, const PeerCtx* peer) {
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (P % 2 != 0 || !al(a) || !al(b) || (reinterpret_cast<uintptr_t>(mult) & 1) != 0) return -1;
   const long long P2 = P / 2;
@@ -311,14 +316,15 @@ int dot1_vec(const double* a, const double* b, const uint8_t* mult, long long P,
   long long need = (P2 + RED_THREADS - 1) / RED_THREADS;
   if (need < (long long)blocks) blocks = (unsigned)(need > 0 ? need : 1);
   mgs2_kernel<false, true, false, false, 1><<<blocks, RED_THREADS, 0, st>>>(
-      const_cast<double*>(a), nullptr, nullptr, b, nullptr, nullptr, mult, P2, wk, out);
+      const_cast<double*>(a), nullptr, nullptr, b, nullptr, nullptr, mult, P2, wk, out,
+      peer ? *peer : PeerCtx{});
   return check_launch("dot");
 }
 
 template <bool PREV, bool NEXT, bool NORM, bool W2>
 static int mgs_launch(double* w, const double* vprev, const double* hprev, const double* vnext,
                       double* w2, const double* v2prev, const uint8_t* mult, long long P,
-                      RedWork wk, double* out, cudaStream_t st) {
+                      RedWork wk, double* out, cudaStream_t st, const PeerCtx* peer) {
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool vec = (P % 2 == 0) && mult && al(w) && (!PREV || al(vprev)) && (!NEXT || al(vnext)) &&
                    (!W2 || (al(w2) && al(v2prev))) && ((reinterpret_cast<uintptr_t>(mult) & 1) == 0);
@@ -328,21 +334,24 @@ static int mgs_launch(double* w, const double* vprev, const double* hprev, const
     long long need = (P2 + RED_THREADS - 1) / RED_THREADS;
     if (need < (long long)blocks) blocks = (unsigned)(need > 0 ? need : 1);
     mgs2_kernel<PREV, NEXT, NORM, W2><<<blocks, RED_THREADS, 0, st>>>(w, vprev, hprev, vnext, w2, v2prev,
-                                                                      mult, P2, wk, out);
+                                                                      mult, P2, wk, out,
+                                                                      peer ? *peer : PeerCtx{});
     return check_launch("mgs_step");
   }
   MgsOp<PREV, NEXT, NORM, W2> op{w, vprev, hprev, vnext, w2, v2prev, mult, 0.0};
-  return launch_map_reduce(op, P, wk, out, st, "mgs_step");
+  const int r = launch_map_reduce(op, P, wk, out, st, "mgs_step");
+  if (r != SF_OK || peer == nullptr || peer->world <= 1) return r;
+  return peer_allreduce(*peer, out, 2, out, st);  // unfused fallback: separate peer kernel
 }
 
 int mgs_step(double* w, const double* vprev, const double* hprev, const double* vnext, double* w2,
              const double* v2prev, const uint8_t* mult, int want_norm, long long P, RedWork wk,
-             double* out, cudaStream_t st) {
+             double* out, cudaStream_t st, const PeerCtx* peer) {
   if (w2 && !vprev) w2 = nullptr;  // w2 is only ever updated together with w
   const int code = (vprev ? 8 : 0) | (vnext ? 4 : 0) | (want_norm ? 2 : 0) | (w2 ? 1 : 0);
   switch (code) {
 #define C(CODE, A, B, N, W) \
-  case CODE: return mgs_launch<A, B, N, W>(w, vprev, hprev, vnext, w2, v2prev, mult, P, wk, out, st);
+  case CODE: return mgs_launch<A, B, N, W>(w, vprev, hprev, vnext, w2, v2prev, mult, P, wk, out, st, peer);
     C(0, false, false, false, false) C(2, false, false, true, false)
     C(4, false, true, false, false) C(6, false, true, true, false)
     C(8, true, false, false, false) C(9, true, false, false, true)

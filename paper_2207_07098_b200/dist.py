@@ -149,6 +149,11 @@ class _PeerReducer:
         torch.cuda.synchronize()
         comm.dist.barrier(group=comm.group)
 
+    def fused_args(self):
+        """(boxes, world, rank, seq, error) for one fused kernel+collective call."""
+        self.seq += 1
+        return (self.boxes, self.comm.world, self.comm.rank, self.seq, _lib.ptr(self.error))
+
     def allreduce_(self, t):
         self.seq += 1
         _lib.call("sf_peer_allreduce_f64", self.boxes, self.comm.world, self.comm.rank, self.seq,

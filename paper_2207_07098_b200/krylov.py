@@ -60,6 +60,12 @@ class _Fused:
         self.comm = sp.comm
 
     def dot(self, a, b, out):
+        peer = self.comm.peer
+        if peer is not None and self.mult is not None:
+            # one kernel: local glsc3 + NVLink cross-rank sum in its last block
+            _lib.call("sf_glsc3_peer_f64", _lib.ptr(a), _lib.ptr(b), self.mult, self.P, *self.w.args(),
+                      _lib.ptr(out), *peer.fused_args(), self.st)
+            return
         _lib.call("sf_glsc3_f64", 1, _ptrs([a]), _ptrs([b]), self.mult, self.P, *self.w.args(),
                   _lib.ptr(out), self.st)
         self.comm.sum_(out)
@@ -72,7 +78,13 @@ class _Fused:
         self.comm.sum_(out[:len(pairs)])
 
     def mgs(self, out, *args):
-        """sf_mgs_step_f64 writing 2 partials to `out` (a 2-slot view), then allreduce."""
+        """sf_mgs_step_f64 writing 2 partials to `out` (a 2-slot view), then allreduce
+        -- fused into the same kernel over NVLink peer memory when available."""
+        peer = self.comm.peer
+        if peer is not None:
+            _lib.call("sf_mgs_step_peer_f64", *args, self.P, *self.w.args(), _lib.ptr(out),
+                      *peer.fused_args(), self.st)
+            return
         _lib.call("sf_mgs_step_f64", *args, self.P, *self.w.args(), _lib.ptr(out), self.st)
         self.comm.sum_(out)
 

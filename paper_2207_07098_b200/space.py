@@ -199,6 +199,11 @@ class GatherScatter:
     def dot_async(self, u, v, out):
         """Write <u, v>_{1/mult} (summed over ranks) into the device scalar ``out``."""
         w = _device.workspace(self.device)
+        peer = self.comm.peer
+        if peer is not None:
+            _lib.call("sf_glsc3_peer_f64", _lib.ptr(u), _lib.ptr(v), _lib.ptr(self.mult8), self.P, *w.args(),
+                      _lib.ptr(out), *peer.fused_args(), _lib.stream_ptr(self.device))
+            return out
         _lib.call("sf_glsc3_f64", 1, ctypes_ptrs([u]), ctypes_ptrs([v]), _lib.ptr(self.mult8), self.P,
                   *w.args(), _lib.ptr(out), _lib.stream_ptr(self.device))
         self.comm.sum_(out)
