@@ -20,7 +20,11 @@ def main():
     ne = int(sys.argv[1]) if len(sys.argv) > 1 else 32
     warm = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     steps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
-    sp, st, state = tgv_problem(ne, device="cuda:0")
+    from paper_2207_07098_b200 import dist
+
+    comm = dist.init_from_env()          # torchrun: one rank per GPU, rank 0 reports
+    dev = torch.device("cuda", torch.cuda.current_device())
+    sp, st, state = tgv_problem(ne, device=dev, comm=comm)
     for _ in range(warm):
         state, d = st.step(state)
     torch.cuda.synchronize()
@@ -29,8 +33,11 @@ def main():
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         for _ in range(steps):
             state, d = st.step(state)
-            print("step", d.step, "p_it", d.p_iterations, "v_it", d.v_iterations, "wall", round(d.wall_time, 4))
+            if comm.rank == 0:
+                print("step", d.step, "p_it", d.p_iterations, "v_it", d.v_iterations, "wall", round(d.wall_time, 4))
         torch.cuda.synchronize()
+    if comm.rank != 0:
+        return
     agg = {}
     total = 0.0
     for ev in prof.events():
