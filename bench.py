@@ -221,7 +221,7 @@ def time_mgs(sp, w0, reps=20):
 
     def fn():
         _lib.call("sf_mgs_step_f64", _lib.ptr(w), _lib.ptr(vp), _lib.ptr(h), _lib.ptr(vn), None, None,
-                  _lib.ptr(sp.gs.mult8), 0, P, *wk.args(), _lib.ptr(out), st.cuda_stream)
+                  _lib.ptr(sp.gs.mult8), 0, P, *wk.args(), _lib.ptr(out), None, st.cuda_stream)
 
     for _ in range(3):
         fn()

@@ -135,10 +135,20 @@ int sf_cg_direction_f64(double* p, const double* r, const double* invdiag, const
 
 /* One modified Gram-Schmidt step (gmres krylov.py:109-123; ProjectionSpace.absorb
  * krylov.py:229-231): if vprev, w -= (*hprev) vprev and, if w2, w2 -= (*hprev) v2prev;
- * out[0] = <w, vnext> (if vnext), out[1] = <w, w> (if want_norm). */
+ * out[0] = <w, vnext> (if vnext), out[1] = <w, w> (if want_norm).
+ * gate (device scalar, may be NULL): when *gate == 0 the pass is skipped entirely
+ * (the conditional second Gram-Schmidt sweep decided on the device; needs
+ * 16-byte aligned arrays and an even P). */
 int sf_mgs_step_f64(double* w, const double* vprev, const double* hprev, const double* vnext,
                     double* w2, const double* v2prev, const uint8_t* mult, int want_norm,
-                    long long P, double* partials, unsigned* counter, double* out, void* stream);
+                    long long P, double* partials, unsigned* counter, double* out,
+                    const double* gate, void* stream);
+
+/* GMRES Arnoldi bookkeeping on the device (krylov.py:110-123): blk holds the
+ * iteration's scalars (first sweep pairs at 2i, second sweep at o2 + 2i);
+ * phase 0 writes blk[o3] = (norm_after < 0.7071 norm_before) and blk[o3+1] =
+ * norm_after, phase 1 replaces blk[o3+1] by the second sweep's norm if blk[o3]. */
+int sf_gmres_gate_f64(double* blk, int j, int o2, int o3, int phase, void* stream);
 
 /* x = x0 + sum_i coef[i] * M v[i] accumulated in i order; v is a DEVICE array
  * of nv pointers, coef a device array (gmres update krylov.py:150-154 with
@@ -207,7 +217,7 @@ int sf_mgs_step_peer_f64(double* w, const double* vprev, const double* hprev, co
                          double* w2, const double* v2prev, const uint8_t* mult, int want_norm,
                          long long P, double* partials, unsigned* counter, double* out,
                          double* const* boxes, int world, int rank, unsigned long long seq,
-                         unsigned* error, void* stream);
+                         unsigned* error, const double* gate, void* stream);
 int sf_glsc3_peer_f64(const double* a, const double* b, const uint8_t* mult, long long P,
                       double* partials, unsigned* counter, double* out, double* const* boxes,
                       int world, int rank, unsigned long long seq, unsigned* error, void* stream);

@@ -38,7 +38,8 @@ _SIGS = {
     "sf_cg_init_f64": [_vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp],
     "sf_cg_update_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp],
     "sf_cg_direction_f64": [_vp, _vp, _vp, _vp, _vp, _ll, _vp],
-    "sf_mgs_step_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _ll, _vp, _vp, _vp, _vp],
+    "sf_mgs_step_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _ll, _vp, _vp, _vp, _vp, _vp],
+    "sf_gmres_gate_f64": [_vp, _i, _i, _i, _i, _vp],
     "sf_lincomb_f64": [_vp, _vp, _vp, _vp, _vp, _i, _ll, _vp],
     "sf_residual_f64": [_vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp],
     "sf_scale_div_f64": [_vp, _vp, _vp, _vp, _vp, _ll, _vp],
@@ -55,7 +56,7 @@ _SIGS = {
     "sf_ipc_close_handle": [_vp],
     "sf_peer_allreduce_f64": [_vp, _i, _i, ctypes.c_ulonglong, _vp, _vp, _i, _vp, _vp],
     "sf_mgs_step_peer_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _ll, _vp, _vp, _vp,
-                             _vp, _i, _i, ctypes.c_ulonglong, _vp, _vp],
+                             _vp, _i, _i, ctypes.c_ulonglong, _vp, _vp, _vp],
     "sf_glsc3_peer_f64": [_vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp, _i, _i, ctypes.c_ulonglong, _vp, _vp],
     "sf_trilinear_coords_f64": [_vp, _vp, _i, _ll, _vp, _vp],
     "sf_metrics_f64": [_vp, _vp, _i, _vp, _ll, _vp, _vp, _vp, _vp, _vp],

@@ -53,7 +53,9 @@ int cg_update(double*, double*, const double*, const double*, const double*, con
 int cg_direction(double*, const double*, const double*, const double*, const double*, long long,
                  cudaStream_t);
 int mgs_step(double*, const double*, const double*, const double*, double*, const double*,
-             const uint8_t*, int, long long, RedWork, double*, cudaStream_t, const PeerCtx*);
+             const uint8_t*, int, long long, RedWork, double*, cudaStream_t, const PeerCtx*,
+             const double*);
+int gmres_gate(double*, int, int, int, int, cudaStream_t);
 int dot1_vec(const double*, const double*, const uint8_t*, long long, RedWork, double*, cudaStream_t,
              const PeerCtx*);
 int peer_allreduce(const PeerCtx&, const double*, int, double*, cudaStream_t);
@@ -162,9 +164,14 @@ int sf_cg_direction_f64(double* p, const double* r, const double* invdiag, const
 
 int sf_mgs_step_f64(double* w, const double* vprev, const double* hprev, const double* vnext,
                     double* w2, const double* v2prev, const uint8_t* mult, int want_norm,
-                    long long P, double* partials, unsigned* counter, double* out, void* stream) {
+                    long long P, double* partials, unsigned* counter, double* out,
+                    const double* gate, void* stream) {
   return mgs_step(w, vprev, hprev, vnext, w2, v2prev, mult, want_norm, P,
-                  RedWork{partials, counter}, out, as_stream(stream), nullptr);
+                  RedWork{partials, counter}, out, as_stream(stream), nullptr, gate);
+}
+
+int sf_gmres_gate_f64(double* blk, int j, int o2, int o3, int phase, void* stream) {
+  return gmres_gate(blk, j, o2, o3, phase, as_stream(stream));
 }
 
 static int make_peer(PeerCtx& c, double* const* boxes, int world, int rank, unsigned long long seq,
@@ -186,12 +193,12 @@ int sf_mgs_step_peer_f64(double* w, const double* vprev, const double* hprev, co
                          double* w2, const double* v2prev, const uint8_t* mult, int want_norm,
                          long long P, double* partials, unsigned* counter, double* out,
                          double* const* boxes, int world, int rank, unsigned long long seq,
-                         unsigned* error, void* stream) {
+                         unsigned* error, const double* gate, void* stream) {
   PeerCtx c;
   int st = make_peer(c, boxes, world, rank, seq, error);
   if (st != SF_OK) return st;
   return mgs_step(w, vprev, hprev, vnext, w2, v2prev, mult, want_norm, P,
-                  RedWork{partials, counter}, out, as_stream(stream), &c);
+                  RedWork{partials, counter}, out, as_stream(stream), &c, gate);
 }
 
 int sf_glsc3_peer_f64(const double* a, const double* b, const uint8_t* mult, long long P,

@@ -238,7 +238,11 @@ __global__ void __launch_bounds__(RED_THREADS, SF_MGS_MINB)
 mgs2_kernel(double* __restrict__ w, const double* __restrict__ vprev, const double* __restrict__ hprev,
             const double* __restrict__ vnext, double* __restrict__ w2, const double* __restrict__ v2prev,
             const uint8_t* __restrict__ mult, long long P2, RedWork wk, double* __restrict__ out,
-            PeerCtx peer) {
+            PeerCtx peer, const double* __restrict__ gate) {
+  // gated pass (GMRES second MGS sweep decided on the device): every block of
+  // every rank reads the same global flag, so all skip together -- no partials,
+  // no counter update, no peer traffic
+  if (gate != nullptr && *gate == 0.0) return;
   constexpr int U = SF_MGS_U;
   __shared__ double im_tab[256];
   init_im_tab(im_tab);
@@ -317,14 +321,15 @@ int dot1_vec(const double* a, const double* b, const uint8_t* mult, long long P,
   if (need < (long long)blocks) blocks = (unsigned)(need > 0 ? need : 1);
   mgs2_kernel<false, true, false, false, 1><<<blocks, RED_THREADS, 0, st>>>(
       const_cast<double*>(a), nullptr, nullptr, b, nullptr, nullptr, mult, P2, wk, out,
-      peer ? *peer : PeerCtx{});
+      peer ? *peer : PeerCtx{}, nullptr);
   return check_launch("dot");
 }
 
 template <bool PREV, bool NEXT, bool NORM, bool W2>
 static int mgs_launch(double* w, const double* vprev, const double* hprev, const double* vnext,
                       double* w2, const double* v2prev, const uint8_t* mult, long long P,
-                      RedWork wk, double* out, cudaStream_t st, const PeerCtx* peer) {
+                      RedWork wk, double* out, cudaStream_t st, const PeerCtx* peer,
+                      const double* gate) {
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool vec = (P % 2 == 0) && mult && al(w) && (!PREV || al(vprev)) && (!NEXT || al(vnext)) &&
                    (!W2 || (al(w2) && al(v2prev))) && ((reinterpret_cast<uintptr_t>(mult) & 1) == 0);
@@ -335,8 +340,12 @@ static int mgs_launch(double* w, const double* vprev, const double* hprev, const
     if (need < (long long)blocks) blocks = (unsigned)(need > 0 ? need : 1);
     mgs2_kernel<PREV, NEXT, NORM, W2><<<blocks, RED_THREADS, 0, st>>>(w, vprev, hprev, vnext, w2, v2prev,
                                                                       mult, P2, wk, out,
-                                                                      peer ? *peer : PeerCtx{});
+                                                                      peer ? *peer : PeerCtx{}, gate);
     return check_launch("mgs_step");
+  }
+  if (gate != nullptr) {
+    set_error("mgs_step: a gated pass needs 16-byte aligned arrays and an even point count");
+    return SF_ERR_UNSUPPORTED;
   }
   MgsOp<PREV, NEXT, NORM, W2> op{w, vprev, hprev, vnext, w2, v2prev, mult, 0.0};
   const int r = launch_map_reduce(op, P, wk, out, st, "mgs_step");
@@ -346,12 +355,12 @@ static int mgs_launch(double* w, const double* vprev, const double* hprev, const
 
 int mgs_step(double* w, const double* vprev, const double* hprev, const double* vnext, double* w2,
              const double* v2prev, const uint8_t* mult, int want_norm, long long P, RedWork wk,
-             double* out, cudaStream_t st, const PeerCtx* peer) {
+             double* out, cudaStream_t st, const PeerCtx* peer, const double* gate) {
   if (w2 && !vprev) w2 = nullptr;  // w2 is only ever updated together with w
   const int code = (vprev ? 8 : 0) | (vnext ? 4 : 0) | (want_norm ? 2 : 0) | (w2 ? 1 : 0);
   switch (code) {
 #define C(CODE, A, B, N, W) \
-  case CODE: return mgs_launch<A, B, N, W>(w, vprev, hprev, vnext, w2, v2prev, mult, P, wk, out, st, peer);
+  case CODE: return mgs_launch<A, B, N, W>(w, vprev, hprev, vnext, w2, v2prev, mult, P, wk, out, st, peer, gate);
     C(0, false, false, false, false) C(2, false, false, true, false)
     C(4, false, true, false, false) C(6, false, true, true, false)
     C(8, true, false, false, false) C(9, true, false, false, true)
@@ -361,6 +370,30 @@ int mgs_step(double* w, const double* vprev, const double* hprev, const double* 
 #undef C
     default: set_error("mgs_step: bad argument combination"); return SF_ERR_ARG;
   }
+}
+
+// GMRES Arnoldi step bookkeeping on the device (krylov.py:110-123, 149), so the
+// host never has to stop the stream inside an iteration.  blk is the iteration's
+// scalar block: first-sweep pairs at [2i, 2i+1] (h_i, <w,w>), the second sweep
+// at o2 + 2i, and [o3] = reorthogonalise flag, [o3+1] = final norm.
+//   phase 0: flag = sqrt(na2) < 0.7071 * sqrt(nb2); norm = sqrt(na2)
+//   phase 1: if flag, norm = sqrt(na2 of the second sweep)
+// (IEEE sqrt and the same comparison the host evaluates: identical decision.)
+__global__ void gmres_gate_kernel(double* blk, int j, int o2, int o3, int phase) {
+  if (threadIdx.x != 0) return;
+  if (phase == 0) {
+    const double nb = sqrt(blk[1]);
+    const double na = sqrt(blk[2 * (j + 1) + 1]);
+    blk[o3] = (na < 0.7071 * nb) ? 1.0 : 0.0;
+    blk[o3 + 1] = na;
+  } else if (blk[o3] != 0.0) {
+    blk[o3 + 1] = sqrt(blk[o2 + 2 * (j + 1) + 1]);
+  }
+}
+
+int gmres_gate(double* blk, int j, int o2, int o3, int phase, cudaStream_t st) {
+  gmres_gate_kernel<<<1, 32, 0, st>>>(blk, j, o2, o3, phase);
+  return check_launch("gmres_gate");
 }
 
 // x = x0 + sum_i coef[i] * M v_i, accumulated in i order (krylov.py:153-154 for

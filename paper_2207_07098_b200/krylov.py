@@ -14,6 +14,7 @@ the reference line by line.
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -77,16 +78,20 @@ class _Fused:
                       self.mult, self.P, *self.w.args(), out.data_ptr() + 8 * c, self.st)
         self.comm.sum_(out[:len(pairs)])
 
-    def mgs(self, out, *args):
+    def mgs(self, out, *args, gate=None):
         """sf_mgs_step_f64 writing 2 partials to `out` (a 2-slot view), then allreduce
-        -- fused into the same kernel over NVLink peer memory when available."""
+        -- fused into the same kernel over NVLink peer memory when available.
+        ``gate``: device scalar; the pass is skipped when it is 0 (all ranks alike)."""
         peer = self.comm.peer
         if peer is not None:
             _lib.call("sf_mgs_step_peer_f64", *args, self.P, *self.w.args(), _lib.ptr(out),
-                      *peer.fused_args(), self.st)
+                      *peer.fused_args(), gate, self.st)
             return
-        _lib.call("sf_mgs_step_f64", *args, self.P, *self.w.args(), _lib.ptr(out), self.st)
-        self.comm.sum_(out)
+        _lib.call("sf_mgs_step_f64", *args, self.P, *self.w.args(), _lib.ptr(out), gate, self.st)
+        if gate is None:
+            self.comm.sum_(out)
+        elif self.comm.world > 1:
+            raise RuntimeError("gated MGS passes across ranks need the peer reducer")
 
     def read(self, t):
         h = t.to("cpu", non_blocking=False)
@@ -292,8 +297,127 @@ def _gmres_generic(apply_a, b, tol, max_iter, restart, precond, dot, x0):
     return SolveInfo(x, total, beta, res0, converged)
 
 
+def _pipelinable(F, b):
+    """The pipelined GMRES needs the gated (vectorised) MGS kernels and, across
+    ranks, the fused peer reduction."""
+    return (F.mult is not None and F.P % 2 == 0 and b.data_ptr() % 16 == 0
+            and (F.comm.world == 1 or F.comm.peer is not None)
+            and os.environ.get("SEMFLOW_B200_GMRES_PIPELINE", "1") != "0")
+
+
+def _gmres_pipelined(F, op, b, tol, max_iter, restart):
+    """GMRES with one Arnoldi step of look-ahead (same arithmetic as _gmres_fused).
+
+    Every Arnoldi step is enqueued without a host round trip: both Gram-Schmidt
+    sweeps, the reorthogonalisation test (sf_gmres_gate_f64: the same IEEE
+    comparison the host makes, evaluated on the device) and the normalisation of
+    the next basis vector.  Step j's scalars are copied to pinned memory behind
+    an event; while the host runs the Givens rotations and the convergence test
+    of step j, step j+1 is already executing.  When step j converges, the
+    speculatively computed step j+1 is discarded (nothing it wrote is used), so
+    the iterate, the iteration count and the residual are those of the
+    reference loop (krylov.py:95-160).  Look-ahead is skipped while the residual
+    estimate is within 10x of the tolerance.
+    """
+    P = F.P
+    dev = F.dev
+    mult = F.mult
+    wk = F.w.args()
+    x = torch.zeros_like(b)
+    r = b.clone()
+    s0 = torch.zeros(4, dtype=torch.float64, device=dev)
+    F.dot(r, r, s0[0:1])
+    beta = math.sqrt(F.read(s0[0:1])[0])
+    res0 = beta
+    if beta <= tol:
+        return SolveInfo(x, 0, beta, res0, True)
+    o2 = 2 * (restart + 2)           # second sweep within an iteration block
+    o3 = 4 * (restart + 2)           # [o3] reorth flag, [o3+1] final norm
+    S = o3 + 4
+    blk = torch.zeros((restart, S), dtype=torch.float64, device=dev)
+    host = torch.zeros((restart, S), dtype=torch.float64, pin_memory=True)
+    z = torch.empty_like(b)
+    total = 0
+    converged = False
+
+    def launch(j, V):
+        bl = blk[j]
+        bp = lambda i: bl.data_ptr() + 8 * i
+        F.precond_into(V[j], z)
+        w = torch.empty_like(b)
+        F.op.apply_into(z, w)
+        F.mgs(bl[0:2], _lib.ptr(w), None, None, _lib.ptr(V[0]), None, None, mult, 1)
+        for i in range(1, j + 1):
+            F.mgs(bl[2 * i:2 * i + 2], _lib.ptr(w), _lib.ptr(V[i - 1]), bp(2 * (i - 1)), _lib.ptr(V[i]),
+                  None, None, mult, 0)
+        F.mgs(bl[2 * (j + 1):2 * (j + 2)], _lib.ptr(w), _lib.ptr(V[j]), bp(2 * j), None, None, None, mult, 1)
+        _lib.call("sf_gmres_gate_f64", bl.data_ptr(), j, o2, o3, 0, F.st)
+        g8 = bp(o3)
+        F.mgs(bl[o2:o2 + 2], _lib.ptr(w), None, None, _lib.ptr(V[0]), None, None, mult, 0, gate=g8)
+        for i in range(1, j + 1):
+            F.mgs(bl[o2 + 2 * i:o2 + 2 * i + 2], _lib.ptr(w), _lib.ptr(V[i - 1]), bp(o2 + 2 * (i - 1)),
+                  _lib.ptr(V[i]), None, None, mult, 0, gate=g8)
+        F.mgs(bl[o2 + 2 * (j + 1):o2 + 2 * (j + 2)], _lib.ptr(w), _lib.ptr(V[j]), bp(o2 + 2 * j), None, None,
+              None, mult, 1, gate=g8)
+        _lib.call("sf_gmres_gate_f64", bl.data_ptr(), j, o2, o3, 1, F.st)
+        host[j].copy_(bl, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(dev))
+        # speculative next basis vector v_{j+1} = w / norm_after (krylov.py:149)
+        _lib.call("sf_scale_div_f64", _lib.ptr(w), _lib.ptr(w), None, None, bp(o3 + 1), P, F.st)
+        V.append(w)
+        return ev
+
+    while total < max_iter and not converged:
+        m = min(restart, max_iter - total)
+        v0 = torch.empty_like(b)
+        s0[1:2].fill_(beta)
+        _lib.call("sf_scale_div_f64", _lib.ptr(v0), _lib.ptr(r), None, None, s0.data_ptr() + 8, P, F.st)
+        V = [v0]
+        h = np.zeros((m + 1, m))
+        cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
+        g[0] = beta
+        j_end = 0
+        evs = {0: launch(0, V)}
+        for j in range(m):
+            if j + 1 < m and j + 1 not in evs and abs(g[j]) > 10.0 * tol:
+                evs[j + 1] = launch(j + 1, V)
+            evs[j].synchronize()
+            vals = host[j].tolist()
+            norm_before = math.sqrt(vals[1])
+            hcol = np.zeros(j + 2)
+            for i in range(j + 1):
+                hcol[i] = vals[2 * i]
+            norm_after = math.sqrt(vals[2 * (j + 1) + 1])
+            if norm_after < 0.7071 * norm_before:
+                for i in range(j + 1):
+                    hcol[i] += vals[o2 + 2 * i]
+                norm_after = math.sqrt(vals[o2 + 2 * (j + 1) + 1])
+            hcol[j + 1] = norm_after
+            _givens_column(hcol, j, cs, sn, g, total)
+            h[: j + 2, j] = hcol
+            total += 1
+            j_end = j + 1
+            happy = norm_after <= 1e-14 * max(norm_before, 1.0)
+            if abs(g[j + 1]) <= tol or happy or total >= max_iter:
+                break
+            if j + 1 < m and j + 1 not in evs:
+                evs[j + 1] = launch(j + 1, V)
+        y = _back_substitute(h, g, j_end)
+        _lincomb(x, x, V[:j_end], y, F.invdiag, P, dev, F.st)
+        ax = op(x)
+        _lib.call("sf_residual_f64", _lib.ptr(r), _lib.ptr(b), _lib.ptr(ax), mult, P, *wk, _lib.ptr(s0[0:1]), F.st)
+        F.comm.sum_(s0[0:1])
+        beta = math.sqrt(F.read(s0[0:1])[0])
+        if beta <= tol:
+            converged = True
+    return SolveInfo(x, total, beta, res0, converged)
+
+
 def _gmres_fused(op, b, tol, max_iter, restart, precond, dot, x0):
     F = _Fused(op, precond, dot)
+    if x0 is None and _pipelinable(F, b.contiguous()):
+        return _gmres_pipelined(F, op, b.contiguous(), tol, max_iter, restart)
     P = F.P
     dev = F.dev
     b = b.contiguous()
@@ -488,7 +612,7 @@ class ProjectionSpace:
                   _lib.ptr(self.xs[i]), _lib.ptr(d) if i else None, _lib.ptr(v2prev), F.mult, 0)
         if k:
             _lib.call("sf_mgs_step_f64", _lib.ptr(ad), _lib.ptr(self.axs[k - 1]), sp(2 + 2 * (k - 1)), None,
-                      _lib.ptr(d), _lib.ptr(self.xs[k - 1]), F.mult, 0, F.P, *wk, sp(2 + 2 * k), F.st)
+                      _lib.ptr(d), _lib.ptr(self.xs[k - 1]), F.mult, 0, F.P, *wk, sp(2 + 2 * k), None, F.st)
         F.dot(d, ad, s[1:2])
         nrm2 = F.read(s[1:2])[0]
         if nrm2 <= 1e-14 * a0:

@@ -46,10 +46,10 @@ def main():
     res["torch copy (16 B/pt)"] = (timeit(lambda: w.copy_(v1)), 16)
     res["mgs prev+next (33 B/pt)"] = (timeit(lambda: _lib.call(
         "sf_mgs_step_f64", w.data_ptr(), v1.data_ptr(), h.data_ptr(), v2.data_ptr(), None, None, m8.data_ptr(),
-        0, P, *wk.args(), out.data_ptr(), st)), 33)
+        0, P, *wk.args(), out.data_ptr(), None, st)), 33)
     res["mgs next+norm (17 B/pt)"] = (timeit(lambda: _lib.call(
         "sf_mgs_step_f64", w.data_ptr(), None, None, v2.data_ptr(), None, None, m8.data_ptr(),
-        1, P, *wk.args(), out.data_ptr(), st)), 17)
+        1, P, *wk.args(), out.data_ptr(), None, st)), 17)
     pa = (ctypes.c_void_p * 1)(w.data_ptr())
     pb = (ctypes.c_void_p * 1)(v1.data_ptr())
     res["glsc3 (17 B/pt)"] = (timeit(lambda: _lib.call(
