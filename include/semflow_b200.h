@@ -104,6 +104,15 @@ int sf_ax_masked_f64(const double* d_host, int n, const double* g, const double*
 int sf_dssum_f64(double* v, const int* offsets, const int* perm, int n_shared, int mode,
                  const double* u, const double* recv, int n_local, void* stream);
 
+/* The same dssum with the shared gids stored by multiplicity class (the layout
+ * space.GatherScatter uses): perm holds n2 index pairs, then n4 quadruples, then
+ * n8 octets (fixed stride, no offsets), then the CSR part of n_gen gids of any
+ * other multiplicity (gen_offsets, n_gen+1 entries relative to that part).  Same
+ * modes, flags, halo convention and per-gid order as sf_dssum_f64. */
+int sf_dssum_cls_f64(double* v, const int* perm, int n2, int n4, int n8, const int* gen_offsets,
+                     int n_gen, int mode, const double* u, const double* recv, int n_local,
+                     void* stream);
+
 /* out[i] = v[idx[i]] -- packs a rank's interface values for the halo exchange. */
 int sf_gather_f64(double* out, const double* v, const int* idx, long long n, void* stream);
 

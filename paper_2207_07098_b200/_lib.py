@@ -32,6 +32,7 @@ _SIGS = {
     "sf_gs_scatter_f64": [_vp, _vp, _vp, _ll, _vp, _vp],
     "sf_ax_masked_f64": [_vp, _i, _vp, _vp, _vp, _vp, _ll, _d, _d, _vp, _vp, _i, _vp],
     "sf_dssum_f64": [_vp, _vp, _vp, _i, _i, _vp, _vp, _i, _vp],
+    "sf_dssum_cls_f64": [_vp, _vp, _i, _i, _i, _vp, _i, _i, _vp, _vp, _i, _vp],
     "sf_gather_f64": [_vp, _vp, _vp, _ll, _vp],
     "sf_rank_sum_f64": [_vp, _i, _i, _vp, _vp],
     "sf_glsc3_f64": [_i, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp],

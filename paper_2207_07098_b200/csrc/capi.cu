@@ -43,6 +43,8 @@ int gs_scatter(const double*, const long long*, const long long*, long long, dou
 int dssum_shared(double*, const int*, const int*, int, int, const double*, const double*, int,
                  cudaStream_t);
 int gather(double*, const double*, const int*, long long, cudaStream_t);
+int dssum_cls(double*, const int*, int, int, int, const int*, int, int, const double*, const double*,
+              int, cudaStream_t);
 int rank_sum(const double*, int, int, double*, cudaStream_t);
 int dot_multi(int, const double* const*, const double* const*, const uint8_t*, long long, RedWork,
               double*, cudaStream_t);
@@ -129,6 +131,12 @@ int sf_ax_masked_f64(const double* d_host, int n, const double* g, const double*
 int sf_dssum_f64(double* v, const int* offsets, const int* perm, int n_shared, int mode,
                  const double* u, const double* recv, int n_local, void* stream) {
   return dssum_shared(v, offsets, perm, n_shared, mode, u, recv, n_local, as_stream(stream));
+}
+
+int sf_dssum_cls_f64(double* v, const int* perm, int n2, int n4, int n8, const int* gen_offsets,
+                     int n_gen, int mode, const double* u, const double* recv, int n_local,
+                     void* stream) {
+  return dssum_cls(v, perm, n2, n4, n8, gen_offsets, n_gen, mode, u, recv, n_local, as_stream(stream));
 }
 
 int sf_gather_f64(double* out, const double* v, const int* idx, long long n, void* stream) {

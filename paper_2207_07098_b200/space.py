@@ -155,12 +155,40 @@ class GatherScatter:
         self.comm.exchange(sends, recvs)
         return self._recvbuf
 
+    def _build_classes(self):
+        """Multiplicity-class layout of the shared maps (sf_dssum_cls_f64): pairs,
+        quads, octets at fixed stride, the rest in CSR; order within a class kept."""
+        dev = self.device
+        off = self.sh_off.long()
+        cnt = off[1:] - off[:-1]
+        parts, n = [], {}
+        for c in (2, 4, 8):
+            sel = torch.nonzero(cnt == c).view(-1)
+            n[c] = int(sel.numel())
+            idx = (off[sel].view(-1, 1) + torch.arange(c, device=dev).view(1, c)).reshape(-1)
+            parts.append(self.sh_perm[idx])
+        other = torch.nonzero((cnt != 2) & (cnt != 4) & (cnt != 8)).view(-1)
+        oc = cnt[other]
+        gen_off = torch.zeros(other.numel() + 1, dtype=torch.int64, device=dev)
+        if other.numel():
+            gen_off[1:] = torch.cumsum(oc, 0)
+        within = torch.arange(int(gen_off[-1]), device=dev) - torch.repeat_interleave(gen_off[:-1], oc)
+        parts.append(self.sh_perm[torch.repeat_interleave(off[other], oc) + within])
+        self.cls_perm = torch.cat(parts).to(torch.int32).contiguous()
+        self.cls_n = (n[2], n[4], n[8])
+        self.cls_gen_off = gen_off.to(torch.int32).contiguous()
+        self.cls_n_gen = int(other.numel())
+
     def dssum_into(self, v, mode, u=None, perm=None):
-        """In-place dssum of one scalar row v (mode 0 add / 1 avg / 2 masked with u)."""
+        """In-place dssum of one scalar row v (mode 0 add / 1 avg / 2 masked with u).
+        ``perm``: a flagged copy of ``cls_perm`` (masked operators)."""
         recv = self.halo_exchange(v)
-        _lib.call("sf_dssum_f64", _lib.ptr(v), _lib.ptr(self.sh_off),
-                  _lib.ptr(self.sh_perm if perm is None else perm), self.n_shared, mode, _lib.ptr(u),
-                  _lib.ptr(recv), self.P, _lib.stream_ptr(self.device))
+        if not hasattr(self, "cls_perm"):
+            self._build_classes()
+        n2, n4, n8 = self.cls_n
+        _lib.call("sf_dssum_cls_f64", _lib.ptr(v), _lib.ptr(self.cls_perm if perm is None else perm), n2, n4, n8,
+                  _lib.ptr(self.cls_gen_off), self.cls_n_gen, mode, _lib.ptr(u), _lib.ptr(recv), self.P,
+                  _lib.stream_ptr(self.device))
 
     def _dssum_rows(self, flat, mode, u=None):
         for row in range(flat.shape[0]):
@@ -188,13 +216,16 @@ class GatherScatter:
         return self.avg_(u.contiguous().clone())
 
     def masked_perm(self, keep_flat):
-        """Shared perm with bit 31 set on the local copies whose mask is 0."""
-        loc = self.sh_perm.long()
+        """Class-layout shared perm (cls_perm) with bit 31 set on the local copies
+        whose mask is 0 -- the map of a masked operator's dssum."""
+        if not hasattr(self, "cls_perm"):
+            self._build_classes()
+        loc = self.cls_perm.long()
         is_local = loc < self.P
         dropped = torch.zeros_like(is_local)
         dropped[is_local] = ~keep_flat[loc[is_local]]
-        return torch.where(dropped, self.sh_perm | torch.tensor(-2**31, dtype=torch.int32, device=self.device),
-                           self.sh_perm).contiguous()
+        return torch.where(dropped, self.cls_perm | torch.tensor(-2**31, dtype=torch.int32, device=self.device),
+                           self.cls_perm).contiguous()
 
     def dot_async(self, u, v, out):
         """Write <u, v>_{1/mult} (summed over ranks) into the device scalar ``out``."""

@@ -72,8 +72,13 @@ def run(ne):
                     L.sf_ax_helm_f64(sp.dmat.ctypes.data, 8, sp.geom.data_ptr(), sp.bm.data_ptr(), u.data_ptr(),
                                      w.data_ptr(), sp.n_elements, 1.0, 0.0, 0, st)
                 else:
-                    L.sf_dssum_f64(w.data_ptr(), gs.sh_off.data_ptr(), op.sh_perm.data_ptr(), gs.n_shared, 2,
-                                   u.data_ptr(), None, 0, st)
+                    if hasattr(L, "sf_dssum_cls_f64"):
+                        n2, n4, n8 = gs.cls_n
+                        L.sf_dssum_cls_f64(w.data_ptr(), op.sh_perm.data_ptr(), n2, n4, n8,
+                                           gs.cls_gen_off.data_ptr(), gs.cls_n_gen, 2, u.data_ptr(), None, 0, st)
+                    else:   # CSR layout (older builds): the plain shared maps
+                        L.sf_dssum_f64(w.data_ptr(), gs.sh_off.data_ptr(), gs.masked_perm_csr.data_ptr(),
+                                       gs.n_shared, 2, u.data_ptr(), None, 0, st)
             for _ in range(3):
                 fn()
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
