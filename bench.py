@@ -183,8 +183,14 @@ def time_kernels(sp, op, u, reps=20):
         else:
             gs.dssum_into(w, 0)
 
+    def fused():
+        op.apply_into(u, w)
+
+    jobs = [("ax", ax), ("dssum", dss)]
+    if getattr(op, "fused", False):
+        jobs.append(("fused", fused))
     res = {}
-    for name, fn in (("ax", ax), ("dssum", dss)):
+    for name, fn in jobs:
         for _ in range(3):
             fn()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
@@ -322,7 +328,8 @@ def bench_poisson(args, world, rank, dev):
     kt = time_kernels(sp, A, torch.randn(sp.shape, dtype=torch.float64, device=dev))
     pk, src = peaks()
     nbytes = ax_dssum_bytes(sp, True)
-    achieved = nbytes / (kt["ax"] + kt["dssum"]) / 1e9
+    t_op = kt.get("fused", kt["ax"] + kt["dssum"])
+    achieved = nbytes / t_op / 1e9
     line = {
         "metric": "GDOF/s per PCG iteration (config 2: Poisson Ax+dssum+Jacobi-CG, 32^3 lx=8)",
         "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -332,9 +339,11 @@ def bench_poisson(args, world, rank, dev):
                    "points": P, "iterations_per_step": its // args.steps, "l2": "inputs larger than L2",
                    "parallelism": f"replicas x{world}" if world > 1 else "single"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm_gbs"], "traffic": None, "kernel": "ax_helm(masked)+dssum",
-                     "algorithmic_bytes": nbytes, "ax_us": kt["ax"] * 1e6, "dssum_us": kt["dssum"] * 1e6,
-                     "peak_source": src},
+                     "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                     "kernel": "ax_dssum8_kernel (fused masked Ax+dssum)" if "fused" in kt
+                     else "ax_helm(masked)+dssum",
+                     "algorithmic_bytes": nbytes, "us": t_op * 1e6, "ax_us": kt["ax"] * 1e6,
+                     "dssum_us": kt["dssum"] * 1e6, "peak_source": src},
         "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
     }
     return line
@@ -430,7 +439,8 @@ def bench_tgv(args, world, rank, dev):
     kt = time_kernels(sp, op, probe)
     pk, src = peaks()
     nbytes = ax_dssum_bytes(sp, op.masked)
-    achieved = nbytes / (kt["ax"] + kt["dssum"]) / 1e9
+    t_op = kt.get("fused", kt["ax"] + kt["dssum"])
+    achieved = nbytes / t_op / 1e9
     # dominant kernel of the step: the GMRES modified-Gram-Schmidt pass
     # (w -= h v_{i-1}; <w, v_i>) -- ~70 % of the step at 64^3 (profiles/)
     t_mgs, mgs_bytes = time_mgs(sp, probe)
@@ -453,9 +463,10 @@ def bench_tgv(args, world, rank, dev):
                      "kernel": "mgs2_kernel<true,true,false,false> (GMRES MGS pass, rank 0)",
                      "algorithmic_bytes": mgs_bytes, "us": t_mgs * 1e6, "peak_source": src,
                      "ax_dssum": {"achieved": achieved, "frac": achieved / pk["hbm_gbs"],
-                                  "algorithmic_bytes": nbytes, "ax_us": kt["ax"] * 1e6,
+                                  "algorithmic_bytes": nbytes, "us": t_op * 1e6, "ax_us": kt["ax"] * 1e6,
                                   "dssum_us": kt["dssum"] * 1e6,
-                                  "kernel": "ax_helm + dssum (pressure Poisson operator)"}},
+                                  "kernel": ("ax_dssum8_kernel, fused" if "fused" in kt else "ax_helm + dssum")
+                                  + " (pressure Poisson operator)"}},
         "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
     }
 

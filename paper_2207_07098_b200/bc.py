@@ -1,8 +1,8 @@
 """Boundary conditions on device (reference semflow/bc.py).
 
-Masks and per-step boundary terms for the kinds the hot path uses:
-``noslip``, ``velocity``, ``function`` (Dirichlet), ``symmetry`` and
-``outflow`` (bc.py:159-270).  Dirichlet evaluators are called with host numpy
+Masks and per-step boundary terms for every reference kind: ``noslip``,
+``velocity``, ``inflow``, ``rotor``, ``function``, ``taylor_green``
+(Dirichlet), ``symmetry`` and ``outflow`` (bc.py:33-270).  Dirichlet evaluators are called with host numpy
 coordinates of the constrained points -- the same call the reference makes
 (bc.py:218-229), so user functions written for the reference work unchanged --
 and only those boundary values cross to the device.
@@ -18,7 +18,7 @@ import torch
 
 from .errors import ConfigError
 
-DIRICHLET_KINDS = ("noslip", "velocity", "function")
+DIRICHLET_KINDS = ("noslip", "velocity", "inflow", "rotor", "function", "taylor_green")
 
 
 def _const_fn(value):
@@ -30,6 +30,81 @@ def _const_fn(value):
         return np.broadcast_to(v.reshape((3,) + (1,) * np.ndim(x)), (3,) + np.shape(x)).copy()
 
     return fn
+
+
+def power_law_profile(y, u_cl, h, exponent=1.0 / 7.0):
+    """Streamwise inflow speed u_cl (y/h)^exponent with y clamped into [0, h]
+    (bc.py:36-45; the out-of-range warning is not reproduced)."""
+    yc = np.minimum(np.maximum(np.asarray(y, dtype=np.float64), 0.0), h)
+    return u_cl * (yc / h) ** exponent
+
+
+def spin_ramp(y, u_spin, delta):
+    """Rotor surface speed vs. height (bc.py:48-66): 0 for y <= 0, u_spin for
+    y >= delta, u_spin / (1 + exp(1/(q-1) + 1/q)) with q = y/delta between
+    (exponent argument clipped to +-700)."""
+    q = np.asarray(y, dtype=np.float64) / delta
+    out = np.where(q >= 1.0, u_spin, 0.0)
+    inner = (q > 0.0) & (q < 1.0)
+    qi = q[inner]
+    out[inner] = u_spin / (1.0 + np.exp(np.clip(1.0 / (qi - 1.0) + 1.0 / qi, -700.0, 700.0)))
+    return out
+
+
+def spinning_wall(x, y, z, u_spin, delta, center=(0.0, 0.0)):
+    """Azimuthal velocity of a cylinder about the y axis (bc.py:69-87):
+    (s dz / rho, 0, -s dx / rho), zero on the axis itself."""
+    dx = np.asarray(x, dtype=np.float64) - center[0]
+    dz = np.asarray(z, dtype=np.float64) - center[1]
+    rho = np.hypot(dx, dz)
+    s = spin_ramp(y, u_spin, delta)
+    fac = np.where(rho > 0.0, s / np.where(rho > 0.0, rho, 1.0), 0.0)
+    out = np.zeros((3,) + np.broadcast(dx, np.asarray(y), dz).shape)
+    out[0] = fac * dz
+    out[2] = -fac * dx
+    return out
+
+
+def decaying_vortex(x, y, z, t, nu):
+    """Planar Taylor-Green velocity (analytic.py:11-17)."""
+    amp = np.exp(-2.0 * nu * t)
+    out = np.zeros((3,) + np.broadcast(np.asarray(x), np.asarray(y)).shape)
+    out[0] = np.sin(x) * np.cos(y) * amp
+    out[1] = -np.cos(x) * np.sin(y) * amp
+    return out
+
+
+def make_evaluator(kind, params):
+    """Host evaluator g(x, y, z, t) -> (3, ...) for a Dirichlet kind (bc.py:142-157)."""
+    if kind == "noslip":
+        return _const_fn((0.0, 0.0, 0.0))
+    if kind == "velocity":
+        return _const_fn(params["value"])
+    if kind == "function":
+        return params["fn"]
+    if kind == "inflow":
+        u_cl, h = float(params["u_cl"]), float(params["h"])
+        ex = float(params.get("exponent", 1.0 / 7.0))
+        if h <= 0.0:
+            raise ConfigError(f"inflow height h must be positive, got {h}")
+
+        def inflow(x, y, z, t):
+            out = np.zeros((3,) + np.shape(x))
+            out[0] = power_law_profile(y, u_cl, h, ex)
+            return out
+        return inflow
+    if kind == "rotor":
+        u_spin = float(params["u_spin"]) if "u_spin" in params else \
+            float(params["u_cl"]) * float(params.get("alpha", 3.0))
+        delta = float(params["delta"])
+        if delta <= 0.0:
+            raise ConfigError(f"rotor smoothing distance delta must be positive, got {delta}")
+        center = tuple(float(c) for c in params.get("center", (0.0, 0.0)))
+        return lambda x, y, z, t: spinning_wall(x, y, z, u_spin, delta, center)
+    if kind == "taylor_green":
+        nu = float(params["nu"])
+        return lambda x, y, z, t: decaying_vortex(x, y, z, t, nu)
+    raise ConfigError(f"unknown Dirichlet kind {kind!r}")
 
 
 class _Scatter:
@@ -85,8 +160,7 @@ class BoundarySet:
             it = torch.from_numpy(idx).to(dev)
             flat = space.facet_flat[it].reshape(-1)
             if kind in DIRICHLET_KINDS:
-                fn = {"noslip": lambda: _const_fn((0.0, 0.0, 0.0)), "velocity": lambda: _const_fn(params["value"]),
-                      "function": lambda: params["fn"]}[kind]()
+                fn = make_evaluator(kind, params)
                 if coords_h is None:
                     coords_h = space.coords.reshape(3, -1)
                 xs = coords_h[:, flat].cpu().numpy()

@@ -43,6 +43,11 @@ def golden_ops():
 
 
 @pytest.fixture(scope="session")
+def golden_bcfun():
+    return load_npz("bcfun.npz")
+
+
+@pytest.fixture(scope="session")
 def golden_solvers():
     with open(os.path.join(GOLDEN, "solvers.json")) as fh:
         return json.load(fh)

@@ -307,7 +307,57 @@ def channel_case(counts, steps):
     return rows
 
 
+KINDS_SPECS = {"xlo": {"kind": "inflow", "u_cl": 1.0, "h": 2.0}, "xhi": {"kind": "outflow"},
+               "ylo": {"kind": "noslip"}, "yhi": {"kind": "taylor_green", "nu": 0.01},
+               "zlo": {"kind": "symmetry"},
+               "zhi": {"kind": "rotor", "u_spin": 0.3, "delta": 0.5, "center": (0.8, 0.0)}}
+
+
+def channel_kinds_case(counts, steps):
+    """Every analytic Dirichlet kind on one box: power-law inflow, decaying-vortex
+    wall, spinning wall with its smoothed ramp (delta inside the face)."""
+    Lx, Ly, Lz = 4 * np.pi / 8, 2.0, 4 * np.pi / 3 / 8
+    sp = build_space(gen_box_mesh((0.0, Lx, 0.0, Ly, 0.0, Lz), counts), make_basis(5))
+    st = Stepper(sp, BoundarySet(sp, KINDS_SPECS), nu=1.0 / 2800.0, dt=2e-3, scheme_order=3,
+                 pressure=SolverOptions(tol=1e-5, max_iter=200, restart=20, precond="jacobi"),
+                 velocity=SolverOptions(tol=1e-8, max_iter=100, precond="jacobi"))
+    state = st.initial_state(np.zeros((3,) + sp.shape))
+    rows = []
+    for _ in range(steps):
+        state, d = st.step(state)
+        rows.append(dict(step=d.step, p_it=d.p_iterations, p_res=d.p_residual, v_it=list(d.v_iterations),
+                         v_res=list(d.v_residual), cfl=d.cfl, div=d.div_norm,
+                         ke=kinetic_energy(sp, state.vel), ens=enstrophy(sp, state.vel)))
+        print(f"channel_kinds step {d.step}: p {d.p_iterations} v {d.v_iterations}", flush=True)
+    return rows
+
+
+def gen_bcfun():
+    """Reference boundary-value evaluators at sample points (bc.py:36-157)."""
+    from semflow import analytic
+    from semflow.bc import inflow_profile, rotor_smoothing, rotor_velocity
+
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-1.0, 1.0, 400)
+    y = np.concatenate([rng.uniform(-0.2, 2.2, 392), [0.0, 0.25, 0.5, 1.0, 2.0, -0.0, 1e-9, 0.5 - 1e-12]])
+    z = rng.uniform(-1.0, 1.0, 400)
+    x[:3] = 0.25
+    z[:3] = 0.0
+    x[3] = z[3] = 0.0          # on the rotor axis
+    with np.errstate(all="ignore"):
+        out = dict(x=x, y=y, z=z,
+                   inflow=inflow_profile(y, 1.3, 2.0, 1.0 / 7.0),
+                   inflow_sq=inflow_profile(y, 0.7, 2.0, 0.5),
+                   ramp=rotor_smoothing(y, 0.9, 0.5),
+                   rotor=rotor_velocity(x, y, z, 0.9, 0.5, (0.25, 0.0)),
+                   tg=analytic.taylor_green_velocity(x, y, z, 0.37, 0.01))
+    np.savez_compressed(os.path.join(OUT, "bcfun.npz"), **out)
+
+
 def main():
+    if "--bcfun" in sys.argv:
+        gen_bcfun()
+        return
     if "--update" in sys.argv:
         # recompute selected solver entries only: --update poisson4 poisson8 ...
         keys = sys.argv[sys.argv.index("--update") + 1:]
@@ -319,6 +369,8 @@ def main():
                 sol[k] = poisson_case(int(k[len("poisson"):]))
             elif k.startswith("tgv"):
                 sol[k] = tgv_case(int(k[3:]), 10)
+            elif k == "channel_kinds":
+                sol[k] = channel_kinds_case((6, 4, 3), 4)
         with open(path, "w") as fh:
             json.dump(sol, fh, indent=1)
         return

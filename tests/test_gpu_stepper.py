@@ -69,6 +69,29 @@ def test_channel_boundary_paths(cuda, golden_solvers):
         assert rel_err(kinetic_energy(sp, state.vel), row["ke"]) < 1e-7
 
 
+def test_channel_all_dirichlet_kinds(cuda, golden_solvers):
+    """Power-law inflow, taylor_green wall, rotor wall with its ramp, from rest."""
+    from paper_2207_07098_b200.basis import make_basis
+    from paper_2207_07098_b200.bc import BoundarySet
+    from paper_2207_07098_b200.mesh import gen_box_mesh
+    from paper_2207_07098_b200.space import build_space
+    from paper_2207_07098_b200.timestep import SolverOptions, Stepper, kinetic_energy
+
+    from test_oracle import KINDS_SPECS
+
+    Lx, Ly, Lz = 4 * np.pi / 8, 2.0, 4 * np.pi / 3 / 8
+    sp = build_space(gen_box_mesh((0.0, Lx, 0.0, Ly, 0.0, Lz), (6, 4, 3)), make_basis(5), device=cuda)
+    st = Stepper(sp, BoundarySet(sp, KINDS_SPECS), nu=1.0 / 2800.0, dt=2e-3, scheme_order=3,
+                 pressure=SolverOptions(tol=1e-5, max_iter=200, restart=20, precond="jacobi"),
+                 velocity=SolverOptions(tol=1e-8, max_iter=100, precond="jacobi"))
+    state = st.initial_state(torch.zeros((3,) + sp.shape, dtype=torch.float64, device=cuda))
+    for row in golden_solvers["channel_kinds"]:
+        state, d = st.step(state)
+        assert d.p_iterations == row["p_it"]
+        assert list(d.v_iterations) == row["v_it"], (d.v_iterations, row["v_it"])
+        assert rel_err(kinetic_energy(sp, state.vel), row["ke"]) < 1e-7
+
+
 def test_zero_state_is_fixed_point(cuda):
     """Reference tests/test_timestep.py:89-100: zero velocity stays zero, no iterations."""
     from paper_2207_07098_b200.timestep import tgv_problem

@@ -183,3 +183,46 @@ def test_oracle_channel_boundary_terms(oracle, golden_solvers, golden_spaces):
         assert d.p_iterations == row["p_it"]
         assert list(d.v_iterations) == row["v_it"]
         assert rel_err(oracle.kinetic_energy(sp, state.vel), row["ke"]) < 1e-9
+
+
+KINDS_SPECS = {"xlo": {"kind": "inflow", "u_cl": 1.0, "h": 2.0}, "xhi": {"kind": "outflow"},
+               "ylo": {"kind": "noslip"}, "yhi": {"kind": "taylor_green", "nu": 0.01},
+               "zlo": {"kind": "symmetry"},
+               "zhi": {"kind": "rotor", "u_spin": 0.3, "delta": 0.5, "center": (0.8, 0.0)}}
+
+
+def _bcfun_cases(golden_bcfun, make):
+    g = golden_bcfun
+    x, y, z = g["x"], g["y"], g["z"]
+    yield "inflow", make("inflow", {"u_cl": 1.3, "h": 2.0})(x, y, z, 0.0)[0], g["inflow"]
+    yield "inflow_sq", make("inflow", {"u_cl": 0.7, "h": 2.0, "exponent": 0.5})(x, y, z, 0.0)[0], g["inflow_sq"]
+    yield "rotor", make("rotor", {"u_spin": 0.9, "delta": 0.5, "center": (0.25, 0.0)})(x, y, z, 0.0), g["rotor"]
+    yield "tg", make("taylor_green", {"nu": 0.01})(x, y, z, 0.37), g["tg"]
+
+
+def test_oracle_dirichlet_kinds_bitwise(oracle, golden_bcfun):
+    """Inflow / rotor / taylor_green evaluators vs the reference's (bc.py:36-157)."""
+    for name, got, want in _bcfun_cases(golden_bcfun, lambda k, p: oracle.dirichlet_fn(k, p)):
+        assert np.array_equal(got, want), name
+
+
+def test_device_bc_evaluators_bitwise(golden_bcfun):
+    """The package's host evaluators (called on boundary points only) match too."""
+    from paper_2207_07098_b200 import bc
+
+    for name, got, want in _bcfun_cases(golden_bcfun, bc.make_evaluator):
+        assert np.array_equal(got, want), name
+    ramp = bc.spin_ramp(golden_bcfun["y"], 0.9, 0.5)
+    assert np.array_equal(ramp, golden_bcfun["ramp"])
+
+
+def test_oracle_channel_all_kinds(oracle, golden_solvers):
+    Lx, Ly, Lz = 4 * np.pi / 8, 2.0, 4 * np.pi / 3 / 8
+    sp = oracle.build_space(oracle.gen_box_mesh((0.0, Lx, 0.0, Ly, 0.0, Lz), (6, 4, 3)), oracle.make_basis(5))
+    st = oracle.Stepper(sp, oracle.Boundary(sp, KINDS_SPECS), 1.0 / 2800.0, 2e-3)
+    state = st.initial_state(np.zeros((3,) + sp.shape))
+    for row in golden_solvers["channel_kinds"][:2]:
+        state, d = st.step(state)
+        assert d.p_iterations == row["p_it"]
+        assert list(d.v_iterations) == row["v_it"]
+        assert rel_err(oracle.kinetic_energy(sp, state.vel), row["ke"]) < 1e-9

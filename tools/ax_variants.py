@@ -13,9 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2207_07098_b200", "variants")
 VARIANTS = {
-    "padded_minb4": "-DSF_AX_MINB=4",
-    "padded_minb5u1": "-DSF_AX_MINB=5 -DSF_AX_UNROLL=1",
-    "padded_minb6": "-DSF_AX_MINB=6",
+    "fused_batch1": "-DSF_DSS_BATCH=1",
 }
 
 
@@ -89,9 +87,35 @@ def run(ne):
                 b.record()
             torch.cuda.synchronize()
             res[kind] = float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3
+        if hasattr(L, "sf_ax_dssum8_f64"):
+            for cpl in os.environ.get("AX_CHUNKS", "592").split(","):
+                cp, lag = (int(x) for x in (cpl.split(":") + ["1"])[:2])
+                plans = {"fmasked": gs.fused_plan(op.sh_perm, chunk_pairs=cp, lag=lag),
+                         "fplain": gs.fused_plan(None, chunk_pairs=cp, lag=lag)}
+                for kind, pl in plans.items():
+                    m = kind == "fmasked"
+
+                    def fn():
+                        L.sf_ax_dssum8_f64(sp.dmat.ctypes.data, sp.geom.data_ptr(), sp.bm.data_ptr(), u.data_ptr(),
+                                           w.data_ptr(), sp.n_elements, 1.0, 0.0,
+                                           op.inmask.data_ptr() if m else None, op.outsel.data_ptr() if m else None,
+                                           2 if m else 0, *pl.launch_args(), 0, st)
+                    for _ in range(3):
+                        fn()
+                    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
+                    torch.cuda.synchronize()
+                    for a, b in ev:
+                        a.record()
+                        fn()
+                        b.record()
+                    torch.cuda.synchronize()
+                    res[f"{kind}{cpl}"] = float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3
         gbs = P * 64 / (res["masked"] * 1e-6) / 1e9
         print(f"{os.path.basename(path):24s} masked {res['masked']:8.1f} us ({gbs:6.0f} GB/s)  plain {res['plain']:8.1f} us"
               f"  dssum {res['dssum']:7.1f} us", flush=True)
+        fk = {k: round(v, 1) for k, v in res.items() if k.startswith("f")}
+        if fk:
+            print("   fused:", fk, flush=True)
 
 
 if __name__ == "__main__":
