@@ -1,6 +1,6 @@
 """Benchmark of the SEM hot path on B200 (one JSON line on rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload tgv|poisson] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload tgv|poisson|channel] [--impl ours|reference]
 
 Workloads (BASELINE.json configs):
   poisson  config 2: Jacobi-PCG on the 32^3-element lx=8 box, Dirichlet walls;
@@ -375,6 +375,30 @@ def cpu_tgv_sample(steps=None, warmup=None, budget=20.0):
                       f"(pressure its {its}), mean {t:.2f} s/step"}
 
 
+def cpu_channel_sample(budget=20.0):
+    """Oracle channel (config-4 set-up) on a 12x8x12 lx=8 box: mean step time over
+    the first steps within the budget (the full 48x32x48 case needs ~40 min per
+    step on the CPU reference)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import semflow_oracle as O
+
+    sp, st, state = O.channel_setup((12, 8, 12))
+    P = int(np.prod(sp.shape))
+    times, its = [], []
+    t_all = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        state, d = st.step(state)
+        times.append(time.perf_counter() - t0)
+        its.append(d.p_iterations)
+        if time.perf_counter() - t_all > budget:
+            break
+    t = float(np.mean(times))
+    return {"value": P / t / 1e9, "unit": "GDOF/s", "cores": O.num_threads(), "kind": "port",
+            "sample": f"oracle channel 12x8x12 lx=8 ({P} points), steps 1-{len(times)} "
+                      f"(pressure its {its}), mean {t:.2f} s/step"}
+
+
 def bench_tgv(args, world, rank, dev):
     import torch
 
@@ -387,10 +411,18 @@ def bench_tgv(args, world, rank, dev):
     # 8 fields (1.07 GB each at 64^3) per step up to 20 solves, so one B200
     # (180 GB) holds 64^3 for at most 8 warm-up + timed steps; longer runs use
     # 48^3 at every GPU count so the strong-scaling series stays one workload.
-    ne = args.ne or (64 if args.warmup + args.steps <= 8 else 48)
     comm = sfdist.init_from_env()
-    sp, st, state = tgv_problem(ne, device=dev, comm=comm)
-    P = ne ** 3 * sp.n ** 3            # global points: strong scaling, fixed total work
+    if args.workload == "channel":
+        from paper_2207_07098_b200.timestep import channel_problem
+
+        counts = (48, 32, 48) if not args.ne else (args.ne, max(1, 2 * args.ne // 3), args.ne)
+        ne = counts
+        sp, st, state = channel_problem(counts, device=dev, comm=comm)
+        P = counts[0] * counts[1] * counts[2] * sp.n ** 3
+    else:
+        ne = args.ne or (64 if args.warmup + args.steps <= 8 else 48)
+        sp, st, state = tgv_problem(ne, device=dev, comm=comm)
+        P = ne ** 3 * sp.n ** 3            # global points: strong scaling, fixed total work
     for _ in range(args.warmup):
         state, d = st.step(state)
     stream = torch.cuda.current_stream()
@@ -445,13 +477,21 @@ def bench_tgv(args, world, rank, dev):
     # (w -= h v_{i-1}; <w, v_i>) -- ~70 % of the step at 64^3 (profiles/)
     t_mgs, mgs_bytes = time_mgs(sp, probe)
     mgs_gbs = mgs_bytes / t_mgs / 1e9
+    if args.workload == "channel":
+        wl_name = (f"channel {ne[0]}x{ne[1]}x{ne[2]} elements lx=8 (config 4{'' if ne == (48, 32, 48) else ' analogue'}),"
+                   " Poiseuille inflow/outflow/no-slip/symmetry, nu=1/2800 dt=2e-3, Jacobi-GMRES(20) p 1e-5,"
+                   " Jacobi-PCG v 1e-8, projection on")
+        metric = "GDOF/s per time step (channel, lx=8)"
+    else:
+        wl_name = (f"TGV Re=1600 {ne}^3 elements lx=8 (config {'3' if ne == 64 else '1' if ne == 8 else '1/3 analogue'}),"
+                   " symmetry box, Jacobi-GMRES(20) p 1e-5, Jacobi-PCG v 1e-8, projection on")
+        metric = "GDOF/s per time step (TGV, lx=8)"
     return {
-        "metric": "GDOF/s per time step (TGV, lx=8)",
+        "metric": metric,
         "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"TGV Re=1600 {ne}^3 elements lx=8 (config {'3' if ne == 64 else '1' if ne == 8 else '1/3 analogue'}),"
-                               " symmetry box, Jacobi-GMRES(20) p 1e-5, Jacobi-PCG v 1e-8, projection on",
+        "config": {"workload": wl_name,
                    "points": P, "steps_timed": f"{args.warmup + 1}-{args.warmup + args.steps}",
                    "p_iterations": p_its, "v_iterations": v_its, "ke_end": ke,
                    "peak_mem_gb_rank0": torch.cuda.max_memory_allocated() / 1e9,
@@ -459,7 +499,7 @@ def bench_tgv(args, world, rank, dev):
                    "parallelism": (f"element partition x{world} (z-slabs), NCCL halo exchange + allgather dots"
                                    if world > 1 else "single")},
         "roofline": {"bound": "hbm", "achieved": mgs_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": mgs_gbs / pk["hbm_gbs"], "traffic": MGS_TRAFFIC.get(ne),
+                     "frac": mgs_gbs / pk["hbm_gbs"], "traffic": MGS_TRAFFIC.get(str(ne)),
                      "kernel": "mgs2_kernel<true,true,false,false> (GMRES MGS pass, rank 0)",
                      "algorithmic_bytes": mgs_bytes, "us": t_mgs * 1e6, "peak_source": src,
                      "ax_dssum": {"achieved": achieved, "frac": achieved / pk["hbm_gbs"],
@@ -477,7 +517,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--workload", default="tgv", choices=("tgv", "poisson"))
+    ap.add_argument("--workload", default="tgv", choices=("tgv", "poisson", "channel"))
     ap.add_argument("--ne", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -489,6 +529,9 @@ def main():
         if args.workload == "tgv":
             base = cpu_tgv_sample(steps=args.steps, warmup=args.warmup)
             metric = "GDOF/s per time step (TGV, lx=8)"
+        elif args.workload == "channel":
+            base = cpu_channel_sample()
+            metric = "GDOF/s per time step (channel, lx=8)"
         else:
             base = cpu_poisson_sample()
             metric = "GDOF/s per PCG iteration (config 2: Poisson Ax+dssum+Jacobi-CG, 32^3 lx=8)"
@@ -504,13 +547,14 @@ def main():
 
     world, rank, local = dist_setup()
     dev = torch.device("cuda", torch.cuda.current_device())
-    line = (bench_tgv if args.workload == "tgv" else bench_poisson)(args, world, rank, dev)
+    line = (bench_poisson if args.workload == "poisson" else bench_tgv)(args, world, rank, dev)
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:
             # the same step numbers as the GPU's timed steps, on the 8^3 mesh the
             # CPU port finishes in seconds (config 1)
-            line["cpu_baseline"] = (cpu_tgv_sample(steps=args.steps, warmup=args.warmup)
-                                    if args.workload == "tgv" else cpu_poisson_sample())
+            line["cpu_baseline"] = {"tgv": lambda: cpu_tgv_sample(steps=args.steps, warmup=args.warmup),
+                                    "channel": lambda: cpu_channel_sample(),
+                                    "poisson": cpu_poisson_sample}[args.workload]()
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

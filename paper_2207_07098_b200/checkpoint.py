@@ -1,0 +1,157 @@
+"""Binary checkpoints and bitwise restart (reference output.py:69-128, runner.py:102-165).
+
+The container is the reference's own format, so checkpoints written by either
+implementation restart the other: 8-byte magic ``SEMFCKPT``, uint32 version 1,
+uint64 header length, a JSON header ``{"arrays": [{"name", "shape"}...],
+"meta": {...}}`` (sort_keys), then the float64 little-endian payloads in
+header order.  Device fields are copied to the host only here.
+
+``save_state`` / ``load_state`` carry exactly what the reference's runner
+carries -- velocity and explicit-term histories, pressure, the projection
+spaces (basis vectors, count, solve counter) and the last scheme order -- so a
+restarted run reproduces the uninterrupted one bit for bit
+(pkg/tests/test_runner.py:101-115).  On several ranks the element slices are
+gathered, so the file is the same for any rank count.
+"""
+
+import json
+
+import numpy as np
+import torch
+
+from . import dist as _dist
+from . import operators
+from .errors import CheckpointError
+from .timestep import FlowState
+
+MAGIC = b"SEMFCKPT"
+VERSION = 1
+
+
+def write_checkpoint(path, arrays, meta):
+    """Named float64 arrays + JSON metadata -> checkpoint file (output.py:69-84)."""
+    specs, payload = [], []
+    for name, arr in arrays.items():
+        a = arr.detach().cpu().numpy() if isinstance(arr, torch.Tensor) else np.asarray(arr)
+        if a.dtype != np.float64:
+            raise CheckpointError(f"checkpoint arrays must be float64, {name} is {a.dtype}")
+        specs.append({"name": name, "shape": list(a.shape)})
+        payload.append(np.ascontiguousarray(a, dtype="<f8"))
+    header = json.dumps({"arrays": specs, "meta": meta}, sort_keys=True).encode("utf-8")
+    with open(path, "wb") as fh:
+        fh.write(MAGIC)
+        fh.write(np.array(VERSION, dtype="<u4").tobytes())
+        fh.write(np.array(len(header), dtype="<u8").tobytes())
+        fh.write(header)
+        for a in payload:
+            fh.write(a.tobytes())
+
+
+def read_checkpoint(path):
+    """Checkpoint file -> (arrays dict of numpy float64, meta dict) (output.py:87-128).
+    Errors name the section and byte offset where the file went wrong."""
+    with open(path, "rb") as fh:
+        blob = memoryview(fh.read())
+    cur = [0]
+
+    def chunk(nbytes, section):
+        at = cur[0]
+        if at + nbytes > len(blob):
+            raise CheckpointError(f"truncated checkpoint: wanted {nbytes} bytes, have {len(blob) - at}",
+                                  offset=at, section=section)
+        cur[0] = at + nbytes
+        return blob[at:at + nbytes]
+
+    magic = bytes(chunk(8, "magic"))
+    if magic != MAGIC:
+        raise CheckpointError(f"bad magic {magic!r}, expected {MAGIC!r}", offset=0, section="magic")
+    version = int(np.frombuffer(chunk(4, "version"), dtype="<u4")[0])
+    if version != VERSION:
+        raise CheckpointError(f"unsupported checkpoint version {version}, this build reads {VERSION}",
+                              offset=8, section="version")
+    hlen = int(np.frombuffer(chunk(8, "header_len"), dtype="<u8")[0])
+    try:
+        header = json.loads(bytes(chunk(hlen, "header")).decode("utf-8"))
+    except (UnicodeDecodeError, json.JSONDecodeError) as exc:
+        raise CheckpointError(f"corrupt JSON header: {exc}", offset=20, section="header") from exc
+    arrays = {}
+    for spec in header["arrays"]:
+        shape = tuple(int(s) for s in spec["shape"])
+        count = int(np.prod(shape)) if shape else 1
+        arrays[spec["name"]] = np.frombuffer(chunk(8 * count, spec["name"]), dtype="<f8").reshape(shape).copy()
+    if cur[0] != len(blob):
+        raise CheckpointError(f"{len(blob) - cur[0]} trailing bytes after the last array",
+                              offset=cur[0], section="trailer")
+    return arrays, header["meta"]
+
+
+def _starts(space):
+    return _dist.element_ranges(space.mesh.n_elements, space.comm.world)
+
+
+def _global(space, t):
+    return space.comm.gather_elements(t, _starts(space))
+
+
+def _local(space, a):
+    e0, e1 = space.e_range
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    return t[..., e0:e1, :, :, :].contiguous().to(space.device)
+
+
+def save_state(path, stepper, state, case="semflow_b200"):
+    """Write the runner's checkpoint for (stepper, state) (runner.py:102-126).
+    Collective on several ranks; rank 0 writes the file."""
+    sp = stepper.space
+    arrays = {}
+    for q, v in enumerate(state.vel_hist):
+        arrays[f"vel_{q}"] = _global(sp, v)
+    for q, nl in enumerate(state.nl_hist):
+        arrays[f"nl_{q}"] = _global(sp, nl)
+    arrays["prs"] = _global(sp, state.prs)
+    proj_meta = {}
+    for name, proj in stepper._proj.items():
+        if proj.xs:
+            arrays[f"proj_{name}_xs"] = torch.stack([_global(sp, x).reshape(-1) for x in proj.xs])
+            arrays[f"proj_{name}_axs"] = torch.stack([_global(sp, a).reshape(-1) for a in proj.axs])
+        proj_meta[name] = {"count": proj.count, "solves": proj._solves}
+    meta = {"case": case, "time": state.time, "nsteps": state.nsteps, "primed": state.primed,
+            "n_vel_hist": len(state.vel_hist), "n_nl_hist": len(state.nl_hist),
+            "last_order": stepper._last_order, "projections": proj_meta, "forcing": None}
+    if sp.comm.rank == 0:
+        write_checkpoint(path, arrays, meta)
+
+
+def load_state(path, stepper):
+    """Rebuild a FlowState and the stepper's side state from a checkpoint
+    (runner.py:129-165); the device histories are this rank's element slice."""
+    sp = stepper.space
+    arrays, meta = read_checkpoint(path)
+    E = sp.mesh.n_elements
+    gshape = (3, E) + sp.shape[1:]
+    try:
+        vel_hist = [_local(sp, arrays[f"vel_{q}"].reshape(gshape)) for q in range(meta["n_vel_hist"])]
+        nl_hist = [_local(sp, arrays[f"nl_{q}"].reshape(gshape)) for q in range(meta["n_nl_hist"])]
+        prs = _local(sp, arrays["prs"].reshape(gshape[1:]))
+    except (KeyError, ValueError) as exc:
+        raise CheckpointError(f"checkpoint does not match this space: {exc}", section="arrays") from exc
+    if meta.get("forcing") is not None:
+        raise CheckpointError("checkpoint carries tripping-forcing state; stochastic forcing is not on "
+                              "the device path", section="meta")
+    state = FlowState(time=float(meta["time"]), nsteps=int(meta["nsteps"]), vel_hist=vel_hist,
+                      curl_hist=[operators.curl(sp, v) for v in vel_hist], nl_hist=nl_hist, prs=prs,
+                      primed=bool(meta["primed"]))
+    for name, pm in meta.get("projections", {}).items():
+        proj = stepper._proj.get(name)
+        if proj is None:
+            continue
+        proj.invalidate()
+        proj._solves = int(pm["solves"])
+        if pm["count"]:
+            xs = arrays[f"proj_{name}_xs"]
+            axs = arrays[f"proj_{name}_axs"]
+            proj.xs = [_local(sp, xs[i].reshape(gshape[1:])) for i in range(xs.shape[0])]
+            proj.axs = [_local(sp, axs[i].reshape(gshape[1:])) for i in range(axs.shape[0])]
+    # the last scheme order keeps projection invalidation on the uninterrupted schedule
+    stepper._last_order = meta.get("last_order")
+    return state

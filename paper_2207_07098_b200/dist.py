@@ -91,6 +91,20 @@ class Comm:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return bool(t.item() > 0.0)
 
+    def gather_elements(self, t, starts):
+        """Concatenate every rank's element slice (leading axes kept, element axis
+        = -4) into the global array on all ranks (checkpoints; not on the hot path)."""
+        if self.world == 1:
+            return t
+        counts = [starts[r + 1] - starts[r] for r in range(self.world)]
+        emax = max(counts)
+        lead = t.shape[:-4]
+        pad = torch.zeros(lead + (emax,) + t.shape[-3:], dtype=t.dtype, device=t.device)
+        pad[..., :t.shape[-4], :, :, :] = t
+        parts = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(parts, pad.contiguous(), group=self.group)
+        return torch.cat([p[..., :c, :, :, :] for p, c in zip(parts, counts)], dim=-4)
+
     def exchange(self, sends, recvs):
         """Post all sends/receives (dict peer -> tensor) and wait (stream-ordered on CUDA)."""
         if self.world == 1 or (not sends and not recvs):

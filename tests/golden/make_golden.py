@@ -354,9 +354,49 @@ def gen_bcfun():
     np.savez_compressed(os.path.join(OUT, "bcfun.npz"), **out)
 
 
+def gen_ckpt():
+    """A checkpoint written by the reference's own writer (output.py:69-84)."""
+    from semflow.output import write_checkpoint
+
+    rng = np.random.default_rng(21)
+    arrays = {"vel_0": rng.standard_normal((3, 2, 3, 3, 3)), "prs": rng.standard_normal((2, 3, 3, 3)) * 1e-300,
+              "scalar": np.array(np.pi), "proj_p_xs": rng.standard_normal((2, 54))}
+    meta = {"case": "golden", "time": 0.125, "nsteps": 10, "primed": False, "n_vel_hist": 1,
+            "n_nl_hist": 0, "last_order": 3, "projections": {"p": {"count": 2, "solves": 7}}, "forcing": None}
+    write_checkpoint(os.path.join(OUT, "ref_state.ckpt"), arrays, meta)
+
+    # a TGV 3^3 state after 3 steps, checkpointed by the reference's runner, and
+    # the diagnostics of 3 more steps of the uninterrupted run
+    from types import SimpleNamespace
+
+    from semflow.runner import _save_checkpoint
+
+    L = 2 * np.pi
+    sp = build_space(gen_box_mesh((0.0, L, 0.0, L, 0.0, L), (3, 3, 3)), make_basis(7))
+    st = Stepper(sp, BoundarySet(sp, all_tags({"kind": "symmetry"})), nu=1.0 / 1600.0, dt=1e-2, scheme_order=3,
+                 pressure=SolverOptions(tol=1e-5, max_iter=200, restart=20, precond="jacobi"),
+                 velocity=SolverOptions(tol=1e-8, max_iter=100, precond="jacobi"))
+    x, y, z = sp.coords
+    state = st.initial_state(np.stack([np.sin(x) * np.cos(y) * np.cos(z), -np.cos(x) * np.sin(y) * np.cos(z),
+                                       np.zeros_like(x)]))
+    for _ in range(3):
+        state, _d = st.step(state)
+    _save_checkpoint(os.path.join(OUT, "tgv3_step3.ckpt"), SimpleNamespace(name="tgv3"), state, st)
+    rows = []
+    for _ in range(3):
+        state, d = st.step(state)
+        rows.append(dict(step=d.step, p_it=d.p_iterations, v_it=list(d.v_iterations),
+                         ke=kinetic_energy(sp, state.vel), ens=enstrophy(sp, state.vel)))
+    with open(os.path.join(OUT, "tgv3_restart.json"), "w") as fh:
+        json.dump(rows, fh, indent=1)
+
+
 def main():
     if "--bcfun" in sys.argv:
         gen_bcfun()
+        return
+    if "--ckpt" in sys.argv:
+        gen_ckpt()
         return
     if "--update" in sys.argv:
         # recompute selected solver entries only: --update poisson4 poisson8 ...

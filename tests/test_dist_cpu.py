@@ -98,7 +98,11 @@ def _worker(rank, world, port, payload, q):
         # deterministic rank-order reduction
         part = torch.tensor([float(rank + 1), 0.5 * rank], dtype=torch.float64)
         comm.sum_(part)
-        q.put((rank, out, part.numpy()))
+        # checkpoint gather of element slices (uneven ranges)
+        n = round(nnn ** (1.0 / 3.0))
+        full = torch.from_numpy(np.stack([u, 2.0 * u, -u]).reshape(3, E, n, n, n))
+        got = comm.gather_elements(full[:, starts[rank]:starts[rank + 1]].contiguous(), starts)
+        q.put((rank, out, part.numpy(), bool(torch.equal(got, full))))
     finally:
         dist.destroy_process_group()
 
@@ -119,7 +123,8 @@ def test_gloo_halo_exchange_world2(oracle, world):
         p.start()
     res = dict()
     for _ in range(world):
-        r, out, part = q.get(timeout=120)
+        r, out, part, gathered = q.get(timeout=120)
+        assert gathered
         res[r] = (out, part)
     for p in procs:
         p.join(timeout=60)
