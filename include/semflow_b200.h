@@ -248,6 +248,26 @@ int sf_glsc3_peer_f64(const double* a, const double* b, const uint8_t* mult, lon
                       double* partials, unsigned* counter, double* out, double* const* boxes,
                       int world, int rank, unsigned long long seq, unsigned* error, void* stream);
 
+/* NVLink halo exchange of the multi-GPU dssum (replaces the NCCL send/recv of
+ * the interface copies; SURVEY 8e collective C1).  Each rank owns an IPC-exported
+ * inbox of sf_halo_inbox_doubles(n_recv) doubles: 32 header doubles (uint64 flag
+ * per sender rank), then two banks of n_recv values (bank = seq & 1) laid out as
+ * the dssum's receive buffer.
+ *   sf_halo_put_f64: v[send_idx[i]] for peer q's segment [seg[q], seg[q+1]) is
+ *     stored at peer_dst[q][bank * peer_stride[q] + i - seg[q]] (NVLink stores);
+ *     after a system-scope fence the last block writes seq to peer_flag[q]
+ *     (release).  counter: a zeroed device uint32, re-armed by the kernel.
+ *   sf_halo_wait: one warp waits (acquire) until own_flags[peer_rank[q]] >= seq
+ *     for every peer; sets *error after 5 s instead of hanging.
+ * Both are stream-ordered; the dssum that follows reads the inbox bank. */
+int sf_halo_inbox_doubles(long long n_recv);
+int sf_halo_put_f64(const double* v, const int* send_idx, int n_peers, const int* peer_rank,
+                    const long long* seg, double* const* peer_dst, const long long* peer_stride,
+                    unsigned long long* const* peer_flag, unsigned long long seq, unsigned* counter,
+                    void* stream);
+int sf_halo_wait(const unsigned long long* own_flags, int n_peers, const int* peer_rank,
+                 unsigned long long seq, unsigned* error, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Function-space setup (space.py:182-245), bit-identical to build_space
  * ------------------------------------------------------------------------- */

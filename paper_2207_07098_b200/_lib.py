@@ -61,6 +61,9 @@ _SIGS = {
     "sf_mgs_step_peer_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _ll, _vp, _vp, _vp,
                              _vp, _i, _i, ctypes.c_ulonglong, _vp, _vp, _vp],
     "sf_glsc3_peer_f64": [_vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp, _i, _i, ctypes.c_ulonglong, _vp, _vp],
+    "sf_halo_inbox_doubles": [_ll],
+    "sf_halo_put_f64": [_vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, ctypes.c_ulonglong, _vp, _vp],
+    "sf_halo_wait": [_vp, _i, _vp, ctypes.c_ulonglong, _vp, _vp],
     "sf_trilinear_coords_f64": [_vp, _vp, _i, _ll, _vp, _vp],
     "sf_metrics_f64": [_vp, _vp, _i, _vp, _ll, _vp, _vp, _vp, _vp, _vp],
 }

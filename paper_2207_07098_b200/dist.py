@@ -53,6 +53,11 @@ class Comm:
     def active(self):
         return self.world > 1
 
+    def check(self):
+        """Raise if a peer-memory collective (allreduce or halo) timed out."""
+        if self.peer is not None:
+            self.peer.check()
+
     def sum_(self, t):
         """In place: t <- sum over ranks of t (rank order; t is a small device vector)."""
         if self.world == 1:
@@ -176,6 +181,96 @@ class _PeerReducer:
     def check(self):
         if int(self.error.item()):
             raise RuntimeError("peer allreduce timed out (a rank did not arrive within 5 s)")
+
+    def close(self):
+        for p in self.opened:
+            _lib.call("sf_ipc_close_handle", p)
+        self.opened = []
+        if self.own:
+            torch.cuda.synchronize()
+            _lib.call("sf_dev_free", self.own)
+            self.own = None
+
+
+class _RawPtr:
+    """Duck-typed device pointer (``data_ptr()``) for buffers not owned by torch."""
+
+    def __init__(self, p):
+        self.p = p
+
+    def data_ptr(self):
+        return self.p
+
+
+class HaloIPC:
+    """IPC inboxes for the NVLink halo exchange of one HaloPlan (csrc/halo.cu).
+
+    Collective at construction (every rank of ``comm`` builds its own for the same
+    space).  ``exchange(v)`` enqueues the put and the wait kernels on the current
+    stream and returns this rank's receive buffer for the call (an inbox bank)."""
+
+    HEADER = 32
+
+    def __init__(self, comm, plan):
+        import ctypes
+
+        lib = _lib.load()
+        self.comm = comm
+        self.plan = plan
+        me = comm.rank
+        self.n_recv = max(int(plan.n_recv_total), 1)
+        nbytes = 8 * lib.sf_halo_inbox_doubles(self.n_recv)
+        own = ctypes.c_void_p()
+        _lib.call("sf_dev_alloc_zero", nbytes, ctypes.byref(own))
+        self.own = own.value
+        hb = lib.sf_ipc_handle_bytes()
+        h = ctypes.create_string_buffer(hb)
+        _lib.call("sf_ipc_get_handle", self.own, h)
+        info = (h.raw, {int(q): int(o) for q, o in plan.recv_off.items()}, self.n_recv, list(plan.peers))
+        allinfo = [None] * comm.world
+        comm.dist.all_gather_object(allinfo, info, group=comm.group)
+        peers = list(plan.peers)
+        for q in peers:
+            if me not in allinfo[q][3]:
+                raise RuntimeError(f"halo plan is not symmetric: rank {me} -> {q}")
+        self.opened = []
+        dst, stride, flag = [], [], []
+        for q in peers:
+            p = ctypes.c_void_p()
+            _lib.call("sf_ipc_open_handle", ctypes.create_string_buffer(allinfo[q][0], hb), ctypes.byref(p))
+            self.opened.append(p.value)
+            dst.append(p.value + 8 * (self.HEADER + allinfo[q][1][me]))
+            stride.append(allinfo[q][2])
+            flag.append(p.value + 8 * me)
+        n = len(peers)
+        self.n_peers = n
+        self.peer_rank = (ctypes.c_int * max(n, 1))(*peers)
+        seg = [plan.send_off[q] for q in peers] + [int(plan.send_all.numel())]
+        self.seg = (ctypes.c_longlong * (n + 1))(*seg)
+        self.dst = (ctypes.c_void_p * max(n, 1))(*dst)
+        self.stride = (ctypes.c_longlong * max(n, 1))(*stride)
+        self.flag = (ctypes.c_void_p * max(n, 1))(*flag)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.counter = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.error = comm.peer.error if comm.peer is not None else torch.zeros(1, dtype=torch.int32, device=dev)
+        self.seq = 0
+        torch.cuda.synchronize()
+        comm.dist.barrier(group=comm.group)
+
+    def exchange(self, v):
+        if self.n_peers == 0:
+            return None
+        self.seq += 1
+        st = _lib.stream_ptr(v.device)
+        _lib.call("sf_halo_put_f64", _lib.ptr(v), _lib.ptr(self.plan.send_all), self.n_peers, self.peer_rank,
+                  self.seg, self.dst, self.stride, self.flag, self.seq, _lib.ptr(self.counter), st)
+        _lib.call("sf_halo_wait", self.own, self.n_peers, self.peer_rank, self.seq, _lib.ptr(self.error), st)
+        self.comm.collectives += 1
+        return _RawPtr(self.own + 8 * (self.HEADER + (self.seq & 1) * self.n_recv))
+
+    def check(self):
+        if int(self.error.item()):
+            raise RuntimeError("halo exchange timed out (a peer did not publish within 5 s)")
 
     def close(self):
         for p in self.opened:

@@ -112,6 +112,12 @@ class GatherScatter:
             self.shared_bits = pack_bits((self.mult8 > 1).view(E, nnn))
             self._sendbuf = torch.empty(int(plan.send_all.numel()), dtype=torch.float64, device=self.device)
             self._recvbuf = torch.empty(max(plan.n_recv_total, 1), dtype=torch.float64, device=self.device)
+            # NVLink halo (csrc/halo.cu) when the peer-memory path is up; NCCL otherwise
+            import os
+
+            self._ipc = None
+            if self.comm.peer is not None and os.environ.get("SEMFLOW_B200_HALO", "ipc") != "nccl":
+                self._ipc = _dist.HaloIPC(self.comm, plan)
             self._masked_perm = {}
             self._mult = None
             return
@@ -163,6 +169,8 @@ class GatherScatter:
         plan = self.plan
         if plan is None or not plan.peers:
             return None
+        if self._ipc is not None:
+            return self._ipc.exchange(v)
         st = _lib.stream_ptr(self.device)
         _lib.call("sf_gather_f64", _lib.ptr(self._sendbuf), _lib.ptr(v), _lib.ptr(plan.send_all),
                   int(plan.send_all.numel()), st)

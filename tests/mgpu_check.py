@@ -54,6 +54,11 @@ def main():
     d_f = full.gs.dot(u_full, ops.make_global_op(full, 1.0, 0.0)(u_full))
     d_p = part.gs.dot(u, ops.make_global_op(part, 1.0, 0.0)(u))
     ok["glsc3"] = abs(d_p - d_f) <= 1e-13 * abs(d_f)
+    # many back-to-back exchanges without host syncs (double-banked halo inboxes)
+    outs = [part.gs.add(u * float(k + 1)) for k in range(64)]
+    ok["dssum_repeat"] = all(bool(torch.equal(o, full.gs.add(u_full * float(k + 1))[e0:e1]))
+                             for k, o in enumerate(outs))
+    ok["halo_path"] = "ipc" if getattr(part.gs, "_ipc", None) is not None else "nccl"
     del full
     torch.cuda.empty_cache()
     res = {"world": W, "ne": ne, "checks": ok}
