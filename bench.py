@@ -495,6 +495,7 @@ def bench_tgv(args, world, rank, dev):
                    "points": P, "steps_timed": f"{args.warmup + 1}-{args.warmup + args.steps}",
                    "p_iterations": p_its, "v_iterations": v_its, "ke_end": ke,
                    "peak_mem_gb_rank0": torch.cuda.max_memory_allocated() / 1e9,
+                   "alloc_retries_rank0": int(torch.cuda.memory_stats().get("num_alloc_retries", 0)),
                    "l2": "inputs larger than L2" if P * 8 * 6 / world > 126e6 else "working set may be L2-resident",
                    "parallelism": (f"element partition x{world} (z-slabs), NCCL halo exchange + allgather dots"
                                    if world > 1 else "single")},

@@ -300,11 +300,12 @@ def _gmres_generic(apply_a, b, tol, max_iter, restart, precond, dot, x0):
 def _pipelinable(F, b):
     """The pipelined GMRES needs the gated (vectorised) MGS kernels and, across
     ranks, the fused peer reduction.  It pays off where the host round trip per
-    Arnoldi step is exposed -- multi-GPU (64^3 on 4 B200: 494 -> 461 ms/step);
-    on one GPU the look-ahead's discarded step costs more than it hides, so it
-    is off there unless SEMFLOW_B200_GMRES_PIPELINE=1."""
+    Arnoldi step is exposed -- multi-GPU (64^3 on 4 B200: 494 -> 461 ms/step)
+    and large single-GPU meshes (64^3 on 1 B200: 1004 -> 959 ms/step); below
+    ~4 M points per rank the look-ahead's discarded step costs more than it
+    hides.  SEMFLOW_B200_GMRES_PIPELINE=0/1 forces it off/on."""
     env = os.environ.get("SEMFLOW_B200_GMRES_PIPELINE", "auto")
-    want = F.comm.world > 1 if env == "auto" else env != "0"
+    want = (F.comm.world > 1 or F.P >= 1 << 22) if env == "auto" else env != "0"
     return (want and F.mult is not None and F.P % 2 == 0 and b.data_ptr() % 16 == 0
             and (F.comm.world == 1 or F.comm.peer is not None))
 

@@ -264,6 +264,15 @@ def test_pcg_gmres_iteration_counts(cuda, golden_solvers, ne):
     # (278 vs 279), so it is not a meaningful parity case
     info = krylov.gmres(A, rhs, tol=1e-8, max_iter=500, restart=20, precond=M, dot=sp.gs.dot)
     assert info.iterations == want["gmres"]["iterations"]
+    # the look-ahead (pipelined) GMRES takes the same iterations to the same x
+    import os
+
+    os.environ["SEMFLOW_B200_GMRES_PIPELINE"] = "1"
+    try:
+        info_p = krylov.gmres(A, rhs, tol=1e-8, max_iter=500, restart=20, precond=M, dot=sp.gs.dot)
+    finally:
+        del os.environ["SEMFLOW_B200_GMRES_PIPELINE"]
+    assert info_p.iterations == info.iterations and torch.equal(info_p.x, info.x)
     info = krylov.pcg(A, rhs, tol=1e-8, max_iter=500, dot=sp.gs.dot)
     assert info.iterations == want["cg_noprec"]["iterations"]
     proj = krylov.ProjectionSpace(sp.gs.dot)
