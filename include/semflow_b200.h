@@ -113,6 +113,17 @@ int sf_dssum_cls_f64(double* v, const int* perm, int n2, int n4, int n8, const i
                      int n_gen, int mode, const double* u, const double* recv, int n_local,
                      void* stream);
 
+/* The class-layout dssum scheduled by element range (the production kernel):
+ * thread block b owns the gids whose lowest local copy lies in its element range,
+ * all classes, so the 32-byte sectors shared by face, edge and vertex copies of
+ * those elements are fetched from HBM once.  block_start: 4 x (n_blocks + 1)
+ * item offsets, one row per class (pairs, quads, octets, generic), each relative
+ * to its class.  Same modes, flags, halo convention and per-gid order as
+ * sf_dssum_f64 (bit-identical results). */
+int sf_dssum_blk_f64(double* v, const int* perm, int n2, int n4, int n8, const int* gen_offsets,
+                     const int* block_start, int n_blocks, int mode, const double* u, const double* recv,
+                     int n_local, void* stream);
+
 /* Fused global operator for n = 8, single rank: sf_ax_helm_f64 / sf_ax_masked_f64
  * followed by sf_dssum_cls_f64 in ONE launch (the whole make_global_op closure,
  * operators.py:51-54, mode 0 = unmasked add, 2 = masked).  `plan` is the int32

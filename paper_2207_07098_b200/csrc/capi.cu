@@ -46,6 +46,8 @@ int gather(double*, const double*, const int*, long long, cudaStream_t);
 int dssum_cls(double*, const int*, int, int, int, const int*, int, int, const double*, const double*,
               int, cudaStream_t);
 int rank_sum(const double*, int, int, double*, cudaStream_t);
+int dssum_blk(double*, const int*, int, int, int, const int*, const int*, int, int, const double*,
+              const double*, int, cudaStream_t);
 int ax_dssum8(const double*, const double*, const double*, const double*, double*, long long, double,
               double, const uint32_t*, const uint32_t*, int, const int*, const long long*,
               unsigned long long*, unsigned long long, int, cudaStream_t);
@@ -140,6 +142,13 @@ int sf_dssum_cls_f64(double* v, const int* perm, int n2, int n4, int n8, const i
                      int n_gen, int mode, const double* u, const double* recv, int n_local,
                      void* stream) {
   return dssum_cls(v, perm, n2, n4, n8, gen_offsets, n_gen, mode, u, recv, n_local, as_stream(stream));
+}
+
+int sf_dssum_blk_f64(double* v, const int* perm, int n2, int n4, int n8, const int* gen_offsets,
+                     const int* block_start, int n_blocks, int mode, const double* u, const double* recv,
+                     int n_local, void* stream) {
+  return dssum_blk(v, perm, n2, n4, n8, gen_offsets, block_start, n_blocks, mode, u, recv, n_local,
+                   as_stream(stream));
 }
 
 int sf_ax_dssum8_f64(const double* d_host, const double* g, const double* b, const double* u,

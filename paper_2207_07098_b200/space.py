@@ -31,6 +31,12 @@ from .errors import ConfigError, GeometryError, TopologyError
 
 _FACE_NORMAL_SIGN = (-1.0, 1.0, 1.0, -1.0, -1.0, 1.0)
 
+#: dssum kernel: "blk" (element-range blocks, default) or "cls" (class by class)
+import os as _os
+
+_DSSUM_KERNEL = _os.environ.get("SEMFLOW_B200_DSSUM", "blk")
+_DSSUM_ITEMS = int(_os.environ.get("SEMFLOW_B200_DSSUM_ITEMS", 1024))   # shared gids per block
+
 
 # --------------------------------------------------------------------------- bits
 
@@ -203,6 +209,31 @@ class GatherScatter:
         self.cls_n = (n[2], n[4], n[8])
         self.cls_gen_off = gen_off.to(torch.int32).contiguous()
         self.cls_n_gen = int(other.numel())
+        # element-range blocks for sf_dssum_blk_f64: every class's items are ordered
+        # by lowest local copy, so a block's items are one contiguous run per class
+        E = self.shape[0]
+        nnn = self.P // E if E else 1
+        big = torch.iinfo(torch.int64).max
+        keys = []
+        for c, part in zip((2, 4, 8), parts[:3]):
+            p = part.view(-1, c).long()
+            keys.append(torch.where(p < self.P, p, torch.full_like(p, big)).min(dim=1).values // nnn
+                        if p.numel() else p.new_zeros(0))
+        gp = parts[3].long()
+        if other.numel():
+            item = torch.repeat_interleave(torch.arange(other.numel(), device=dev), oc)
+            kl = torch.where(gp < self.P, gp, torch.full_like(gp, big))
+            keys.append(torch.full((other.numel(),), big, dtype=torch.int64, device=dev)
+                        .scatter_reduce(0, item, kl, "amin") // nnn)
+        else:
+            keys.append(gp.new_zeros(0))
+        total = sum(int(k.numel()) for k in keys)
+        eb = max(1, round(_DSSUM_ITEMS * E / total)) if total else 1
+        nb = (E + eb - 1) // eb if total else 0
+        edges = torch.arange(nb + 1, device=dev, dtype=torch.int64) * eb
+        self.cls_nb, self.cls_eb = nb, eb
+        self.cls_bstart = torch.cat([torch.searchsorted(k.contiguous(), edges) for k in keys]).to(torch.int32) \
+            if nb else torch.zeros(4, dtype=torch.int32, device=dev)
 
     def fused_plan(self, perm=None, chunk_pairs=None, lag=None):
         """Schedule for the fused Ax+dssum kernel (sf_ax_dssum8_f64), single rank.
@@ -321,9 +352,14 @@ class GatherScatter:
         if not hasattr(self, "cls_perm"):
             self._build_classes()
         n2, n4, n8 = self.cls_n
-        _lib.call("sf_dssum_cls_f64", _lib.ptr(v), _lib.ptr(self.cls_perm if perm is None else perm), n2, n4, n8,
-                  _lib.ptr(self.cls_gen_off), self.cls_n_gen, mode, _lib.ptr(u), _lib.ptr(recv), self.P,
-                  _lib.stream_ptr(self.device))
+        pm = self.cls_perm if perm is None else perm
+        if _DSSUM_KERNEL == "cls":
+            _lib.call("sf_dssum_cls_f64", _lib.ptr(v), _lib.ptr(pm), n2, n4, n8, _lib.ptr(self.cls_gen_off),
+                      self.cls_n_gen, mode, _lib.ptr(u), _lib.ptr(recv), self.P, _lib.stream_ptr(self.device))
+        else:
+            _lib.call("sf_dssum_blk_f64", _lib.ptr(v), _lib.ptr(pm), n2, n4, n8, _lib.ptr(self.cls_gen_off),
+                      _lib.ptr(self.cls_bstart), self.cls_nb, mode, _lib.ptr(u), _lib.ptr(recv), self.P,
+                      _lib.stream_ptr(self.device))
 
     def _dssum_rows(self, flat, mode, u=None):
         for row in range(flat.shape[0]):

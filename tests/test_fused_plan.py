@@ -118,3 +118,28 @@ def test_fused_plan_schedule(golden_spaces, key, masked, chunk_pairs, lag):
         want = np.where(shared & ~km, u, want)
     want = np.where(np.bincount(gid)[gid] > 1, want, w)
     assert np.array_equal(out, want)
+
+
+@pytest.mark.parametrize("key", ["pbox543", "pbox322", "rotor", "cube222"])
+def test_dssum_block_ranges(golden_spaces, key):
+    """sf_dssum_blk_f64 schedule: per class, block b's items are exactly those whose
+    lowest local copy lies in elements [b*eb, (b+1)*eb); every item once."""
+    gs, E, nnn = _gs(golden_spaces, key)
+    gs._build_classes()
+    nb, eb = gs.cls_nb, gs.cls_eb
+    bs = gs.cls_bstart.numpy().reshape(4, nb + 1)
+    perm = gs.cls_perm.numpy()
+    n2, n4, n8 = gs.cls_n
+    go = gs.cls_gen_off.numpy()
+    items = []
+    o = 0
+    for c, n in ((2, n2), (4, n4), (8, n8)):
+        items.append([perm[o + c * i:o + c * (i + 1)] for i in range(n)])
+        o += c * n
+    items.append([perm[o + go[i]:o + go[i + 1]] for i in range(gs.cls_n_gen)])
+    assert nb * eb >= E
+    for row, its in zip(bs, items):
+        assert row[0] == 0 and row[-1] == len(its) and np.all(np.diff(row) >= 0)
+        for b in range(nb):
+            for it in its[row[b]:row[b + 1]]:
+                assert b * eb <= it.min() // nnn < (b + 1) * eb

@@ -12,9 +12,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2207_07098_b200", "variants")
-VARIANTS = {
-    "fused_batch1": "-DSF_DSS_BATCH=1",
-}
+VARIANTS = {}
 
 
 def build():
@@ -60,7 +58,7 @@ def run(ne):
         for name, args in _lib._SIGS.items():
             getattr(L, name).argtypes = args
         res = {}
-        for kind in ("masked", "plain", "dssum"):
+        for kind in ("masked", "plain", "dssum", "dssum_blk"):
             def fn():
                 if kind == "masked":
                     L.sf_ax_masked_f64(sp.dmat.ctypes.data, 8, sp.geom.data_ptr(), sp.bm.data_ptr(), u.data_ptr(),
@@ -69,6 +67,12 @@ def run(ne):
                 elif kind == "plain":
                     L.sf_ax_helm_f64(sp.dmat.ctypes.data, 8, sp.geom.data_ptr(), sp.bm.data_ptr(), u.data_ptr(),
                                      w.data_ptr(), sp.n_elements, 1.0, 0.0, 0, st)
+                elif kind == "dssum_blk":
+                    if not hasattr(gs, "cls_nb"):
+                        gs._build_classes()
+                    n2, n4, n8 = gs.cls_n
+                    L.sf_dssum_blk_f64(w.data_ptr(), op.sh_perm.data_ptr(), n2, n4, n8, gs.cls_gen_off.data_ptr(),
+                                       gs.cls_bstart.data_ptr(), gs.cls_nb, 2, u.data_ptr(), None, 0, st)
                 else:
                     if hasattr(L, "sf_dssum_cls_f64"):
                         n2, n4, n8 = gs.cls_n
@@ -112,7 +116,7 @@ def run(ne):
                     res[f"{kind}{cpl}"] = float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3
         gbs = P * 64 / (res["masked"] * 1e-6) / 1e9
         print(f"{os.path.basename(path):24s} masked {res['masked']:8.1f} us ({gbs:6.0f} GB/s)  plain {res['plain']:8.1f} us"
-              f"  dssum {res['dssum']:7.1f} us", flush=True)
+              f"  dssum {res['dssum']:7.1f} us  dssum_blk {res['dssum_blk']:7.1f} us", flush=True)
         fk = {k: round(v, 1) for k, v in res.items() if k.startswith("f")}
         if fk:
             print("   fused:", fk, flush=True)
