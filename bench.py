@@ -206,7 +206,7 @@ def time_kernels(sp, op, u, reps=20):
 
 #: dram__bytes_read.sum + dram__bytes_write.sum per launch of the MGS pass, from
 #: the ncu --set full capture committed under profiles/ (keyed by mesh size)
-MGS_TRAFFIC = {}
+MGS_TRAFFIC = {"64": 4431794000}     # profiles/r1_ncu_full_tgv64.json: 3.355504 + 1.076290 GB
 
 
 def time_mgs(sp, w0, reps=20):
