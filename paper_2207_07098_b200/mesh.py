@@ -84,3 +84,166 @@ def gen_box_mesh(extent, counts, tags=None):
     ft = np.asarray(tag_idx, dtype=np.int64)[ff]
     return Mesh(vertices=vertices, elements=elements, facet_elem=fe, facet_face=ff,
                 facet_tag=ft, tag_names=tuple(names))
+
+
+# --------------------------------------------------------------------------- cylinder in a box
+
+CYLINDER_TAGS = ("inflow", "outflow", "bottom", "top", "span", "cylinder")
+
+
+def _gll_points(order):
+    from .basis import make_basis
+
+    return make_basis(order).points
+
+
+def gen_cylinder_box_mesh(diameter, xlim, zlim, height, n_azimuthal=8, n_radial=2, n_axial=2,
+                          n_upstream=None, n_downstream=None, n_front=None, n_back=None, collar=None,
+                          geom_order=7):
+    """Vertical cylinder (axis x = z = 0, standing on y = 0) in a box: an O-grid of
+    n_azimuthal x n_radial columns in the square collar [-c, c]^2 and eight
+    Cartesian frame blocks around it, n_axial layers in y (mesh.py:231-438).
+
+    Same mesh as the reference, bit for bit: vertices numbered by first
+    appearance over the element corners (coordinates compared as values, so
+    -0.0 == 0.0), elements O-grid first (layer, ring, sector), then the frame
+    blocks (upstream, downstream, front, back, then the four corners), facets per
+    element in the reference's order, and curved records (GLL lattice of
+    ``geom_order``) for the ring touching the cylinder.  Vectorised: the config-5
+    mesh (2 M elements) builds in seconds instead of the reference's 33 s.
+    Tags: inflow (x = xlim[0]), outflow (x = xlim[1]), bottom (y = 0),
+    top (y = height), span (both z sides), cylinder.
+    """
+    if n_azimuthal % 4 != 0 or n_azimuthal < 4:
+        raise ValueError("n_azimuthal must be a positive multiple of 4")
+    if n_radial < 1 or n_axial < 1:
+        raise ValueError("n_radial and n_axial must be >= 1")
+    if geom_order < 1:
+        raise ValueError("geom_order must be >= 1")
+    radius = float(diameter) / 2.0
+    if radius <= 0:
+        raise ValueError("diameter must be positive")
+    c = float(collar) if collar is not None else float(diameter)
+    if c <= radius:
+        raise ValueError(f"collar half-width {c} must exceed the cylinder radius {radius}")
+    x0, x1 = float(xlim[0]), float(xlim[1])
+    z0, z1 = float(zlim[0]), float(zlim[1])
+    height = float(height)
+    if not (x0 < -c < c < x1 and z0 < -c < c < z1):
+        raise ValueError(f"box must strictly contain the collar square [-{c}, {c}]^2: got x={xlim}, z={zlim}")
+    if height <= 0:
+        raise ValueError("height must be positive")
+    a = n_azimuthal // 4
+
+    def frame_count(given, dist):
+        return int(given) if given is not None else max(1, int(round(dist / (2.0 * c))))
+
+    n_up, n_down = frame_count(n_upstream, -c - x0), frame_count(n_downstream, x1 - c)
+    n_fr, n_bk = frame_count(n_front, -c - z0), frame_count(n_back, z1 - c)
+    if min(n_up, n_down, n_fr, n_bk) < 1:
+        raise ValueError("frame element counts must be >= 1")
+
+    u_side = np.linspace(-c, c, a + 1)
+    ys = np.linspace(0.0, height, n_axial + 1)
+    naz = 4 * a
+    # collar square walked counterclockwise from (+c, -c): one point per sector boundary
+    jj = np.arange(a)
+    sq = np.concatenate([
+        np.stack([np.full(a, c), u_side[jj]], axis=1),
+        np.stack([u_side[a - jj], np.full(a, c)], axis=1),
+        np.stack([np.full(a, -c), u_side[a - jj]], axis=1),
+        np.stack([u_side[jj], np.full(a, -c)], axis=1)])
+    theta = np.arctan2(sq[:, 1], sq[:, 0])
+    circ = np.stack([radius * np.cos(theta), radius * np.sin(theta)], axis=1)
+    sigma = (np.arange(n_radial + 1) / n_radial)[:, None, None]
+    ring = (1.0 - sigma) * circ[None, :, :] + sigma * sq[None, :, :]      # (n_radial+1, naz, 2)
+
+    cr = np.arange(8) & 1
+    cs = (np.arange(8) >> 1) & 1
+    ct = (np.arange(8) >> 2) & 1
+    t_in, t_out, t_bot, t_top, t_span, t_cyl = range(6)
+    corner_blocks, facet_lists = [], []   # per block: (E_b, 8, 3) corners; (elem, face, tag, rank) facets
+    e_base = 0
+
+    # O-grid, local axes (r, s, t) = (azimuthal, radial, vertical); loops m, j, k
+    m, j, k = (g.ravel() for g in np.meshgrid(np.arange(n_axial), np.arange(n_radial), np.arange(naz),
+                                               indexing="ij"))
+    kk = np.where(cr[None, :] == 1, ((k + 1) % naz)[:, None], k[:, None])
+    p = ring[j[:, None] + cs[None, :], kk]                                  # (E_o, 8, 2)
+    corner_blocks.append(np.stack([p[..., 0], ys[m[:, None] + ct[None, :]], p[..., 1]], axis=-1))
+    eo = np.arange(m.size)
+    facet_lists.append((eo[j == 0], 2, t_cyl, 0))
+    facet_lists.append((eo[m == 0], 4, t_bot, 1))
+    facet_lists.append((eo[m == n_axial - 1], 5, t_top, 2))
+    e_base = m.size
+
+    def block(xc, zc, xlo=None, xhi=None, zlo=None, zhi=None):
+        nonlocal e_base
+        nx, nz = len(xc) - 1, len(zc) - 1
+        bm, biz, bix = (g.ravel() for g in np.meshgrid(np.arange(n_axial), np.arange(nz), np.arange(nx),
+                                                      indexing="ij"))
+        corner_blocks.append(np.stack([xc[bix[:, None] + cs[None, :]], ys[bm[:, None] + ct[None, :]],
+                                       zc[biz[:, None] + cr[None, :]]], axis=-1))
+        eb = e_base + np.arange(bm.size)
+        for sel, face, tag, rank in ((biz == 0, 0, zlo, 0), (biz == nz - 1, 1, zhi, 1),
+                                     (bix == 0, 2, xlo, 2), (bix == nx - 1, 3, xhi, 3),
+                                     (bm == 0, 4, t_bot, 4), (bm == n_axial - 1, 5, t_top, 5)):
+            if tag is not None:
+                facet_lists.append((eb[sel], face, tag, rank))
+        e_base += bm.size
+
+    xs_left, xs_right = np.linspace(x0, -c, n_up + 1), np.linspace(c, x1, n_down + 1)
+    zs_front, zs_back = np.linspace(z0, -c, n_fr + 1), np.linspace(c, z1, n_bk + 1)
+    block(xs_left, u_side, xlo=t_in)
+    block(xs_right, u_side, xhi=t_out)
+    block(u_side, zs_front, zlo=t_span)
+    block(u_side, zs_back, zhi=t_span)
+    block(xs_left, zs_front, xlo=t_in, zlo=t_span)
+    block(xs_right, zs_front, xhi=t_out, zlo=t_span)
+    block(xs_left, zs_back, xlo=t_in, zhi=t_span)
+    block(xs_right, zs_back, xhi=t_out, zhi=t_span)
+
+    corners = np.concatenate(corner_blocks).reshape(-1, 3)
+    # vertex ids by first appearance, values compared with -0.0 == 0.0 (the
+    # reference keys a dict on float tuples)
+    key = np.ascontiguousarray(corners + 0.0).view(np.dtype((np.void, 24))).ravel()
+    _, first, inv = np.unique(key, return_index=True, return_inverse=True)
+    rank_of = np.empty(first.size, dtype=np.int64)
+    rank_of[np.argsort(first, kind="stable")] = np.arange(first.size)
+    vertices = corners[np.sort(first)]
+    elements = rank_of[inv.ravel()].reshape(-1, 8)
+
+    fe = np.concatenate([f[0] for f in facet_lists])
+    ff = np.concatenate([np.full(f[0].size, f[1], dtype=np.int64) for f in facet_lists])
+    ft = np.concatenate([np.full(f[0].size, f[2], dtype=np.int64) for f in facet_lists])
+    fr = np.concatenate([np.full(f[0].size, f[3], dtype=np.int64) for f in facet_lists])
+    order = np.lexsort((fr, fe))
+
+    # curved records of the O-grid ring touching the cylinder (j == 0)
+    xi01 = (_gll_points(geom_order) + 1.0) / 2.0
+    ng1 = geom_order + 1
+    recs_k = []
+    for kq in range(naz):
+        k1 = (kq + 1) % naz
+        th_lo, th_hi = theta[kq], theta[k1]
+        while th_hi <= th_lo:
+            th_hi += 2.0 * np.pi
+        th_i = th_lo + xi01 * (th_hi - th_lo)
+        arc = np.stack([radius * np.cos(th_i), radius * np.sin(th_i)], axis=1)
+        outer = ring[1, kq][None, :] + xi01[:, None] * (ring[1, k1] - ring[1, kq])[None, :]
+        recs_k.append((1.0 - xi01)[None, :, None] * arc[:, None, :] + xi01[None, :, None] * outer[:, None, :])
+    curved_elem, curved = [], []
+    for mq in range(n_axial):
+        yy = ys[mq] + xi01 * (ys[mq + 1] - ys[mq])
+        for kq in range(naz):
+            blend = recs_k[kq]
+            rec = np.empty((ng1, ng1, ng1, 3))
+            rec[:, :, :, 0] = blend[:, :, None, 0]
+            rec[:, :, :, 2] = blend[:, :, None, 1]
+            rec[:, :, :, 1] = yy[None, None, :]
+            curved_elem.append((mq * n_radial + 0) * naz + kq)
+            curved.append(rec)
+    return Mesh(vertices=vertices, elements=elements, facet_elem=fe[order], facet_face=ff[order],
+                facet_tag=ft[order], tag_names=CYLINDER_TAGS,
+                curved_elem=np.asarray(curved_elem, dtype=np.int64), curved_coords=np.asarray(curved),
+                geom_order=geom_order)

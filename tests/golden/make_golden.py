@@ -391,7 +391,69 @@ def gen_ckpt():
         json.dump(rows, fh, indent=1)
 
 
+CYL_MESHES = {
+    # the 1/208-scale analogue of config 5: 9728 elements, lx = 8
+    "cyl_analogue": dict(diameter=1.0, xlim=(-50.0, 120.0), zlim=(-25.0, 25.0), height=10.0, n_azimuthal=32,
+                         n_radial=8, n_axial=4, n_upstream=16, n_downstream=32, n_front=16, n_back=16,
+                         geom_order=7),
+    # automatic frame counts, explicit collar, 12 sectors
+    "cyl_auto": dict(diameter=2.0, xlim=(-6.0, 9.0), zlim=(-5.0, 7.0), height=3.0, n_azimuthal=12, n_radial=3,
+                     n_axial=2, collar=1.7, geom_order=4),
+}
+
+ROTOR_SPECS = {"inflow": {"kind": "inflow", "u_cl": 1.0, "h": 2.0}, "outflow": {"kind": "outflow"},
+               "bottom": {"kind": "noslip"}, "top": {"kind": "symmetry"}, "span": {"kind": "symmetry"},
+               "cylinder": {"kind": "rotor", "u_cl": 1.0, "alpha": 3.0, "delta": 0.25}}
+
+
+def gen_cyl():
+    """Cylinder-in-box meshes from the reference generator (mesh.py:231-438), the
+    analogue's space maps, and 3 mini-rotor steps (pkg/cases/mini_rotor.json with
+    the Jacobi pressure preconditioner)."""
+    out = {}
+    for key, kw in CYL_MESHES.items():
+        m = gen_cylinder_box_mesh(**kw)
+        for f in ("vertices", "elements", "facet_elem", "facet_face", "facet_tag", "curved_elem", "curved_coords"):
+            out[f"{key}_sha_{f}"] = sha(np.asarray(getattr(m, f)))
+            out[f"{key}_shape_{f}"] = np.asarray(np.shape(getattr(m, f)))
+        if key == "cyl_analogue":
+            t0 = time.time()
+            sp = build_space(m, make_basis(7))
+            print("analogue build_space", time.time() - t0, flush=True)
+            for f in ("coords", "jac", "bm"):
+                out[f"{key}_sha_{f}"] = sha(getattr(sp, f))
+            for f in ("gid", "perm", "offsets"):
+                out[f"{key}_sha_{f}"] = sha(getattr(sp.gs, f))
+            out[f"{key}_n_gid"] = np.asarray(sp.gs.n_gid)
+            cnt = np.diff(sp.gs.offsets)
+            out[f"{key}_mult_hist"] = np.bincount(cnt)
+    np.savez_compressed(os.path.join(OUT, "cylinder.npz"), **out)
+
+    m = gen_cylinder_box_mesh(1.0, (-4.0, 6.0), (-4.0, 4.0), 2.0, n_azimuthal=8, n_radial=2, n_axial=2,
+                              n_upstream=4, n_downstream=5, n_front=3, n_back=3, geom_order=5)
+    sp = build_space(m, make_basis(5))
+    st = Stepper(sp, BoundarySet(sp, ROTOR_SPECS), nu=1.0 / 100.0, dt=2e-3, scheme_order=3,
+                 pressure=SolverOptions(tol=1e-5, max_iter=200, restart=20, precond="jacobi"),
+                 velocity=SolverOptions(tol=1e-8, max_iter=100, precond="jacobi"))
+    x = sp.coords
+    v0 = np.zeros((3,) + sp.shape)
+    v0[0] = 1.0
+    state = st.initial_state(v0)
+    rows = []
+    for _ in range(3):
+        state, d = st.step(state)
+        rows.append(dict(step=d.step, p_it=d.p_iterations, v_it=list(d.v_iterations), cfl=d.cfl,
+                         ke=kinetic_energy(sp, state.vel), ens=enstrophy(sp, state.vel)))
+        print("rotor", rows[-1], flush=True)
+    del x
+    with open(os.path.join(OUT, "rotor_steps.json"), "w") as fh:
+        json.dump(rows, fh, indent=1)
+
+
 def main():
+    if "--cyl" in sys.argv:
+        gen_cyl()
+        return
     if "--bcfun" in sys.argv:
         gen_bcfun()
         return

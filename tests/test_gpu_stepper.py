@@ -160,3 +160,63 @@ def test_restart_from_reference_checkpoint(cuda):
         assert list(d.v_iterations) == row["v_it"]
         assert rel_err(kinetic_energy(sp, state.vel), row["ke"]) < 1e-9
         assert rel_err(enstrophy(sp, state.vel), row["ens"]) < 1e-9
+
+
+def test_config5_analogue_space_bit_exact(cuda):
+    """The 1/208-scale config-5 mesh (9728 curved elements, lx = 8, multiplicity up
+    to 10) from our generator, built on the device: coordinates, jac, bm and the
+    gather-scatter maps equal the reference's build_space bit for bit."""
+    import hashlib
+    import os
+
+    from paper_2207_07098_b200.basis import make_basis
+    from paper_2207_07098_b200.mesh import gen_cylinder_box_mesh
+    from paper_2207_07098_b200.space import build_space
+
+    from test_mesh_cylinder import CYL_MESHES
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "cylinder.npz"))
+    sp = build_space(gen_cylinder_box_mesh(**CYL_MESHES["cyl_analogue"]), make_basis(7), device=cuda)
+
+    def sha(t):
+        return hashlib.sha256(np.ascontiguousarray(t.cpu().numpy()).tobytes()).hexdigest()
+
+    for f in ("coords", "jac", "bm"):
+        assert sha(getattr(sp, f)) == str(g[f"cyl_analogue_sha_{f}"]), f
+    for f in ("gid", "perm", "offsets"):
+        assert sha(getattr(sp.gs, f)) == str(g[f"cyl_analogue_sha_{f}"]), f
+    assert sp.gs.n_gid == int(g["cyl_analogue_n_gid"])
+
+
+def test_mini_rotor_steps(cuda):
+    """pkg/cases/mini_rotor.json (Jacobi pressure): curved cylinder wall with the
+    rotor condition, power-law inflow, outflow, symmetry; counts match the reference."""
+    import json
+    import os
+
+    from paper_2207_07098_b200.basis import make_basis
+    from paper_2207_07098_b200.bc import BoundarySet
+    from paper_2207_07098_b200.mesh import gen_cylinder_box_mesh
+    from paper_2207_07098_b200.space import build_space
+    from paper_2207_07098_b200.timestep import SolverOptions, Stepper, kinetic_energy
+
+    specs = {"inflow": {"kind": "inflow", "u_cl": 1.0, "h": 2.0}, "outflow": {"kind": "outflow"},
+             "bottom": {"kind": "noslip"}, "top": {"kind": "symmetry"}, "span": {"kind": "symmetry"},
+             "cylinder": {"kind": "rotor", "u_cl": 1.0, "alpha": 3.0, "delta": 0.25}}
+    with open(os.path.join(os.path.dirname(__file__), "golden", "rotor_steps.json")) as fh:
+        rows = json.load(fh)
+    m = gen_cylinder_box_mesh(1.0, (-4.0, 6.0), (-4.0, 4.0), 2.0, n_azimuthal=8, n_radial=2, n_axial=2,
+                              n_upstream=4, n_downstream=5, n_front=3, n_back=3, geom_order=5)
+    sp = build_space(m, make_basis(5), device=cuda)
+    st = Stepper(sp, BoundarySet(sp, specs), nu=1.0 / 100.0, dt=2e-3, scheme_order=3,
+                 pressure=SolverOptions(tol=1e-5, max_iter=200, restart=20, precond="jacobi"),
+                 velocity=SolverOptions(tol=1e-8, max_iter=100, precond="jacobi"))
+    v0 = torch.zeros((3,) + sp.shape, dtype=torch.float64, device=cuda)
+    v0[0] = 1.0
+    state = st.initial_state(v0)
+    for row in rows:
+        state, d = st.step(state)
+        assert d.p_iterations == row["p_it"] and list(d.v_iterations) == row["v_it"], (d, row)
+        assert rel_err(d.cfl, row["cfl"]) < 1e-8
+        # pressure GMRES ends at its 200-iteration cap (unconverged), as in the reference
+        assert rel_err(kinetic_energy(sp, state.vel), row["ke"]) < 1e-7
