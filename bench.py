@@ -1,13 +1,17 @@
 """Benchmark of the SEM hot path on B200 (one JSON line on rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload tgv|poisson|channel] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload tgv|poisson|channel|cylinder]
+                    [--ne N] [--impl ours|reference]
 
 Workloads (BASELINE.json configs):
   poisson  config 2: Jacobi-PCG on the 32^3-element lx=8 box, Dirichlet walls;
            one step = one PCG solve (42 iterations, tol 1e-8, identical to the
            reference's count); metric value = P * iterations / t (GDOF/s of
            operator work).
-  tgv      configs 1/3: BDF3/EXT3 Taylor-Green step (see bench_tgv in this file).
+  tgv      configs 1/3 (default): BDF3/EXT3 Taylor-Green step, 64^3 (--ne).
+  channel  config 4: 48x32x48 channel box (--ne scales it).
+  cylinder config 5: cylinder-in-box (Flettner rotor) mesh, counts / --ne
+           (default 2: 252 928 curved elements, 129 M points).
 
 Timing: W untimed warm-up steps, then K steps bracketed by barrier +
 synchronize, timed with CUDA events on the launching stream, max over ranks.
@@ -399,6 +403,41 @@ def cpu_channel_sample(budget=20.0):
                       f"(pressure its {its}), mean {t:.2f} s/step"}
 
 
+def cpu_cylinder_sample(budget=20.0):
+    """Oracle on the config-5 set-up at counts / 16 (456 curved elements, lx=8):
+    mean step time over the first steps within the budget.  The mesh comes from
+    the package's generator, which is bit-identical to the reference's."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import semflow_oracle as O
+
+    from paper_2207_07098_b200.mesh import gen_cylinder_box_mesh
+    from paper_2207_07098_b200.timestep import cylinder_params
+
+    prm = cylinder_params(16)
+    sp = O.build_space(gen_cylinder_box_mesh(**prm), O.make_basis(7))
+    bc = O.Boundary(sp, {"inflow": {"kind": "inflow", "u_cl": 1.0, "h": prm["height"]}, "outflow": {"kind": "outflow"},
+                         "bottom": {"kind": "noslip"}, "top": {"kind": "symmetry"}, "span": {"kind": "symmetry"},
+                         "cylinder": {"kind": "rotor", "u_cl": 1.0, "alpha": 3.0, "delta": 0.25}})
+    st = O.Stepper(sp, bc, 1.0 / 100.0, 2e-3)
+    v0 = np.zeros((3,) + sp.shape)
+    v0[0] = 1.0
+    state = st.initial_state(v0)
+    P = int(np.prod(sp.shape))
+    times, its = [], []
+    t_all = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        state, d = st.step(state)
+        times.append(time.perf_counter() - t0)
+        its.append(d.p_iterations)
+        if time.perf_counter() - t_all > budget:
+            break
+    t = float(np.mean(times))
+    return {"value": P / t / 1e9, "unit": "GDOF/s", "cores": O.num_threads(), "kind": "port",
+            "sample": f"oracle cylinder config-5 counts/16 ({sp.shape[0]} elements, {P} points), steps "
+                      f"1-{len(times)} (pressure its {its}), mean {t:.2f} s/step"}
+
+
 def bench_tgv(args, world, rank, dev):
     import torch
 
@@ -419,6 +458,12 @@ def bench_tgv(args, world, rank, dev):
         ne = counts
         sp, st, state = channel_problem(counts, device=dev, comm=comm)
         P = counts[0] * counts[1] * counts[2] * sp.n ** 3
+    elif args.workload == "cylinder":
+        from paper_2207_07098_b200.timestep import cylinder_problem
+
+        ne = args.ne or 2                    # scale divisor of the config-5 counts
+        sp, st, state = cylinder_problem(ne, device=dev, comm=comm)
+        P = sp.mesh.n_elements * sp.n ** 3
     else:
         ne = args.ne or (64 if args.warmup + args.steps <= 8 else 48)
         sp, st, state = tgv_problem(ne, device=dev, comm=comm)
@@ -482,6 +527,11 @@ def bench_tgv(args, world, rank, dev):
                    " Poiseuille inflow/outflow/no-slip/symmetry, nu=1/2800 dt=2e-3, Jacobi-GMRES(20) p 1e-5,"
                    " Jacobi-PCG v 1e-8, projection on")
         metric = "GDOF/s per time step (channel, lx=8)"
+    elif args.workload == "cylinder":
+        wl_name = (f"cylinder-in-box (Flettner-rotor) {sp.mesh.n_elements} curved/unstructured hex elements lx=8"
+                   f" (config 5{'' if ne == 1 else f' counts / {ne}'}), rotor wall, power-law inflow, Re=100"
+                   " dt=2e-3, Jacobi-GMRES(20) p 1e-5, Jacobi-PCG v 1e-8, projection on")
+        metric = "GDOF/s per time step (cylinder, lx=8)"
     else:
         wl_name = (f"TGV Re=1600 {ne}^3 elements lx=8 (config {'3' if ne == 64 else '1' if ne == 8 else '1/3 analogue'}),"
                    " symmetry box, Jacobi-GMRES(20) p 1e-5, Jacobi-PCG v 1e-8, projection on")
@@ -518,7 +568,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--workload", default="tgv", choices=("tgv", "poisson", "channel"))
+    ap.add_argument("--workload", default="tgv", choices=("tgv", "poisson", "channel", "cylinder"))
     ap.add_argument("--ne", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -533,6 +583,9 @@ def main():
         elif args.workload == "channel":
             base = cpu_channel_sample()
             metric = "GDOF/s per time step (channel, lx=8)"
+        elif args.workload == "cylinder":
+            base = cpu_cylinder_sample()
+            metric = "GDOF/s per time step (cylinder, lx=8)"
         else:
             base = cpu_poisson_sample()
             metric = "GDOF/s per PCG iteration (config 2: Poisson Ax+dssum+Jacobi-CG, 32^3 lx=8)"
@@ -555,6 +608,7 @@ def main():
             # CPU port finishes in seconds (config 1)
             line["cpu_baseline"] = {"tgv": lambda: cpu_tgv_sample(steps=args.steps, warmup=args.warmup),
                                     "channel": lambda: cpu_channel_sample(),
+                                    "cylinder": lambda: cpu_cylinder_sample(),
                                     "poisson": cpu_poisson_sample}[args.workload]()
         print(json.dumps(line), flush=True)
     if world > 1:
