@@ -547,7 +547,10 @@ def bench_tgv(args, world, rank, dev):
                    "peak_mem_gb_rank0": torch.cuda.max_memory_allocated() / 1e9,
                    "alloc_retries_rank0": int(torch.cuda.memory_stats().get("num_alloc_retries", 0)),
                    "l2": "inputs larger than L2" if P * 8 * 6 / world > 126e6 else "working set may be L2-resident",
-                   "parallelism": (f"element partition x{world} (z-slabs), NCCL halo exchange + allgather dots"
+                   "parallelism": (f"element partition x{world} (contiguous element ranges), "
+                                   + ("NVLink IPC halo exchange + peer-memory glsc3 allreduce fused into the "
+                                      "Krylov kernels" if sp.comm.peer is not None else
+                                      "NCCL halo exchange + all-gather dots")
                                    if world > 1 else "single")},
         "roofline": {"bound": "hbm", "achieved": mgs_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": mgs_gbs / pk["hbm_gbs"], "traffic": MGS_TRAFFIC.get(str(ne)),

@@ -105,7 +105,8 @@ int sf_dssum_f64(double* v, const int* offsets, const int* perm, int n_shared, i
                  const double* u, const double* recv, int n_local, void* stream);
 
 /* The same dssum with the shared gids stored by multiplicity class (the layout
- * space.GatherScatter uses): perm holds n2 index pairs, then n4 quadruples, then
+ * space.GatherScatter uses): perm holds n2 index pairs (the segment padded to a
+ * multiple of 4 ints, so perm must be 16-byte aligned), then n4 quadruples, then
  * n8 octets (fixed stride, no offsets), then the CSR part of n_gen gids of any
  * other multiplicity (gen_offsets, n_gen+1 entries relative to that part).  Same
  * modes, flags, halo convention and per-gid order as sf_dssum_f64. */

@@ -75,6 +75,10 @@ __global__ void dssum_shared_kernel(double* __restrict__ v, const int* __restric
 // loads and two stores -- the offsets load is gone from the dependent chain that
 // bounds the CSR kernel (ncu: 30 cycles of long-scoreboard stall per instruction,
 // 39 % of DRAM peak).  Per-gid order and arithmetic are unchanged.
+// The pairs segment is padded to a multiple of 4 ints so the quads and octets
+// that follow are 16-byte aligned for their int4 loads.
+__host__ __device__ __forceinline__ long long pairs_span(int n2) { return (2LL * n2 + 3) & ~3LL; }
+
 template <int MODE>
 __device__ __forceinline__ void dss_finish(double* __restrict__ v, const double* __restrict__ u,
                                            const int* idx, int c, double acc, int n_local) {
@@ -112,7 +116,7 @@ dssum_cls_kernel(double* __restrict__ v, const int* __restrict__ perm, int n2, i
     return;
   }
   g -= n2;
-  const int* p4 = perm + 2LL * n2;
+  const int* p4 = perm + pairs_span(n2);
   if (g < n4) {
     const int4 q = __ldg(reinterpret_cast<const int4*>(p4) + g);
     const int idx[4] = {q.x, q.y, q.z, q.w};
@@ -169,9 +173,9 @@ dssum_blk_kernel(double* __restrict__ v, const int* __restrict__ perm, int n2, i
                  const double* __restrict__ u, const double* __restrict__ recv, int n_local) {
   const int b = blockIdx.x;
   const int2* p2 = reinterpret_cast<const int2*>(perm);
-  const int4* p4 = reinterpret_cast<const int4*>(perm + 2LL * n2);
-  const int4* p8 = reinterpret_cast<const int4*>(perm + 2LL * n2 + 4LL * n4);
-  const int* pg = perm + 2LL * n2 + 4LL * n4 + 8LL * n8;
+  const int4* p4 = reinterpret_cast<const int4*>(perm + pairs_span(n2));
+  const int4* p8 = reinterpret_cast<const int4*>(perm + pairs_span(n2) + 4LL * n4);
+  const int* pg = perm + pairs_span(n2) + 4LL * n4 + 8LL * n8;
   {
     const int s = __ldg(bstart + b), e = __ldg(bstart + b + 1);
     for (int g = s + threadIdx.x; g < e; g += 2 * blockDim.x) {

@@ -205,7 +205,11 @@ class GatherScatter:
             gen_off[1:] = torch.cumsum(oc, 0)
         within = torch.arange(int(gen_off[-1]), device=dev) - torch.repeat_interleave(gen_off[:-1], oc)
         parts.append(self.sh_perm[torch.repeat_interleave(off[other], oc) + within])
-        self.cls_perm = torch.cat(parts).to(torch.int32).contiguous()
+        # pairs segment padded to a multiple of 4 ints: the quads/octets after it
+        # are read as 16-byte int4 (csrc/gs.cu pairs_span)
+        self.cls_pad2 = (-2 * n[2]) % 4
+        pad = torch.zeros(self.cls_pad2, dtype=parts[0].dtype, device=dev)
+        self.cls_perm = torch.cat([parts[0], pad] + parts[1:]).to(torch.int32).contiguous()
         self.cls_n = (n[2], n[4], n[8])
         self.cls_gen_off = gen_off.to(torch.int32).contiguous()
         self.cls_n_gen = int(other.numel())
@@ -276,7 +280,7 @@ class GatherScatter:
             counts.append(torch.bincount(chunk_hi, minlength=K)[:K])
             los.append(torch.full((K,), 2**31 - 1, dtype=torch.int64, device=dev).scatter_reduce(
                 0, chunk_hi, chunk_lo, "amin"))
-            o += c * n
+            o += c * n + (self.cls_pad2 if c == 2 else 0)
         goff = self.cls_gen_off.long()
         ng = self.cls_n_gen
         gflat = flat[o:]

@@ -59,6 +59,17 @@ def main():
     ok["dssum_repeat"] = all(bool(torch.equal(o, full.gs.add(u_full * float(k + 1))[e0:e1]))
                              for k, o in enumerate(outs))
     ok["halo_path"] = "ipc" if getattr(part.gs, "_ipc", None) is not None else "nccl"
+    # unstructured: the curved mini-rotor mesh (multiplicities up to 10, odd class sizes)
+    from paper_2207_07098_b200.mesh import gen_cylinder_box_mesh
+
+    rm = gen_cylinder_box_mesh(1.0, (-4.0, 6.0), (-4.0, 4.0), 2.0, n_azimuthal=8, n_radial=2, n_axial=2,
+                               n_upstream=4, n_downstream=5, n_front=3, n_back=3, geom_order=5)
+    rfull = build_space(rm, make_basis(5), device=dev)
+    rpart = build_space(rm, make_basis(5), device=dev, comm=comm)
+    q0, q1 = rpart.e_range
+    ru = torch.randn(rfull.shape, generator=g, dtype=torch.float64).to(dev)
+    ok["rotor_dssum"] = bool(torch.equal(rpart.gs.add(ru[q0:q1].contiguous()), rfull.gs.add(ru)[q0:q1]))
+    del rfull, rpart
     del full
     torch.cuda.empty_cache()
     res = {"world": W, "ne": ne, "checks": ok}

@@ -90,7 +90,7 @@ def test_fused_plan_schedule(golden_spaces, key, masked, chunk_pairs, lag):
     o = 0
     for c, n in ((2, n2), (4, n4), (8, n8)):
         ref_items += [tuple(int(x) for x in r) for r in cls_perm[o:o + c * n].reshape(-1, c)]
-        o += c * n
+        o += c * n + (gs.cls_pad2 if c == 2 else 0)
     go = gs.cls_gen_off.numpy()
     ref_items += [tuple(int(x) for x in cls_perm[o + go[i]:o + go[i + 1]]) for i in range(gs.cls_n_gen)]
     assert sorted(seen) == sorted(ref_items)
@@ -135,7 +135,8 @@ def test_dssum_block_ranges(golden_spaces, key):
     o = 0
     for c, n in ((2, n2), (4, n4), (8, n8)):
         items.append([perm[o + c * i:o + c * (i + 1)] for i in range(n)])
-        o += c * n
+        o += c * n + (gs.cls_pad2 if c == 2 else 0)
+        assert c != 2 or o % 4 == 0        # quads start 16-byte aligned
     items.append([perm[o + go[i]:o + go[i + 1]] for i in range(gs.cls_n_gen)])
     assert nb * eb >= E
     for row, its in zip(bs, items):
