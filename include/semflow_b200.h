@@ -120,10 +120,20 @@ int sf_dssum_cls_f64(double* v, const int* perm, int n2, int n4, int n8, const i
  * those elements are fetched from HBM once.  block_start: 4 x (n_blocks + 1)
  * item offsets, one row per class (pairs, quads, octets, generic), each relative
  * to its class.  Same modes, flags, halo convention and per-gid order as
- * sf_dssum_f64 (bit-identical results). */
+ * sf_dssum_f64 (bit-identical results).  pre (optional, mode 2): masked copies
+ * receive pre[p] * u[p] -- the input of an operator applied by sf_ax_pre_f64. */
 int sf_dssum_blk_f64(double* v, const int* perm, int n2, int n4, int n8, const int* gen_offsets,
-                     const int* block_start, int n_blocks, int mode, const double* u, const double* recv,
-                     int n_local, void* stream);
+                     const int* block_start, int n_blocks, int mode, const double* u, const double* pre,
+                     const double* recv, int n_local, void* stream);
+
+/* Ax_helm of the Jacobi-scaled vector pre .* u without materialising it
+ * (`z = precond(v); w = apply_a(z)`, krylov.py:106-107 with BlockJacobi,
+ * precond.py:58-59): each u value is multiplied by pre as it is loaded, the same
+ * IEEE product `inv_diag * v` rounds to.  inmask/outsel optional (both or
+ * neither, as in sf_ax_masked_f64).  n = 8 only (SF_ERR_UNSUPPORTED otherwise). */
+int sf_ax_pre_f64(const double* d_host, int n, const double* g, const double* b, const double* u,
+                  const double* pre, double* w, long long E, double lam_visc, double lam_mass,
+                  const uint32_t* inmask, const uint32_t* outsel, int exact, void* stream);
 
 /* Fused global operator for n = 8, single rank: sf_ax_helm_f64 / sf_ax_masked_f64
  * followed by sf_dssum_cls_f64 in ONE launch (the whole make_global_op closure,

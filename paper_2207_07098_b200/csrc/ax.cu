@@ -149,12 +149,13 @@ ax_helm_kernel(DMat<N> D, const double* __restrict__ g, const double* __restrict
 
 // K1 for n = 8: the one-pencil kernel with a bank-swizzled shared layout
 // (body in ax8s.cuh, shared with the fused Ax+dssum kernel).
-template <bool EX, bool MASK>
+template <bool EX, bool MASK, bool PRE = false>
 __global__ void __launch_bounds__(128, SF_AX8S_MINB)
 ax_helm8s_kernel(DMat<8> D, const double* __restrict__ g, const double* __restrict__ b,
                  const double* __restrict__ u, double* __restrict__ w, long long E, double lv,
-                 double lm, const uint32_t* __restrict__ inmask, const uint32_t* __restrict__ outsel) {
-  ax8s_pair<EX, MASK>(D, g, b, u, w, E, lv, lm, inmask, outsel, (long long)blockIdx.x);
+                 double lm, const uint32_t* __restrict__ inmask, const uint32_t* __restrict__ outsel,
+                 const double* __restrict__ pre = nullptr) {
+  ax8s_pair<EX, MASK, PRE>(D, g, b, u, w, E, lv, lm, inmask, outsel, (long long)blockIdx.x, nullptr, pre);
 }
 
 // K1 for n = 8, two pencils per thread (experimental, -DSF_AX_PENCIL2; measured
@@ -421,12 +422,29 @@ static DMat<N> load_dmat(const double* d_host) {
 template <int N>
 static int launch_ax(const double* d_host, const double* g, const double* b, const double* u,
                      double* w, long long E, double lv, double lm, const uint32_t* inmask,
-                     const uint32_t* outsel, int exact, cudaStream_t st) {
+                     const uint32_t* outsel, int exact, cudaStream_t st, const double* pre) {
   using C = AxCfg<N>;
   if (E <= 0) return SF_OK;
   DMat<N> D = load_dmat<N>(d_host);
   dim3 grid((unsigned)((E + C::EPB - 1) / C::EPB));
   const bool masked = inmask != nullptr;
+  if (pre != nullptr) {
+    // fused Jacobi scaling: n = 8 swizzled kernel only
+    if constexpr (N == 8) {
+      dim3 g8((unsigned)((E + 1) / 2));
+      if (exact) {
+        if (masked) ax_helm8s_kernel<true, true, true><<<g8, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel, pre);
+        else ax_helm8s_kernel<true, false, true><<<g8, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, nullptr, nullptr, pre);
+      } else {
+        if (masked) ax_helm8s_kernel<false, true, true><<<g8, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel, pre);
+        else ax_helm8s_kernel<false, false, true><<<g8, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, nullptr, nullptr, pre);
+      }
+      return check_launch("ax_helm8s_pre");
+    } else {
+      set_error("ax_helm: the fused pre-scaling is implemented for n = 8 only (got n = %d)", N);
+      return SF_ERR_UNSUPPORTED;
+    }
+  }
   if constexpr (N == 8) {
 #ifdef SF_AX_PENCIL2
     dim3 g8((unsigned)((E + AX8_EPB - 1) / AX8_EPB));
@@ -484,12 +502,12 @@ static int launch_grad(const double* d_host, const double* u, double* ur, double
 
 int ax_helm(const double* d_host, int n, const double* g, const double* b, const double* u,
             double* w, long long E, double lv, double lm, const uint32_t* inmask,
-            const uint32_t* outsel, int exact, cudaStream_t st) {
+            const uint32_t* outsel, int exact, cudaStream_t st, const double* pre) {
   if ((inmask == nullptr) != (outsel == nullptr)) {
     set_error("ax_helm: inmask and outsel must both be given or both be null");
     return SF_ERR_ARG;
   }
-#define CALL(NV) launch_ax<NV>(d_host, g, b, u, w, E, lv, lm, inmask, outsel, exact, st)
+#define CALL(NV) launch_ax<NV>(d_host, g, b, u, w, E, lv, lm, inmask, outsel, exact, st, pre)
   SF_DISPATCH_N(n, CALL)
 #undef CALL
 }

@@ -29,13 +29,18 @@ constexpr int kAxUnroll = SF_AX_UNROLL;
 #endif
 
 // 128 threads: elements 2*pair and 2*pair+1 (64 threads each).
-template <bool EX, bool MASK>
+// PRE: the operator is applied to pre .* u (the Jacobi-preconditioned Krylov
+// vector, `precond(v)` then `apply_a`, krylov.py:106-107) without materialising
+// it: each u value is scaled as it is loaded (one IEEE multiply, the same bits
+// as `inv_diag * v`), including the masked rows that pass u through.
+template <bool EX, bool MASK, bool PRE = false>
 __device__ __forceinline__ void ax8s_pair(const DMat<8>& D, const double* __restrict__ g,
                                           const double* __restrict__ b, const double* __restrict__ u,
                                           double* __restrict__ w, long long E, double lv, double lm,
                                           const uint32_t* __restrict__ inmask,
                                           const uint32_t* __restrict__ outsel, long long pair,
-                                          unsigned long long* signal = nullptr) {
+                                          unsigned long long* signal = nullptr,
+                                          const double* __restrict__ pre = nullptr) {
   constexpr int N = 8, NN = 64, NNN = 512, EPB = 2, WPE = 16;
   __shared__ __align__(16) double us_[EPB][NNN];
   __shared__ __align__(16) double f1s[EPB][NNN];
@@ -80,6 +85,7 @@ __device__ __forceinline__ void ax8s_pair(const DMat<8>& D, const double* __rest
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     double uv = active ? __ldg(u + base + i * NN) : 0.0;
+    if constexpr (PRE) uv = active ? __dmul_rn(__ldg(pre + base + i * NN), uv) : 0.0;
     if constexpr (MASK) {
       if (!((inb >> i) & 1u)) uv = 0.0;
     }
@@ -154,7 +160,10 @@ __device__ __forceinline__ void ax8s_pair(const DMat<8>& D, const double* __rest
     double wv = mul<EX>(lv, acc);
     if (mass) wv = add<EX>(wv, mul<EX>(mul<EX>(lm, __ldg(b + base + i * NN)), su[i * NN + st]));
     if constexpr (MASK) {
-      if (!((outb >> i) & 1u)) wv = __ldg(u + base + i * NN);
+      if (!((outb >> i) & 1u)) {
+        wv = __ldg(u + base + i * NN);
+        if constexpr (PRE) wv = __dmul_rn(__ldg(pre + base + i * NN), wv);
+      }
     }
     w[base + i * NN] = wv;
   }

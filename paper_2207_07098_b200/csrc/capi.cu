@@ -34,7 +34,7 @@ int check_launch(const char* what) {
 
 // implemented in ax.cu, gs.cu, vec.cu, ops.cu, geom.cu
 int ax_helm(const double*, int, const double*, const double*, const double*, double*, long long,
-            double, double, const uint32_t*, const uint32_t*, int, cudaStream_t);
+            double, double, const uint32_t*, const uint32_t*, int, cudaStream_t, const double*);
 int grad_ref(const double*, int, const double*, double*, double*, double*, long long, int,
              cudaStream_t);
 int apply_axis(int, const double*, int, int, const double*, double*, long long, int, cudaStream_t);
@@ -47,7 +47,7 @@ int dssum_cls(double*, const int*, int, int, int, const int*, int, int, const do
               int, cudaStream_t);
 int rank_sum(const double*, int, int, double*, cudaStream_t);
 int dssum_blk(double*, const int*, int, int, int, const int*, const int*, int, int, const double*,
-              const double*, int, cudaStream_t);
+              const double*, const double*, int, cudaStream_t);
 int ax_dssum8(const double*, const double*, const double*, const double*, double*, long long, double,
               double, const uint32_t*, const uint32_t*, int, const int*, const long long*,
               unsigned long long*, unsigned long long, int, cudaStream_t);
@@ -109,7 +109,7 @@ int sf_ax_helm_f64(const double* d_host, int n, const double* g, const double* b
                    double* w, long long E, double lam_visc, double lam_mass, int exact,
                    void* stream) {
   return ax_helm(d_host, n, g, b, u, w, E, lam_visc, lam_mass, nullptr, nullptr, exact,
-                 as_stream(stream));
+                 as_stream(stream), nullptr);
 }
 
 int sf_gs_gather_f64(const double* vals, const long long* perm, const long long* offsets,
@@ -130,7 +130,18 @@ int sf_ax_masked_f64(const double* d_host, int n, const double* g, const double*
     return SF_ERR_ARG;
   }
   return ax_helm(d_host, n, g, b, u, w, E, lam_visc, lam_mass, inmask, outsel, exact,
-                 as_stream(stream));
+                 as_stream(stream), nullptr);
+}
+
+int sf_ax_pre_f64(const double* d_host, int n, const double* g, const double* b, const double* u,
+                  const double* pre, double* w, long long E, double lam_visc, double lam_mass,
+                  const uint32_t* inmask, const uint32_t* outsel, int exact, void* stream) {
+  if (!pre || (inmask == nullptr) != (outsel == nullptr)) {
+    set_error("sf_ax_pre_f64: pre is required; inmask/outsel both or neither");
+    return SF_ERR_ARG;
+  }
+  return ax_helm(d_host, n, g, b, u, w, E, lam_visc, lam_mass, inmask, outsel, exact,
+                 as_stream(stream), pre);
 }
 
 int sf_dssum_f64(double* v, const int* offsets, const int* perm, int n_shared, int mode,
@@ -145,9 +156,9 @@ int sf_dssum_cls_f64(double* v, const int* perm, int n2, int n4, int n8, const i
 }
 
 int sf_dssum_blk_f64(double* v, const int* perm, int n2, int n4, int n8, const int* gen_offsets,
-                     const int* block_start, int n_blocks, int mode, const double* u, const double* recv,
-                     int n_local, void* stream) {
-  return dssum_blk(v, perm, n2, n4, n8, gen_offsets, block_start, n_blocks, mode, u, recv, n_local,
+                     const int* block_start, int n_blocks, int mode, const double* u, const double* pre,
+                     const double* recv, int n_local, void* stream) {
+  return dssum_blk(v, perm, n2, n4, n8, gen_offsets, block_start, n_blocks, mode, u, pre, recv, n_local,
                    as_stream(stream));
 }
 

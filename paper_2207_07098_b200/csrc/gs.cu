@@ -79,15 +79,24 @@ __global__ void dssum_shared_kernel(double* __restrict__ v, const int* __restric
 // that follow are 16-byte aligned for their int4 loads.
 __host__ __device__ __forceinline__ long long pairs_span(int n2) { return (2LL * n2 + 3) & ~3LL; }
 
+// masked finalisation value: the operator input u, or pre .* u when the operator
+// was applied to the Jacobi-scaled vector on the fly (sf_ax_pre_f64)
+__device__ __forceinline__ double dss_input(const double* __restrict__ u, const double* __restrict__ pre,
+                                           int p) {
+  const double x = u[p];
+  return pre != nullptr ? __dmul_rn(__ldg(pre + p), x) : x;
+}
+
 template <int MODE>
 __device__ __forceinline__ void dss_finish(double* __restrict__ v, const double* __restrict__ u,
-                                           const int* idx, int c, double acc, int n_local) {
+                                           const int* idx, int c, double acc, int n_local,
+                                           const double* __restrict__ pre = nullptr) {
   if (MODE == 1) acc = __dmul_rn(acc, __drcp_rn((double)c));
   for (int o = 0; o < c; ++o) {
     int p = idx[o];
     if (MODE == 2 && p < 0) {
       p &= 0x7fffffff;
-      v[p] = u[p];
+      v[p] = dss_input(u, pre, p);
     } else if (p < n_local) {
       v[p] = acc;
     }
@@ -170,7 +179,8 @@ template <int MODE>
 __global__ void __launch_bounds__(256)
 dssum_blk_kernel(double* __restrict__ v, const int* __restrict__ perm, int n2, int n4, int n8,
                  const int* __restrict__ gen_off, const int* __restrict__ bstart, int nb,
-                 const double* __restrict__ u, const double* __restrict__ recv, int n_local) {
+                 const double* __restrict__ u, const double* __restrict__ pre,
+                 const double* __restrict__ recv, int n_local) {
   const int b = blockIdx.x;
   const int2* p2 = reinterpret_cast<const int2*>(perm);
   const int4* p4 = reinterpret_cast<const int4*>(perm + pairs_span(n2));
@@ -189,10 +199,10 @@ dssum_blk_kernel(double* __restrict__ v, const int* __restrict__ perm, int n2, i
         b1 = dss_load(v, recv, qb.y, n_local);
       }
       const int ia[2] = {qa.x, qa.y};
-      dss_finish<MODE>(v, u, ia, 2, __dadd_rn(__dadd_rn(0.0, a0), a1), n_local);
+      dss_finish<MODE>(v, u, ia, 2, __dadd_rn(__dadd_rn(0.0, a0), a1), n_local, pre);
       if (g2 < e) {
         const int ib[2] = {qb.x, qb.y};
-        dss_finish<MODE>(v, u, ib, 2, __dadd_rn(__dadd_rn(0.0, b0), b1), n_local);
+        dss_finish<MODE>(v, u, ib, 2, __dadd_rn(__dadd_rn(0.0, b0), b1), n_local, pre);
       }
     }
   }
@@ -207,7 +217,7 @@ dssum_blk_kernel(double* __restrict__ v, const int* __restrict__ perm, int n2, i
       double acc = 0.0;
 #pragma unroll
       for (int o = 0; o < 4; ++o) acc = __dadd_rn(acc, a[o]);
-      dss_finish<MODE>(v, u, idx, 4, acc, n_local);
+      dss_finish<MODE>(v, u, idx, 4, acc, n_local, pre);
     }
   }
   {
@@ -221,7 +231,7 @@ dssum_blk_kernel(double* __restrict__ v, const int* __restrict__ perm, int n2, i
       double acc = 0.0;
 #pragma unroll
       for (int o = 0; o < 8; ++o) acc = __dadd_rn(acc, a[o]);
-      dss_finish<MODE>(v, u, idx, 8, acc, n_local);
+      dss_finish<MODE>(v, u, idx, 8, acc, n_local, pre);
     }
   }
   {
@@ -235,7 +245,7 @@ dssum_blk_kernel(double* __restrict__ v, const int* __restrict__ perm, int n2, i
         int p = __ldg(pg + o);
         if (MODE == 2 && p < 0) {
           p &= 0x7fffffff;
-          v[p] = u[p];
+          v[p] = dss_input(u, pre, p);
         } else if (p < n_local) {
           v[p] = acc;
         }
@@ -315,15 +325,16 @@ int dssum_cls(double* v, const int* perm, int n2, int n4, int n8, const int* gen
 }
 
 int dssum_blk(double* v, const int* perm, int n2, int n4, int n8, const int* gen_off, const int* bstart,
-              int nb, int mode, const double* u, const double* recv, int n_local, cudaStream_t st) {
+              int nb, int mode, const double* u, const double* pre, const double* recv, int n_local,
+              cudaStream_t st) {
   if (nb <= 0) return SF_OK;
   if (recv == nullptr) n_local = 0x7fffffff;
   switch (mode) {
-    case 0: dssum_blk_kernel<0><<<nb, 256, 0, st>>>(v, perm, n2, n4, n8, gen_off, bstart, nb, nullptr, recv, n_local); break;
-    case 1: dssum_blk_kernel<1><<<nb, 256, 0, st>>>(v, perm, n2, n4, n8, gen_off, bstart, nb, nullptr, recv, n_local); break;
+    case 0: dssum_blk_kernel<0><<<nb, 256, 0, st>>>(v, perm, n2, n4, n8, gen_off, bstart, nb, nullptr, nullptr, recv, n_local); break;
+    case 1: dssum_blk_kernel<1><<<nb, 256, 0, st>>>(v, perm, n2, n4, n8, gen_off, bstart, nb, nullptr, nullptr, recv, n_local); break;
     case 2:
       if (u == nullptr) { set_error("dssum_blk: masked mode needs u"); return SF_ERR_ARG; }
-      dssum_blk_kernel<2><<<nb, 256, 0, st>>>(v, perm, n2, n4, n8, gen_off, bstart, nb, u, recv, n_local);
+      dssum_blk_kernel<2><<<nb, 256, 0, st>>>(v, perm, n2, n4, n8, gen_off, bstart, nb, u, pre, recv, n_local);
       break;
     default: set_error("dssum_blk: bad mode %d", mode); return SF_ERR_ARG;
   }

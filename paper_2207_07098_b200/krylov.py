@@ -25,6 +25,9 @@ from .errors import SolverBreakdownError
 from .operators import GlobalOp
 from .precond import BlockJacobi
 
+#: Jacobi scaling formed inside the Ax kernel (SEMFLOW_B200_PRE_FUSED=0 materialises z)
+_PRE_FUSED = os.environ.get("SEMFLOW_B200_PRE_FUSED", "1") != "0"
+
 
 @dataclass
 class SolveInfo:
@@ -103,6 +106,20 @@ class _Fused:
         else:
             torch.mul(self.invdiag, v, out=z)
         return z
+
+    def apply_precond(self, v, w, z):
+        """w <- A M^-1 v (krylov.py:106-107, z = precond(v); w = apply_a(z)).  With
+        Jacobi at n = 8 the product inv_diag * v is formed inside the Ax kernel as v
+        is loaded (same bits, z never written); without a preconditioner A acts on
+        v directly (the reference's copy is identical)."""
+        if self.invdiag is None:
+            self.op.apply_into(v, w)
+        elif self.sp.n == 8 and _PRE_FUSED:
+            self.op.apply_into(v, w, pre=self.invdiag)
+        else:
+            self.precond_into(v, z)
+            self.op.apply_into(z, w)
+        return w
 
 
 def _fusable(apply_a, precond, dot):
@@ -348,9 +365,8 @@ def _gmres_pipelined(F, op, b, tol, max_iter, restart):
     def launch(j, V):
         bl = blk[j]
         bp = lambda i: bl.data_ptr() + 8 * i
-        F.precond_into(V[j], z)
         w = torch.empty_like(b)
-        F.op.apply_into(z, w)
+        F.apply_precond(V[j], w, z)
         F.mgs(bl[0:2], _lib.ptr(w), None, None, _lib.ptr(V[0]), None, None, mult, 1)
         for i in range(1, j + 1):
             F.mgs(bl[2 * i:2 * i + 2], _lib.ptr(w), _lib.ptr(V[i - 1]), bp(2 * (i - 1)), _lib.ptr(V[i]),
@@ -457,9 +473,8 @@ def _gmres_fused(op, b, tol, max_iter, restart, precond, dot, x0):
         g[0] = beta
         j_end = 0
         for j in range(m):
-            F.precond_into(vs[j], z)
             w = torch.empty_like(b)
-            op.apply_into(z, w)
+            F.apply_precond(vs[j], w, z)
             # MGS sweep: pass 0 = (<w,v0>, <w,w>), pass i = (w -= h_{i-1} v_{i-1}; <w,v_i>),
             # last = (w -= h_j v_j; <w,w>)
             F.mgs(hs[0:2], _lib.ptr(w), None, None, _lib.ptr(vs[0]), None, None, mult, 1)

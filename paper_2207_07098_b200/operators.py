@@ -88,12 +88,27 @@ class GlobalOp:
             self._plan = self.space.gs.fused_plan(self.sh_perm if self.masked else None)
         return self._plan
 
-    def apply_into(self, u, w):
-        """w <- A u (w must not alias u)."""
+    def apply_into(self, u, w, pre=None):
+        """w <- A u (w must not alias u).  With ``pre`` (n = 8): w <- A (pre * u),
+        the product formed as u is loaded -- the Jacobi-preconditioned Krylov
+        vector is never written (krylov.py:106-107)."""
         sp = self.space
         gs = sp.gs
         st = _lib.stream_ptr(sp.device)
         E = sp.n_elements
+        if pre is not None:
+            if sp.n != 8:
+                return self.apply_into(pre * u, w)
+            _lib.call("sf_ax_pre_f64", sp.dmat.ctypes.data, sp.n, _lib.ptr(sp.geom), _lib.ptr(sp.bm),
+                      _lib.ptr(u), _lib.ptr(pre), _lib.ptr(w), E, self.lam_visc, self.lam_mass,
+                      _lib.ptr(self.inmask) if self.masked else None,
+                      _lib.ptr(self.outsel) if self.masked else None, _ex(), st)
+            if self.masked:
+                gs.dssum_into(w, 2, u=u, perm=self.sh_perm, pre=pre)
+            else:
+                gs.dssum_into(w, 0)
+            self.launches += 2
+            return w
         if self.fused:
             pl = self.fused_plan()
             _lib.call("sf_ax_dssum8_f64", sp.dmat.ctypes.data, _lib.ptr(sp.geom), _lib.ptr(sp.bm),

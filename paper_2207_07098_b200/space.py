@@ -349,21 +349,22 @@ class GatherScatter:
         meta = np.array([len(sched), cp, K] + offs, dtype=np.int64)
         return FusedPlan(plan, meta, torch.zeros(K + 1, dtype=torch.int64, device=dev), len(sched))
 
-    def dssum_into(self, v, mode, u=None, perm=None):
+    def dssum_into(self, v, mode, u=None, perm=None, pre=None):
         """In-place dssum of one scalar row v (mode 0 add / 1 avg / 2 masked with u).
-        ``perm``: a flagged copy of ``cls_perm`` (masked operators)."""
+        ``perm``: a flagged copy of ``cls_perm`` (masked operators); ``pre``: the
+        masked copies receive pre * u (operator applied with sf_ax_pre_f64)."""
         recv = self.halo_exchange(v)
         if not hasattr(self, "cls_perm"):
             self._build_classes()
         n2, n4, n8 = self.cls_n
         pm = self.cls_perm if perm is None else perm
-        if _DSSUM_KERNEL == "cls":
+        if _DSSUM_KERNEL == "cls" and pre is None:
             _lib.call("sf_dssum_cls_f64", _lib.ptr(v), _lib.ptr(pm), n2, n4, n8, _lib.ptr(self.cls_gen_off),
                       self.cls_n_gen, mode, _lib.ptr(u), _lib.ptr(recv), self.P, _lib.stream_ptr(self.device))
         else:
             _lib.call("sf_dssum_blk_f64", _lib.ptr(v), _lib.ptr(pm), n2, n4, n8, _lib.ptr(self.cls_gen_off),
-                      _lib.ptr(self.cls_bstart), self.cls_nb, mode, _lib.ptr(u), _lib.ptr(recv), self.P,
-                      _lib.stream_ptr(self.device))
+                      _lib.ptr(self.cls_bstart), self.cls_nb, mode, _lib.ptr(u), _lib.ptr(pre), _lib.ptr(recv),
+                      self.P, _lib.stream_ptr(self.device))
 
     def _dssum_rows(self, flat, mode, u=None):
         for row in range(flat.shape[0]):

@@ -72,7 +72,7 @@ def run(ne):
                         gs._build_classes()
                     n2, n4, n8 = gs.cls_n
                     L.sf_dssum_blk_f64(w.data_ptr(), op.sh_perm.data_ptr(), n2, n4, n8, gs.cls_gen_off.data_ptr(),
-                                       gs.cls_bstart.data_ptr(), gs.cls_nb, 2, u.data_ptr(), None, 0, st)
+                                       gs.cls_bstart.data_ptr(), gs.cls_nb, 2, u.data_ptr(), None, None, 0, st)
                 else:
                     if hasattr(L, "sf_dssum_cls_f64"):
                         n2, n4, n8 = gs.cls_n
