@@ -158,6 +158,13 @@ ax_helm8s_kernel(DMat<8> D, const double* __restrict__ g, const double* __restri
   ax8s_pair<EX, MASK, PRE>(D, g, b, u, w, E, lv, lm, inmask, outsel, (long long)blockIdx.x, nullptr, pre);
 }
 
+template <bool EX, bool MASK, bool PRE>
+static void launch8s(dim3 grid, cudaStream_t st, const DMat<8>& D, const double* g, const double* b,
+                     const double* u, double* w, long long E, double lv, double lm, const uint32_t* inmask,
+                     const uint32_t* outsel, const double* pre) {
+  ax_helm8s_kernel<EX, MASK, PRE><<<grid, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel, pre);
+}
+
 // K1 for n = 8, two pencils per thread (experimental, -DSF_AX_PENCIL2; measured
 // 305 us vs 246 us for the one-pencil kernel at 32^3, kept for further tuning).  One warp owns one element; lane (j, kk)
 // owns the r-pencils (j, 2kk) and (j, 2kk+1).  Global accesses are 16-byte
@@ -433,11 +440,11 @@ static int launch_ax(const double* d_host, const double* g, const double* b, con
     if constexpr (N == 8) {
       dim3 g8((unsigned)((E + 1) / 2));
       if (exact) {
-        if (masked) ax_helm8s_kernel<true, true, true><<<g8, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel, pre);
-        else ax_helm8s_kernel<true, false, true><<<g8, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, nullptr, nullptr, pre);
+        if (masked) launch8s<true, true, true>(g8, st, D, g, b, u, w, E, lv, lm, inmask, outsel, pre);
+        else launch8s<true, false, true>(g8, st, D, g, b, u, w, E, lv, lm, nullptr, nullptr, pre);
       } else {
-        if (masked) ax_helm8s_kernel<false, true, true><<<g8, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel, pre);
-        else ax_helm8s_kernel<false, false, true><<<g8, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, nullptr, nullptr, pre);
+        if (masked) launch8s<false, true, true>(g8, st, D, g, b, u, w, E, lv, lm, inmask, outsel, pre);
+        else launch8s<false, false, true>(g8, st, D, g, b, u, w, E, lv, lm, nullptr, nullptr, pre);
       }
       return check_launch("ax_helm8s_pre");
     } else {
@@ -459,11 +466,11 @@ static int launch_ax(const double* d_host, const double* g, const double* b, con
 #elif !defined(SF_AX8_UNSWIZZLED)
     dim3 g8((unsigned)((E + 1) / 2));
     if (exact) {
-      if (masked) ax_helm8s_kernel<true, true><<<g8, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel);
-      else ax_helm8s_kernel<true, false><<<g8, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, nullptr, nullptr);
+      if (masked) launch8s<true, true, false>(g8, st, D, g, b, u, w, E, lv, lm, inmask, outsel, nullptr);
+      else launch8s<true, false, false>(g8, st, D, g, b, u, w, E, lv, lm, nullptr, nullptr, nullptr);
     } else {
-      if (masked) ax_helm8s_kernel<false, true><<<g8, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel);
-      else ax_helm8s_kernel<false, false><<<g8, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, nullptr, nullptr);
+      if (masked) launch8s<false, true, false>(g8, st, D, g, b, u, w, E, lv, lm, inmask, outsel, nullptr);
+      else launch8s<false, false, false>(g8, st, D, g, b, u, w, E, lv, lm, nullptr, nullptr, nullptr);
     }
     return check_launch("ax_helm8s");
 #endif

@@ -99,6 +99,9 @@ __device__ __forceinline__ void ax8s_pair(const DMat<8>& D, const double* __rest
     dk[q] = D.v[k * N + q];
   }
   const double* gp = g + (active ? base : 0);
+  // (a per-thread cp.async ring holding 3 layers of G in shared memory was
+  // measured slower: 238 vs 220 us at 32^3 -- the extra LDGSTS/LDS traffic costs
+  // more than the deeper prefetch gains)
   double gn[6];
 #pragma unroll
   for (int m = 0; m < 6; ++m) gn[m] = active ? __ldg(gp + m * gstride) : 0.0;

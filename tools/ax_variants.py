@@ -57,6 +57,7 @@ def run(ne):
         L = ctypes.CDLL(path)
         for name, args in _lib._SIGS.items():
             getattr(L, name).argtypes = args
+        L.sf_last_error.restype = ctypes.c_char_p
         res = {}
         for kind in ("masked", "plain", "dssum", "dssum_blk"):
             def fn():
@@ -83,6 +84,10 @@ def run(ne):
                                        gs.n_shared, 2, u.data_ptr(), None, 0, st)
             for _ in range(3):
                 fn()
+            torch.cuda.synchronize()
+            err = L.sf_last_error()
+            if err:
+                print("   ", kind, "error:", err)
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
             torch.cuda.synchronize()
             for a, b in ev:
