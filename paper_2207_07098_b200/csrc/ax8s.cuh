@@ -123,6 +123,8 @@ __device__ __forceinline__ void ax8s_pair(const DMat<8>& D, const double* __rest
       for (int m = 0; m < 6; ++m) gn[m] = active ? __ldg(gp + (i + 1) * NN + m * gstride) : 0.0;
     }
     double ar = 0.0, as = 0.0, at = 0.0;
+    // (splitting these three chains further into even/odd halves measured
+    // slower: 230 vs 216 us at 32^3)
 #pragma unroll
     for (int q = 0; q < N; ++q) {
       ar = mac<EX>(ar, D.v[i * N + q], um[q]);
@@ -150,15 +152,35 @@ __device__ __forceinline__ void ax8s_pair(const DMat<8>& D, const double* __rest
 #pragma unroll (kAxUnroll)
   for (int i = 0; i < N; ++i) {
     double acc = 0.0;
+    if constexpr (EX) {
+      // the reference's single interleaved accumulator (_numba.py:119-126)
 #pragma unroll
-    for (int q = 0; q < N; q += 2) {
-      const double2 t3 = *reinterpret_cast<const double2*>(s3 + i * NN + j * N + (q ^ sj));
-      acc = mac<EX>(acc, D.v[q * N + i], s1[q * NN + st]);
-      acc = mac<EX>(acc, dj[q], s2[i * NN + q * N + (k ^ SW(q))]);
-      acc = mac<EX>(acc, dk[q], t3.x);
-      acc = mac<EX>(acc, D.v[(q + 1) * N + i], s1[(q + 1) * NN + st]);
-      acc = mac<EX>(acc, dj[q + 1], s2[i * NN + (q + 1) * N + (k ^ SW(q + 1))]);
-      acc = mac<EX>(acc, dk[q + 1], t3.y);
+      for (int q = 0; q < N; q += 2) {
+        const double2 t3 = *reinterpret_cast<const double2*>(s3 + i * NN + j * N + (q ^ sj));
+        acc = mac<EX>(acc, D.v[q * N + i], s1[q * NN + st]);
+        acc = mac<EX>(acc, dj[q], s2[i * NN + q * N + (k ^ SW(q))]);
+        acc = mac<EX>(acc, dk[q], t3.x);
+        acc = mac<EX>(acc, D.v[(q + 1) * N + i], s1[(q + 1) * NN + st]);
+        acc = mac<EX>(acc, dj[q + 1], s2[i * NN + (q + 1) * N + (k ^ SW(q + 1))]);
+        acc = mac<EX>(acc, dk[q + 1], t3.y);
+      }
+    } else {
+      // production: three independent DFMA chains (r, s, t) instead of one
+      // 24-long chain -- ncu showed 'wait' (fixed-latency dependency) as the
+      // second stall reason; the sum differs from the reference's order only
+      // by rounding (<= 1e-15 relative)
+      double ar = 0.0, as = 0.0, at = 0.0;
+#pragma unroll
+      for (int q = 0; q < N; q += 2) {
+        const double2 t3 = *reinterpret_cast<const double2*>(s3 + i * NN + j * N + (q ^ sj));
+        ar = fma(D.v[q * N + i], s1[q * NN + st], ar);
+        as = fma(dj[q], s2[i * NN + q * N + (k ^ SW(q))], as);
+        at = fma(dk[q], t3.x, at);
+        ar = fma(D.v[(q + 1) * N + i], s1[(q + 1) * NN + st], ar);
+        as = fma(dj[q + 1], s2[i * NN + (q + 1) * N + (k ^ SW(q + 1))], as);
+        at = fma(dk[q + 1], t3.y, at);
+      }
+      acc = (ar + as) + at;
     }
     double wv = mul<EX>(lv, acc);
     if (mass) wv = add<EX>(wv, mul<EX>(mul<EX>(lm, __ldg(b + base + i * NN)), su[i * NN + st]));
