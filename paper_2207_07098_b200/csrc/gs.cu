@@ -175,6 +175,11 @@ dssum_cls_kernel(double* __restrict__ v, const int* __restrict__ perm, int n2, i
 // (edges and vertices run long after the faces of the same element).  Keeping an
 // element range's classes together in one block lets those sectors hit in L2.
 // bstart: 4 x (nb + 1) item offsets (per class, relative to the class start).
+#ifndef SF_DSS_PB
+#define SF_DSS_PB 2
+#endif
+constexpr int DSS_PB = SF_DSS_PB;
+
 template <int MODE>
 __global__ void __launch_bounds__(256)
 dssum_blk_kernel(double* __restrict__ v, const int* __restrict__ perm, int n2, int n4, int n8,
@@ -188,21 +193,29 @@ dssum_blk_kernel(double* __restrict__ v, const int* __restrict__ perm, int n2, i
   const int* pg = perm + pairs_span(n2) + 4LL * n4 + 8LL * n8;
   {
     const int s = __ldg(bstart + b), e = __ldg(bstart + b + 1);
-    for (int g = s + threadIdx.x; g < e; g += 2 * blockDim.x) {
-      const int g2 = g + blockDim.x;
-      const int2 qa = __ldg(p2 + g);
-      const int2 qb = g2 < e ? __ldg(p2 + g2) : make_int2(0, 0);
-      const double a0 = dss_load(v, recv, qa.x, n_local), a1 = dss_load(v, recv, qa.y, n_local);
-      double b0 = 0.0, b1 = 0.0;
-      if (g2 < e) {
-        b0 = dss_load(v, recv, qb.x, n_local);
-        b1 = dss_load(v, recv, qb.y, n_local);
+    // DSS_PB pairs per thread in flight: all index loads, then all value loads,
+    // then the sums and stores (the kernel is latency-bound: ncu long-scoreboard)
+    for (int g = s + threadIdx.x; g < e; g += DSS_PB * blockDim.x) {
+      int2 q[DSS_PB];
+      double a0[DSS_PB], a1[DSS_PB];
+#pragma unroll
+      for (int k = 0; k < DSS_PB; ++k) {
+        const int gk = g + k * blockDim.x;
+        q[k] = gk < e ? __ldg(p2 + gk) : make_int2(0, 0);
       }
-      const int ia[2] = {qa.x, qa.y};
-      dss_finish<MODE>(v, u, ia, 2, __dadd_rn(__dadd_rn(0.0, a0), a1), n_local, pre);
-      if (g2 < e) {
-        const int ib[2] = {qb.x, qb.y};
-        dss_finish<MODE>(v, u, ib, 2, __dadd_rn(__dadd_rn(0.0, b0), b1), n_local, pre);
+#pragma unroll
+      for (int k = 0; k < DSS_PB; ++k) {
+        if (g + k * blockDim.x < e) {
+          a0[k] = dss_load(v, recv, q[k].x, n_local);
+          a1[k] = dss_load(v, recv, q[k].y, n_local);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < DSS_PB; ++k) {
+        if (g + k * blockDim.x < e) {
+          const int ik[2] = {q[k].x, q[k].y};
+          dss_finish<MODE>(v, u, ik, 2, __dadd_rn(__dadd_rn(0.0, a0[k]), a1[k]), n_local, pre);
+        }
       }
     }
   }
