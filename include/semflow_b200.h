@@ -53,6 +53,11 @@ int sf_red_workspace_doubles(void);
  * Replaces kernels/_numba.py:15-60 (apply_r :15, apply_s :31, apply_t :47). */
 int sf_apply_axis_f64(int axis, const double* a, int m, int n, const double* u, double* out,
                       long long E, int exact, void* stream);
+/* The same contraction on non-cubic elements u (E, d0, d1, d2): axis `axis`
+ * (extent d_axis) is replaced by m -- the reference kernels accept any element
+ * shape, which the dealiasing chain needs (operators.py:141-147). */
+int sf_apply_axis3_f64(int axis, const double* a, int m, int d0, int d1, int d2, const double* u,
+                       double* out, long long E, int exact, void* stream);
 
 /* grad_ref: (ur, us, ut) = reference derivatives of u.  d_host is the n x n GLL
  * differentiation matrix in host memory.  Replaces kernels/_numba.py:63-83. */

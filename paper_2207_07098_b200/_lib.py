@@ -26,6 +26,7 @@ _SIGS = {
     "sf_last_error": [],
     "sf_red_workspace_doubles": [],
     "sf_apply_axis_f64": [_i, _vp, _i, _i, _vp, _vp, _ll, _i, _vp],
+    "sf_apply_axis3_f64": [_i, _vp, _i, _i, _i, _i, _vp, _vp, _ll, _i, _vp],
     "sf_grad_ref_f64": [_vp, _i, _vp, _vp, _vp, _vp, _ll, _i, _vp],
     "sf_ax_helm_f64": [_vp, _i, _vp, _vp, _vp, _vp, _ll, _d, _d, _i, _vp],
     "sf_gs_gather_f64": [_vp, _vp, _vp, _ll, _vp, _vp],

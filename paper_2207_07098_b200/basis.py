@@ -87,3 +87,33 @@ def make_basis(order):
     for a in (pts, wts, d):
         a.setflags(write=False)
     return Basis1D(order=n, points=pts, weights=wts, dmat=d)
+
+
+def interp_matrix(basis, targets):
+    """J[k, j] = l_j(targets[k]), barycentric form; rows of targets that hit a
+    node (|diff| < 1e-14) are exact unit vectors (basis.py:142-174)."""
+    t = np.atleast_1d(np.asarray(targets, dtype=np.float64))
+    if t.ndim != 1:
+        raise ValueError("target points must be one-dimensional")
+    outside = (t < -1.0 - 1e-12) | (t > 1.0 + 1e-12)
+    if np.any(outside):
+        raise ValueError(f"interpolation target {t[outside][0]} lies outside [-1, 1]")
+    pts = basis.points
+    lam = _bary(pts)
+    dist = t[:, None] - pts[None, :]
+    hit_r, hit_c = np.nonzero(np.abs(dist) < 1e-14)
+    J = np.zeros((t.size, pts.size))
+    free = np.ones(t.size, dtype=bool)
+    free[hit_r] = False
+    if np.any(free):
+        q = lam[None, :] / dist[free]
+        J[free] = q / np.sum(q, axis=1, keepdims=True)
+    J[hit_r, hit_c] = 1.0
+    return J
+
+
+def gauss_legendre(m):
+    """m-point Gauss-Legendre rule on [-1, 1] (basis.py:177-181, numpy's leggauss)."""
+    if m < 1:
+        raise ValueError(f"Gauss-Legendre rule needs at least 1 point, got {m}")
+    return np.polynomial.legendre.leggauss(m)

@@ -385,31 +385,32 @@ grad_ref_kernel(DMat<N> D, const double* __restrict__ u, double* __restrict__ ur
 // apply_{r,s,t}: out = A (m x n) contracted along one axis, rectangular allowed.
 // One block per element; the element and A sit in shared memory; each output
 // point is one sequential dot over the contracted index (`_numba.py:15-60`).
+// Elements may be non-cubic (d0, d1, d2): the dealiasing chain contracts one
+// axis at a time from n to m points (operators.py:141-147).
 template <int AXIS, bool EX>
-__global__ void apply_axis_kernel(const double* __restrict__ a, int m, int n,
+__global__ void apply_axis_kernel(const double* __restrict__ a, int m, int d0, int d1, int d2,
                                   const double* __restrict__ u, double* __restrict__ out,
                                   long long E) {
   extern __shared__ double sm[];
+  const int n = AXIS == 0 ? d0 : (AXIS == 1 ? d1 : d2);
+  const int o0 = AXIS == 0 ? m : d0, o1 = AXIS == 1 ? m : d1, o2 = AXIS == 2 ? m : d2;
   double* as = sm;          // m*n
-  double* ue = sm + m * n;  // n^3
+  double* ue = sm + m * n;  // d0*d1*d2
   const long long e = blockIdx.x;
-  const int nnn = n * n * n;
+  const int nin = d0 * d1 * d2;
   for (int x = threadIdx.x; x < m * n; x += blockDim.x) as[x] = a[x];
-  for (int x = threadIdx.x; x < nnn; x += blockDim.x) ue[x] = u[e * nnn + x];
+  for (int x = threadIdx.x; x < nin; x += blockDim.x) ue[x] = u[e * nin + x];
   __syncthreads();
-  const int nout = m * n * n;
+  const int nout = o0 * o1 * o2;
   for (int x = threadIdx.x; x < nout; x += blockDim.x) {
-    int i0, i1, i2;  // output index (d0, d1, d2) with the contracted axis of extent m
-    if (AXIS == 0) { i0 = x / (n * n); i1 = (x / n) % n; i2 = x % n; }
-    else if (AXIS == 1) { i0 = x / (m * n); i1 = (x / n) % m; i2 = x % n; }
-    else { i0 = x / (n * m); i1 = (x / m) % n; i2 = x % m; }
+    const int i0 = x / (o1 * o2), i1 = (x / o2) % o1, i2 = x % o2;
     double acc = 0.0;
     for (int q = 0; q < n; ++q) {
       double uv;
       int p;
-      if (AXIS == 0) { p = i0; uv = ue[(q * n + i1) * n + i2]; }
-      else if (AXIS == 1) { p = i1; uv = ue[(i0 * n + q) * n + i2]; }
-      else { p = i2; uv = ue[(i0 * n + i1) * n + q]; }
+      if (AXIS == 0) { p = i0; uv = ue[(q * d1 + i1) * d2 + i2]; }
+      else if (AXIS == 1) { p = i1; uv = ue[(i0 * d1 + q) * d2 + i2]; }
+      else { p = i2; uv = ue[(i0 * d1 + i1) * d2 + q]; }
       acc = mac<EX>(acc, as[p * n + q], uv);
     }
     out[e * nout + x] = acc;
@@ -526,14 +527,15 @@ int grad_ref(const double* d_host, int n, const double* u, double* ur, double* u
 #undef CALL
 }
 
-int apply_axis(int axis, const double* a, int m, int n, const double* u, double* out, long long E,
-               int exact, cudaStream_t st) {
+int apply_axis3(int axis, const double* a, int m, int d0, int d1, int d2, const double* u, double* out,
+                long long E, int exact, cudaStream_t st) {
   if (E <= 0) return SF_OK;
-  if (axis < 0 || axis > 2 || m <= 0 || n <= 0) {
-    set_error("apply_axis: bad axis/shape (%d, %d, %d)", axis, m, n);
+  const int n = axis == 0 ? d0 : (axis == 1 ? d1 : d2);
+  if (axis < 0 || axis > 2 || m <= 0 || d0 <= 0 || d1 <= 0 || d2 <= 0) {
+    set_error("apply_axis: bad axis/shape (%d; %d x [%d %d %d])", axis, m, d0, d1, d2);
     return SF_ERR_ARG;
   }
-  size_t smem = sizeof(double) * ((size_t)m * n + (size_t)n * n * n);
+  size_t smem = sizeof(double) * ((size_t)m * n + (size_t)d0 * d1 * d2);
   if (smem > 200 * 1024) {
     set_error("apply_axis: element too large for shared memory");
     return SF_ERR_UNSUPPORTED;
@@ -548,16 +550,24 @@ int apply_axis(int axis, const double* a, int m, int n, const double* u, double*
   }
   dim3 grid((unsigned)E);
   int threads = 128;
+#define SF_AXIS_LAUNCH(AX, EXV) \
+  apply_axis_kernel<AX, EXV><<<grid, threads, smem, st>>>(a, m, d0, d1, d2, u, out, E)
   if (exact) {
-    if (axis == 0) apply_axis_kernel<0, true><<<grid, threads, smem, st>>>(a, m, n, u, out, E);
-    else if (axis == 1) apply_axis_kernel<1, true><<<grid, threads, smem, st>>>(a, m, n, u, out, E);
-    else apply_axis_kernel<2, true><<<grid, threads, smem, st>>>(a, m, n, u, out, E);
+    if (axis == 0) SF_AXIS_LAUNCH(0, true);
+    else if (axis == 1) SF_AXIS_LAUNCH(1, true);
+    else SF_AXIS_LAUNCH(2, true);
   } else {
-    if (axis == 0) apply_axis_kernel<0, false><<<grid, threads, smem, st>>>(a, m, n, u, out, E);
-    else if (axis == 1) apply_axis_kernel<1, false><<<grid, threads, smem, st>>>(a, m, n, u, out, E);
-    else apply_axis_kernel<2, false><<<grid, threads, smem, st>>>(a, m, n, u, out, E);
+    if (axis == 0) SF_AXIS_LAUNCH(0, false);
+    else if (axis == 1) SF_AXIS_LAUNCH(1, false);
+    else SF_AXIS_LAUNCH(2, false);
   }
+#undef SF_AXIS_LAUNCH
   return check_launch("apply_axis");
+}
+
+int apply_axis(int axis, const double* a, int m, int n, const double* u, double* out, long long E,
+               int exact, cudaStream_t st) {
+  return apply_axis3(axis, a, m, n, n, n, u, out, E, exact, st);
 }
 
 }  // namespace sf

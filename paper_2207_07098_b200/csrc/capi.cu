@@ -38,6 +38,8 @@ int ax_helm(const double*, int, const double*, const double*, const double*, dou
 int grad_ref(const double*, int, const double*, double*, double*, double*, long long, int,
              cudaStream_t);
 int apply_axis(int, const double*, int, int, const double*, double*, long long, int, cudaStream_t);
+int apply_axis3(int, const double*, int, int, int, int, const double*, double*, long long, int,
+                cudaStream_t);
 int gs_gather(const double*, const long long*, const long long*, long long, double*, cudaStream_t);
 int gs_scatter(const double*, const long long*, const long long*, long long, double*, cudaStream_t);
 int dssum_shared(double*, const int*, const int*, int, int, const double*, const double*, int,
@@ -98,6 +100,11 @@ int sf_red_workspace_doubles(void) { return K_MAX * RED_BLOCKS; }
 int sf_apply_axis_f64(int axis, const double* a, int m, int n, const double* u, double* out,
                       long long E, int exact, void* stream) {
   return apply_axis(axis, a, m, n, u, out, E, exact, as_stream(stream));
+}
+
+int sf_apply_axis3_f64(int axis, const double* a, int m, int d0, int d1, int d2, const double* u,
+                       double* out, long long E, int exact, void* stream) {
+  return apply_axis3(axis, a, m, d0, d1, d2, u, out, E, exact, as_stream(stream));
 }
 
 int sf_grad_ref_f64(const double* d_host, int n, const double* u, double* ur, double* us,

@@ -38,16 +38,14 @@ def _apply(axis, a, u):
     a = np.asarray(a, dtype=np.float64)
     u = np.asarray(u, dtype=np.float64)
     e, n1, n2, n3 = u.shape
-    if not (n1 == n2 == n3):
-        raise ValueError("b200 lane expects cubic elements (E, n, n, n)")
     m, n = a.shape
-    if n != n1:
+    if n != (n1, n2, n3)[axis]:
         raise ValueError(f"contraction size mismatch: a is {a.shape}, u is {u.shape}")
     shape = [e, n1, n2, n3]
     shape[1 + axis] = m
     ad, ud = _to_dev(a), _to_dev(u)
     out = torch.empty(shape, dtype=torch.float64, device=ud.device)
-    _lib.call("sf_apply_axis_f64", axis, _lib.ptr(ad), m, n, _lib.ptr(ud), _lib.ptr(out), e, 1,
+    _lib.call("sf_apply_axis3_f64", axis, _lib.ptr(ad), m, n1, n2, n3, _lib.ptr(ud), _lib.ptr(out), e, 1,
               _lib.stream_ptr())
     return out.cpu().numpy()
 

@@ -166,15 +166,76 @@ def curl(space, v):
 
 
 def advect_vec(space, c, v, dealias=None, sign=1.0):
-    """(c . grad) v_l for l = 0, 1, 2 (operators.py:108-126, collocation)."""
+    """(c . grad) v_l for l = 0, 1, 2 (operators.py:108-126): collocation, or
+    over-integrated on the Gauss-Legendre grid with a :class:`Dealias`."""
     if dealias is not None:
-        raise NotImplementedError("over-integration (Dealias) is not on the device path yet")
+        out = dealias.advect_vec(c, v)
+        return out if sign == 1.0 else out * sign
     return _deriv(space, OP_ADVECT, v, c=c, sign=sign)
 
 
 def advect(space, c, u, dealias=None):
+    """(c . grad) u for a scalar u (operators.py:108-116)."""
+    if dealias is not None:
+        return dealias.advect(c, u)
     g = grad(space, u)
     return c[0] * g[0] + c[1] * g[1] + c[2] * g[2]
+
+
+class Dealias:
+    """Over-integration of the convective term on ceil(3 n / 2) Gauss-Legendre
+    points per direction (operators.py:129-158): c and grad u are interpolated
+    to the fine grid, multiplied there, weighted by the fine quadrature and
+    Jacobian and L2-projected back, then divided by the GLL mass."""
+
+    def __init__(self, space):
+        from .basis import gauss_legendre, interp_matrix
+
+        self.space = space
+        n = space.n
+        self.m = int(np.ceil(1.5 * n))
+        pts, wts = gauss_legendre(self.m)
+        self.interp = np.ascontiguousarray(interp_matrix(space.basis, pts))
+        self.interp_t = np.ascontiguousarray(self.interp.T)
+        dev = space.device
+        self._J = torch.from_numpy(self.interp).to(dev)
+        self._Jt = torch.from_numpy(self.interp_t).to(dev)
+        w3 = wts[:, None, None] * wts[None, :, None] * wts[None, None, :]
+        self.wjac_f = torch.from_numpy(np.ascontiguousarray(w3)).to(dev)[None] * self._to_fine(space.jac)
+
+    def _chain(self, mat, u):
+        """apply_t(A, apply_s(A, apply_r(A, u))) (operators.py:141-147)."""
+        m = mat.shape[0]
+        out = u.contiguous()
+        for axis in (0, 1, 2):
+            shape = list(out.shape)
+            shape[1 + axis] = m
+            nxt = torch.empty(shape, dtype=torch.float64, device=out.device)
+            _lib.call("sf_apply_axis3_f64", axis, _lib.ptr(mat), m, out.shape[1], out.shape[2], out.shape[3],
+                      _lib.ptr(out), _lib.ptr(nxt), out.shape[0], _ex(), _lib.stream_ptr(out.device))
+            out = nxt
+        return out
+
+    def _to_fine(self, u):
+        return self._chain(self._J, u)
+
+    def _project_back(self, f):
+        return self._chain(self._Jt, f)
+
+    def _advect_fine(self, cf, u):
+        g = grad(self.space, u)
+        fine = cf[0] * self._to_fine(g[0])
+        fine += cf[1] * self._to_fine(g[1])
+        fine += cf[2] * self._to_fine(g[2])
+        weak = self._project_back(self.wjac_f * fine)
+        return weak / self.space.bm
+
+    def advect(self, c, u):
+        return self._advect_fine([self._to_fine(c[l]) for l in range(3)], u)
+
+    def advect_vec(self, c, v):
+        cf = [self._to_fine(c[l]) for l in range(3)]     # the advecting field, once
+        return torch.stack([self._advect_fine(cf, v[l]) for l in range(3)])
 
 
 def weak_grad_dot(space, w):
