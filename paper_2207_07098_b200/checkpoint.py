@@ -21,7 +21,7 @@ import torch
 
 from . import dist as _dist
 from . import operators
-from .errors import CheckpointError
+from .errors import CheckpointError, ConfigError
 from .timestep import FlowState
 
 MAGIC = b"SEMFCKPT"
@@ -117,7 +117,8 @@ def save_state(path, stepper, state, case="semflow_b200"):
         proj_meta[name] = {"count": proj.count, "solves": proj._solves}
     meta = {"case": case, "time": state.time, "nsteps": state.nsteps, "primed": state.primed,
             "n_vel_hist": len(state.vel_hist), "n_nl_hist": len(state.nl_hist),
-            "last_order": stepper._last_order, "projections": proj_meta, "forcing": None}
+            "last_order": stepper._last_order, "projections": proj_meta,
+            "forcing": stepper.forcing.get_state() if stepper.forcing is not None else None}
     if sp.comm.rank == 0:
         write_checkpoint(path, arrays, meta)
 
@@ -136,8 +137,9 @@ def load_state(path, stepper):
     except (KeyError, ValueError) as exc:
         raise CheckpointError(f"checkpoint does not match this space: {exc}", section="arrays") from exc
     if meta.get("forcing") is not None:
-        raise CheckpointError("checkpoint carries tripping-forcing state; stochastic forcing is not on "
-                              "the device path", section="meta")
+        if stepper.forcing is None:
+            raise ConfigError("checkpoint carries tripping state but the case has none")   # runner.py:158-159
+        stepper.forcing.set_state(meta["forcing"])
     state = FlowState(time=float(meta["time"]), nsteps=int(meta["nsteps"]), vel_hist=vel_hist,
                       curl_hist=[operators.curl(sp, v) for v in vel_hist], nl_hist=nl_hist, prs=prs,
                       primed=bool(meta["primed"]))

@@ -487,7 +487,60 @@ def gen_dealias():
         json.dump(rows, fh, indent=1)
 
 
+TRIP = dict(x0=0.7, length_x=0.2, length_y=0.1, z_min=0.0, z_max=np.pi / 8, amp_steady=0.02,
+            amp_unsteady=0.05, t_scale=2e-3, n_modes=6, seed=5)
+
+
+def gen_trip():
+    """Tripping force (forcing.py:24-133) values over several segments, its state,
+    and 3 channel-box steps with it (test_runner.py:117-134 set-up)."""
+    from semflow.forcing import TrippingForcing
+
+    trip = TrippingForcing(**TRIP)
+    rng = np.random.default_rng(8)
+    x = rng.uniform(0.4, 1.0, 64)
+    y = rng.uniform(0.0, 0.3, 64)
+    z = np.concatenate([rng.uniform(-0.05, np.pi / 8 + 0.05, 60), [0.0, np.pi / 8, -1e-12, 0.2]])
+    out = {"x": x, "y": y, "z": z}
+    times = [-4e-3, 0.0, 1e-3, 2.5e-3, 9e-3, 9.5e-3, 2.1e-2]
+    for k, t in enumerate(times):
+        out[f"f{k}"] = trip.evaluate(x, y, z, t)
+    out["times"] = np.array(times)
+    np.savez_compressed(os.path.join(OUT, "trip.npz"), **out)
+    with open(os.path.join(OUT, "trip_state.json"), "w") as fh:
+        json.dump(trip.get_state(), fh)
+    # channel box with the trip and Poiseuille inflow
+    Lx, Ly, Lz = 4 * np.pi / 8, 2.0, 4 * np.pi / 3 / 8
+    sp = build_space(gen_box_mesh((0.0, Lx, 0.0, Ly, 0.0, Lz), (6, 4, 3)), make_basis(5))
+
+    def pois(x, y, z, t):
+        o = np.zeros((3,) + np.shape(x))
+        o[0] = 1.5 * y * (2.0 - y)
+        return o
+
+    specs = {"xlo": {"kind": "function", "fn": pois}, "xhi": {"kind": "outflow"},
+             "ylo": {"kind": "noslip"}, "yhi": {"kind": "noslip"},
+             "zlo": {"kind": "symmetry"}, "zhi": {"kind": "symmetry"}}
+    st = Stepper(sp, BoundarySet(sp, specs), nu=1.0 / 2800.0, dt=2e-3, scheme_order=3,
+                 forcing=TrippingForcing(**TRIP),
+                 pressure=SolverOptions(tol=1e-5, max_iter=200, restart=20, precond="jacobi"),
+                 velocity=SolverOptions(tol=1e-8, max_iter=100, precond="jacobi"))
+    xs, ys, zs = sp.coords
+    state = st.initial_state(pois(xs, ys, zs, 0.0))
+    rows = []
+    for _ in range(3):
+        state, d = st.step(state)
+        rows.append(dict(step=d.step, p_it=d.p_iterations, v_it=list(d.v_iterations),
+                         ke=kinetic_energy(sp, state.vel), ens=enstrophy(sp, state.vel)))
+        print("trip channel", rows[-1], flush=True)
+    with open(os.path.join(OUT, "trip_channel.json"), "w") as fh:
+        json.dump(rows, fh, indent=1)
+
+
 def main():
+    if "--trip" in sys.argv:
+        gen_trip()
+        return
     if "--dealias" in sys.argv:
         gen_dealias()
         return
