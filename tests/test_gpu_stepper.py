@@ -220,3 +220,42 @@ def test_mini_rotor_steps(cuda):
         assert rel_err(d.cfl, row["cfl"]) < 1e-8
         # pressure GMRES ends at its 200-iteration cap (unconverged), as in the reference
         assert rel_err(kinetic_energy(sp, state.vel), row["ke"]) < 1e-7
+
+
+def test_primed_taylor_green(cuda):
+    """primed_state (timestep.py:174-200) with taylor_green walls: full-order steps
+    from an exact history; counts, KE and the error against the analytic vortex."""
+    import json
+    import os
+
+    from paper_2207_07098_b200.basis import make_basis
+    from paper_2207_07098_b200.bc import BoundarySet, decaying_vortex
+    from paper_2207_07098_b200.mesh import gen_box_mesh
+    from paper_2207_07098_b200.space import build_space
+    from paper_2207_07098_b200.timestep import SolverOptions, Stepper, kinetic_energy
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "primed_tg.json")) as fh:
+        rows = json.load(fh)
+    nu = 0.01
+    L = 2 * np.pi
+    sp = build_space(gen_box_mesh((0.0, L, 0.0, L, 0.0, 0.5 * np.pi), (4, 4, 2)), make_basis(6), device=cuda)
+    specs = {t: {"kind": "taylor_green", "nu": nu} for t in ("xlo", "xhi", "ylo", "yhi")}
+    specs.update({"zlo": {"kind": "symmetry"}, "zhi": {"kind": "symmetry"}})
+    st = Stepper(sp, BoundarySet(sp, specs), nu=nu, dt=5e-3, scheme_order=3,
+                 pressure=SolverOptions(tol=1e-8, max_iter=300, restart=20, precond="jacobi"),
+                 velocity=SolverOptions(tol=1e-10, max_iter=200, precond="jacobi"))
+
+    def prs(x, y, z, t):
+        return 0.25 * (np.cos(2.0 * x) + np.cos(2.0 * y)) * np.exp(-4.0 * nu * t)
+
+    state = st.primed_state(lambda x, y, z, t: decaying_vortex(x, y, z, t, nu), 0.0, prs_fn=prs)
+    assert state.primed and len(state.vel_hist) == 3 and len(state.nl_hist) == 2
+    xs = sp.coords.cpu().numpy()
+    for row in rows:
+        state, d = st.step(state)
+        assert st._last_order == 3
+        assert d.p_iterations == row["p_it"] and list(d.v_iterations) == row["v_it"], (d, row)
+        assert rel_err(kinetic_energy(sp, state.vel), row["ke"]) < 1e-9
+        ex = torch.from_numpy(decaying_vortex(xs[0], xs[1], xs[2], state.time, nu)).to(cuda)
+        err = float(np.sqrt(sum(sp.integral((state.vel[l] - ex[l]) ** 2) for l in range(3))))
+        assert rel_err(err, row["err"]) < 1e-6
