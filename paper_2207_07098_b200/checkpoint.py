@@ -27,6 +27,23 @@ from .timestep import FlowState
 MAGIC = b"SEMFCKPT"
 VERSION = 1
 
+#: per-step diagnostics CSV of the reference's runner (runner.py:27-28, 92-99)
+DIAG_HEADER = ("step,time,cfl,p_iters,p_res,ux_iters,uy_iters,uz_iters,"
+               "ux_res,uy_res,uz_res,div_norm,wall_time")
+
+
+def _fmt(x):
+    return f"{float(x):.17g}"
+
+
+def diag_row(d):
+    """One diagnostics.csv row for a StepDiagnostics, formatted as the reference
+    writes it (17 significant digits), so runs can be diffed column by column."""
+    vi, vr = d.v_iterations, d.v_residual
+    return ",".join([str(d.step), _fmt(d.time), _fmt(d.cfl), str(d.p_iterations), _fmt(d.p_residual),
+                     str(vi[0]), str(vi[1]), str(vi[2]), _fmt(vr[0]), _fmt(vr[1]), _fmt(vr[2]),
+                     _fmt(d.div_norm), _fmt(d.wall_time)])
+
 
 def write_checkpoint(path, arrays, meta):
     """Named float64 arrays + JSON metadata -> checkpoint file (output.py:69-84)."""

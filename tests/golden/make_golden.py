@@ -365,6 +365,16 @@ def gen_ckpt():
             "n_nl_hist": 0, "last_order": 3, "projections": {"p": {"count": 2, "solves": 7}}, "forcing": None}
     write_checkpoint(os.path.join(OUT, "ref_state.ckpt"), arrays, meta)
 
+    # the runner's diagnostics.csv row format (runner.py:92-99)
+    from semflow.runner import _DIAG_HEADER, _diag_row
+    from semflow.timestep import StepDiagnostics
+
+    d = StepDiagnostics(step=7, time=0.07000000000000001, cfl=0.2012345678901234, div_norm=1.25e-5,
+                        p_iterations=33, p_residual=9.87654321e-6, v_iterations=(4, 4, 3),
+                        v_residual=(1e-9, 2.5e-9, 3.333e-9), wall_time=0.0123)
+    with open(os.path.join(OUT, "diag_row.txt"), "w") as fh:
+        fh.write(_DIAG_HEADER + "\n" + _diag_row(d) + "\n")
+
     # a TGV 3^3 state after 3 steps, checkpointed by the reference's runner, and
     # the diagnostics of 3 more steps of the uninterrupted run
     from types import SimpleNamespace

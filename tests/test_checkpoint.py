@@ -109,3 +109,15 @@ def test_empty(tmp_path):
     p = tmp_path / "empty.ckpt"
     write_checkpoint(str(p), {}, {})
     assert read_checkpoint(str(p)) == ({}, {})
+
+
+def test_diagnostics_csv_row_matches_reference_runner():
+    from paper_2207_07098_b200.checkpoint import DIAG_HEADER, diag_row
+    from paper_2207_07098_b200.timestep import StepDiagnostics
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "diag_row.txt")) as fh:
+        header, row = fh.read().splitlines()
+    d = StepDiagnostics(step=7, time=0.07000000000000001, cfl=0.2012345678901234, div_norm=1.25e-5,
+                        p_iterations=33, p_residual=9.87654321e-6, v_iterations=(4, 4, 3),
+                        v_residual=(1e-9, 2.5e-9, 3.333e-9), wall_time=0.0123)
+    assert DIAG_HEADER == header and diag_row(d) == row
