@@ -247,3 +247,96 @@ def gen_cylinder_box_mesh(diameter, xlim, zlim, height, n_azimuthal=8, n_radial=
                 facet_tag=ft[order], tag_names=CYLINDER_TAGS,
                 curved_elem=np.asarray(curved_elem, dtype=np.int64), curved_coords=np.asarray(curved),
                 geom_order=geom_order)
+
+
+# --------------------------------------------------------------------------- mesh files
+
+MESH_MAGIC = b"SEMFMESH"
+MESH_VERSION = 1
+
+
+def write_mesh(mesh, path):
+    """The reference's versioned little-endian mesh file (mesh.py:444-466): magic,
+    uint32 version, uint64 header length, JSON header (sort_keys), then vertices,
+    elements, facet element/face/tag, curved element ids and curved records."""
+    import json
+
+    header = {"vertex_count": int(mesh.vertices.shape[0]), "element_count": int(mesh.elements.shape[0]),
+              "facet_count": int(np.asarray(mesh.facet_elem).size), "tag_names": list(mesh.tag_names),
+              "curved_count": int(np.asarray(mesh.curved_elem).size),
+              "geom_order": None if mesh.geom_order is None else int(mesh.geom_order)}
+    blob = json.dumps(header, sort_keys=True).encode("utf-8")
+    parts = [MESH_MAGIC, np.array(MESH_VERSION, dtype="<u4").tobytes(), np.array(len(blob), dtype="<u8").tobytes(),
+             blob]
+    for a, dt in ((mesh.vertices, "<f8"), (mesh.elements, "<i8"), (mesh.facet_elem, "<i8"),
+                  (mesh.facet_face, "<i8"), (mesh.facet_tag, "<i8"), (mesh.curved_elem, "<i8"),
+                  (mesh.curved_coords, "<f8")):
+        parts.append(np.ascontiguousarray(a, dtype=dt).tobytes())
+    with open(path, "wb") as fh:
+        for p in parts:
+            fh.write(p)
+
+
+def read_mesh(path):
+    """Read a mesh file (mesh.py:469-560); damage raises MeshFormatError naming
+    the byte offset and section."""
+    import json
+
+    from .errors import MeshFormatError
+
+    with open(path, "rb") as fh:
+        data = memoryview(fh.read())
+    cur = [0]
+
+    def chunk(nbytes, section):
+        at = cur[0]
+        if at + nbytes > len(data):
+            raise MeshFormatError(f"truncated file: need {nbytes} bytes, have {len(data) - at}",
+                                  offset=at, section=section)
+        cur[0] = at + nbytes
+        return data[at:at + nbytes]
+
+    magic = bytes(chunk(len(MESH_MAGIC), "magic"))
+    if magic != MESH_MAGIC:
+        raise MeshFormatError(f"bad magic {magic!r}, expected {MESH_MAGIC!r}", offset=0, section="magic")
+    version = int(np.frombuffer(chunk(4, "version"), dtype="<u4")[0])
+    if version != MESH_VERSION:
+        raise MeshFormatError(f"unsupported mesh format version {version}", offset=8, section="version")
+    hlen = int(np.frombuffer(chunk(8, "header"), dtype="<u8")[0])
+    hstart = cur[0]
+    try:
+        header = json.loads(bytes(chunk(hlen, "header")).decode("utf-8"))
+    except (UnicodeDecodeError, json.JSONDecodeError) as exc:
+        raise MeshFormatError(f"header is not valid JSON: {exc}", offset=hstart, section="header") from exc
+    try:
+        nv, ne, nf = int(header["vertex_count"]), int(header["element_count"]), int(header["facet_count"])
+        tags = tuple(str(t) for t in header["tag_names"])
+        nc = int(header["curved_count"])
+        go = header["geom_order"]
+    except (KeyError, TypeError, ValueError) as exc:
+        raise MeshFormatError(f"header missing or malformed field: {exc}", offset=hstart, section="header") from exc
+    if min(nv, ne, nf, nc) < 0:
+        raise MeshFormatError("negative count in header", offset=hstart, section="header")
+    if nc > 0 and go is None:
+        raise MeshFormatError("curved records present but geom_order is null", offset=hstart, section="header")
+
+    def arr(shape, dt, section):
+        count = int(np.prod(shape))
+        return np.frombuffer(chunk(count * 8, section), dtype=dt).reshape(shape).copy()
+
+    vertices = arr((nv, 3), "<f8", "vertices").astype(np.float64)
+    elements = arr((ne, 8), "<i8", "elements").astype(np.int64)
+    fe = arr((nf,), "<i8", "facet_elem").astype(np.int64)
+    ff = arr((nf,), "<i8", "facet_face").astype(np.int64)
+    ft = arr((nf,), "<i8", "facet_tag").astype(np.int64)
+    ce = arr((nc,), "<i8", "curved_elem").astype(np.int64)
+    if nc > 0:
+        g1 = int(go) + 1
+        cc = arr((nc, g1, g1, g1, 3), "<f8", "curved_coords").astype(np.float64)
+    else:
+        cc = np.zeros((0, 2, 2, 2, 3))
+    if cur[0] != len(data):
+        raise MeshFormatError(f"{len(data) - cur[0]} trailing bytes after final section", offset=cur[0],
+                              section="end")
+    return Mesh(vertices=vertices, elements=elements, facet_elem=fe, facet_face=ff, facet_tag=ft,
+                tag_names=tags, curved_elem=ce, curved_coords=cc, geom_order=None if go is None else int(go))

@@ -438,6 +438,12 @@ def gen_cyl():
             cnt = np.diff(sp.gs.offsets)
             out[f"{key}_mult_hist"] = np.bincount(cnt)
     np.savez_compressed(os.path.join(OUT, "cylinder.npz"), **out)
+    # the mini-rotor mesh in the reference's binary file format (mesh.py:444-466)
+    from semflow.mesh import write_mesh
+
+    write_mesh(gen_cylinder_box_mesh(1.0, (-4.0, 6.0), (-4.0, 4.0), 2.0, n_azimuthal=8, n_radial=2, n_axial=2,
+                                     n_upstream=4, n_downstream=5, n_front=3, n_back=3, geom_order=5),
+               os.path.join(OUT, "mini_rotor.mesh"))
 
     m = gen_cylinder_box_mesh(1.0, (-4.0, 6.0), (-4.0, 4.0), 2.0, n_azimuthal=8, n_radial=2, n_axial=2,
                               n_upstream=4, n_downstream=5, n_front=3, n_back=3, geom_order=5)
