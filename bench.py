@@ -466,7 +466,7 @@ def bench_tgv(args, world, rank, dev):
         P = sp.mesh.n_elements * sp.n ** 3
     else:
         ne = args.ne or (64 if args.warmup + args.steps <= 8 else 48)
-        sp, st, state = tgv_problem(ne, device=dev, comm=comm)
+        sp, st, state = tgv_problem(ne, device=dev, comm=comm, precond=args.precond)
         P = ne ** 3 * sp.n ** 3            # global points: strong scaling, fixed total work
     for _ in range(args.warmup):
         state, d = st.step(state)
@@ -534,7 +534,8 @@ def bench_tgv(args, world, rank, dev):
         metric = "GDOF/s per time step (cylinder, lx=8)"
     else:
         wl_name = (f"TGV Re=1600 {ne}^3 elements lx=8 (config {'3' if ne == 64 else '1' if ne == 8 else '1/3 analogue'}),"
-                   " symmetry box, Jacobi-GMRES(20) p 1e-5, Jacobi-PCG v 1e-8, projection on")
+                   f" symmetry box, {'Schwarz' if args.precond == 'schwarz' else 'Jacobi'}-GMRES(20) p 1e-5,"
+                   " Jacobi-PCG v 1e-8, projection on")
         metric = "GDOF/s per time step (TGV, lx=8)"
     return {
         "metric": metric,
@@ -585,6 +586,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--workload", default="tgv", choices=("tgv", "poisson", "channel", "cylinder"))
     ap.add_argument("--ne", type=int, default=0)
+    ap.add_argument("--precond", default="jacobi", choices=("jacobi", "schwarz"),
+                    help="TGV pressure preconditioner (schwarz: the reference's default, small meshes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
