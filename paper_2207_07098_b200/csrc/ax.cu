@@ -149,20 +149,26 @@ ax_helm_kernel(DMat<N> D, const double* __restrict__ g, const double* __restrict
 
 // K1 for n = 8: the one-pencil kernel with a bank-swizzled shared layout
 // (body in ax8s.cuh, shared with the fused Ax+dssum kernel).
-template <bool EX, bool MASK, bool PRE = false>
+template <bool EX, bool MASK, bool PRE = false, bool MASS = true>
 __global__ void __launch_bounds__(128, SF_AX8S_MINB)
 ax_helm8s_kernel(DMat<8> D, const double* __restrict__ g, const double* __restrict__ b,
                  const double* __restrict__ u, double* __restrict__ w, long long E, double lv,
                  double lm, const uint32_t* __restrict__ inmask, const uint32_t* __restrict__ outsel,
                  const double* __restrict__ pre = nullptr) {
-  ax8s_pair<EX, MASK, PRE>(D, g, b, u, w, E, lv, lm, inmask, outsel, (long long)blockIdx.x, nullptr, pre);
+  ax8s_pair<EX, MASK, PRE, MASS>(D, g, b, u, w, E, lv, lm, inmask, outsel, (long long)blockIdx.x, nullptr,
+                                 pre);
 }
 
+// Poisson-type operators (lam_mass == 0) run the variant without the mass term:
+// the B prefetch register would otherwise cost the common case ~8 %.
 template <bool EX, bool MASK, bool PRE>
 static void launch8s(dim3 grid, cudaStream_t st, const DMat<8>& D, const double* g, const double* b,
                      const double* u, double* w, long long E, double lv, double lm, const uint32_t* inmask,
                      const uint32_t* outsel, const double* pre) {
-  ax_helm8s_kernel<EX, MASK, PRE><<<grid, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel, pre);
+  if (lm != 0.0)
+    ax_helm8s_kernel<EX, MASK, PRE, true><<<grid, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel, pre);
+  else
+    ax_helm8s_kernel<EX, MASK, PRE, false><<<grid, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel, pre);
 }
 
 // K1 for n = 8, two pencils per thread (experimental, -DSF_AX_PENCIL2; measured

@@ -33,7 +33,9 @@ constexpr int kAxUnroll = SF_AX_UNROLL;
 // vector, `precond(v)` then `apply_a`, krylov.py:106-107) without materialising
 // it: each u value is scaled as it is loaded (one IEEE multiply, the same bits
 // as `inv_diag * v`), including the masked rows that pass u through.
-template <bool EX, bool MASK, bool PRE = false>
+// MASS: false compiles the mass term out (callers pass it only when lam_mass == 0,
+// where the reference skips the term, _numba.py:128); true keeps the runtime test.
+template <bool EX, bool MASK, bool PRE = false, bool MASS = true>
 __device__ __forceinline__ void ax8s_pair(const DMat<8>& D, const double* __restrict__ g,
                                           const double* __restrict__ b, const double* __restrict__ u,
                                           double* __restrict__ w, long long E, double lv, double lm,
@@ -145,12 +147,22 @@ __device__ __forceinline__ void ax8s_pair(const DMat<8>& D, const double* __rest
     dj[q] = D.v[q * N + j];
     dk[q] = D.v[q * N + k];
   }
+  // mass term: B is streamed one layer ahead (issued before the barrier) so its
+  // load latency hides behind the contraction instead of stalling each output
+  // layer (ncu/profile: the Helmholtz operator ran 1.5x the Poisson one)
+  const bool mass = MASS && lm != 0.0;
+  double bnext = 0.0;
+  if constexpr (MASS) bnext = (mass && active) ? __ldg(b + base) : 0.0;
   __syncthreads();
   if (!active) return;
 
-  const bool mass = lm != 0.0;
 #pragma unroll (kAxUnroll)
   for (int i = 0; i < N; ++i) {
+    double bi = 0.0;
+    if constexpr (MASS) {
+      bi = bnext;
+      if (mass && i + 1 < N) bnext = __ldg(b + base + (i + 1) * NN);
+    }
     double acc = 0.0;
     if constexpr (EX) {
       // the reference's single interleaved accumulator (_numba.py:119-126)
@@ -183,7 +195,7 @@ __device__ __forceinline__ void ax8s_pair(const DMat<8>& D, const double* __rest
       acc = (ar + as) + at;
     }
     double wv = mul<EX>(lv, acc);
-    if (mass) wv = add<EX>(wv, mul<EX>(mul<EX>(lm, __ldg(b + base + i * NN)), su[i * NN + st]));
+    if (mass) wv = add<EX>(wv, mul<EX>(mul<EX>(lm, bi), su[i * NN + st]));
     if constexpr (MASK) {
       if (!((outb >> i) & 1u)) {
         wv = __ldg(u + base + i * NN);

@@ -59,7 +59,7 @@ def run(ne):
             getattr(L, name).argtypes = args
         L.sf_last_error.restype = ctypes.c_char_p
         res = {}
-        for kind in ("masked", "plain", "dssum", "dssum_blk"):
+        for kind in ("masked", "plain", "dssum", "dssum_blk", "helm"):
             def fn():
                 if kind == "masked":
                     L.sf_ax_masked_f64(sp.dmat.ctypes.data, 8, sp.geom.data_ptr(), sp.bm.data_ptr(), u.data_ptr(),
@@ -68,6 +68,10 @@ def run(ne):
                 elif kind == "plain":
                     L.sf_ax_helm_f64(sp.dmat.ctypes.data, 8, sp.geom.data_ptr(), sp.bm.data_ptr(), u.data_ptr(),
                                      w.data_ptr(), sp.n_elements, 1.0, 0.0, 0, st)
+                elif kind == "helm":
+                    L.sf_ax_masked_f64(sp.dmat.ctypes.data, 8, sp.geom.data_ptr(), sp.bm.data_ptr(), u.data_ptr(),
+                                       w.data_ptr(), sp.n_elements, 1.0 / 1600, 183.3, op.inmask.data_ptr(),
+                                       op.outsel.data_ptr(), 0, st)
                 elif kind == "dssum_blk":
                     if not hasattr(gs, "cls_nb"):
                         gs._build_classes()
@@ -121,7 +125,8 @@ def run(ne):
                     res[f"{kind}{cpl}"] = float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3
         gbs = P * 64 / (res["masked"] * 1e-6) / 1e9
         print(f"{os.path.basename(path):24s} masked {res['masked']:8.1f} us ({gbs:6.0f} GB/s)  plain {res['plain']:8.1f} us"
-              f"  dssum {res['dssum']:7.1f} us  dssum_blk {res['dssum_blk']:7.1f} us", flush=True)
+              f"  dssum {res['dssum']:7.1f} us  dssum_blk {res['dssum_blk']:7.1f} us  helm {res['helm']:7.1f} us",
+              flush=True)
         fk = {k: round(v, 1) for k, v in res.items() if k.startswith("f")}
         if fk:
             print("   fused:", fk, flush=True)
