@@ -327,6 +327,37 @@ def _pipelinable(F, b):
             and (F.comm.world == 1 or F.comm.peer is not None))
 
 
+class _GraphBuffers:
+    """Fixed buffers and the per-step CUDA graphs of the look-ahead GMRES for one
+    (operator, preconditioner, restart, size) -- kept on the operator."""
+
+    def __init__(self, b, restart, S, key):
+        self.key = key
+        self.V = torch.empty((restart + 1,) + tuple(b.shape), dtype=torch.float64, device=b.device)
+        self.blk = torch.zeros((restart, S), dtype=torch.float64, device=b.device)
+        self.host = torch.zeros((restart, S), dtype=torch.float64, pin_memory=True)
+        self.z = torch.empty_like(b)
+        self.graphs = {}
+        self.pool = torch.cuda.graph_pool_handle()
+
+
+def _graph_buffers(F, op, b, restart, S):
+    """Graph replay applies on one rank (the fused NVLink reductions take a per-call
+    sequence number) unless SEMFLOW_B200_GRAPHS=0."""
+    if F.comm.world > 1 or os.environ.get("SEMFLOW_B200_GRAPHS", "1") == "0":
+        return None
+    # every device address a captured step reads: the graphs stay valid only while
+    # these are the same tensors (the buffers below are held alive by the cache)
+    key = (restart, tuple(b.shape), F.invdiag.data_ptr() if F.invdiag is not None else None, F.mult,
+           F.w.args()[0], _lib.stream_ptr(F.dev))
+    gb = getattr(op, "_gmres_graphs", None)
+    if gb is None or gb.key != key:
+        gb = _GraphBuffers(b, restart, S, key)
+        gb.refs = (F.invdiag,)
+        op._gmres_graphs = gb
+    return gb
+
+
 def _gmres_pipelined(F, op, b, tol, max_iter, restart):
     """GMRES with one Arnoldi step of look-ahead (same arithmetic as _gmres_fused).
 
@@ -356,16 +387,42 @@ def _gmres_pipelined(F, op, b, tol, max_iter, restart):
     o2 = 2 * (restart + 2)           # second sweep within an iteration block
     o3 = 4 * (restart + 2)           # [o3] reorth flag, [o3+1] final norm
     S = o3 + 4
-    blk = torch.zeros((restart, S), dtype=torch.float64, device=dev)
-    host = torch.zeros((restart, S), dtype=torch.float64, pin_memory=True)
-    z = torch.empty_like(b)
     total = 0
     converged = False
+    gb = _graph_buffers(F, op, b, restart, S)
+    if gb is not None:
+        blk, host, z, Vbuf = gb.blk, gb.host, gb.z, gb.V
+    else:
+        blk = torch.zeros((restart, S), dtype=torch.float64, device=dev)
+        host = torch.zeros((restart, S), dtype=torch.float64, pin_memory=True)
+        z = torch.empty_like(b)
+        Vbuf = None
 
     def launch(j, V):
+        if gb is not None:
+            # the whole Arnoldi step replayed from a CUDA graph captured once per
+            # operator (fixed buffers; ~10 us of host time instead of ~30 launches)
+            g = gb.graphs.get(j)
+            if g is None:
+                g = torch.cuda.CUDAGraph()
+                st_saved = F.st
+                with torch.cuda.graph(g, pool=gb.pool):
+                    F.st = _lib.stream_ptr(dev)
+                    body(j, V)
+                F.st = st_saved
+                gb.graphs[j] = g
+            g.replay()
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(dev))
+            V.append(Vbuf[j + 1])
+            return ev
+        ev = body(j, V)
+        return ev
+
+    def body(j, V):
         bl = blk[j]
         bp = lambda i: bl.data_ptr() + 8 * i
-        w = torch.empty_like(b)
+        w = torch.empty_like(b) if Vbuf is None else Vbuf[j + 1]
         F.apply_precond(V[j], w, z)
         F.mgs(bl[0:2], _lib.ptr(w), None, None, _lib.ptr(V[0]), None, None, mult, 1)
         for i in range(1, j + 1):
@@ -382,6 +439,9 @@ def _gmres_pipelined(F, op, b, tol, max_iter, restart):
               None, mult, 1, gate=g8)
         _lib.call("sf_gmres_gate_f64", bl.data_ptr(), j, o2, o3, 1, F.st)
         host[j].copy_(bl, non_blocking=True)
+        if Vbuf is not None:          # graph capture: the caller records the event
+            _lib.call("sf_scale_div_f64", _lib.ptr(w), _lib.ptr(w), None, None, bp(o3 + 1), P, F.st)
+            return None
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(dev))
         # speculative next basis vector v_{j+1} = w / norm_after (krylov.py:149)
@@ -391,7 +451,7 @@ def _gmres_pipelined(F, op, b, tol, max_iter, restart):
 
     while total < max_iter and not converged:
         m = min(restart, max_iter - total)
-        v0 = torch.empty_like(b)
+        v0 = torch.empty_like(b) if Vbuf is None else Vbuf[0]
         s0[1:2].fill_(beta)
         _lib.call("sf_scale_div_f64", _lib.ptr(v0), _lib.ptr(r), None, None, s0.data_ptr() + 8, P, F.st)
         V = [v0]
