@@ -311,3 +311,26 @@ def test_generic_solver_path_matches_fused(cuda):
     # the generic path rounds x += alpha p in two steps (torch), the fused one
     # uses DFMA: after 44 iterations the iterates differ at the ~1e-10 level
     assert rel_err(fused.x.cpu().numpy(), generic.x.cpu().numpy()) < 1e-8
+
+
+def test_gmres_graph_replay_reuse(cuda, golden_solvers, monkeypatch):
+    """Look-ahead GMRES replaying captured Arnoldi steps: the first solve captures,
+    later solves (other right-hand sides) replay; every solve equals the
+    un-captured path bit for bit and the reference's iteration count."""
+    from paper_2207_07098_b200 import krylov, operators as ops
+    from paper_2207_07098_b200.precond import BlockJacobi
+
+    sp, mask, rhs = _poisson_dev(4)
+    A = ops.make_global_op(sp, 1.0, 0.0, mask)
+    M = BlockJacobi(sp, 1.0, 0.0, mask)
+    monkeypatch.setenv("SEMFLOW_B200_GMRES_PIPELINE", "1")
+    want_its = golden_solvers["poisson4"]["gmres"]["iterations"]
+    results = []
+    for scale in (1.0, 0.5, 1.0):
+        info = krylov.gmres(A, rhs * scale, tol=1e-8 * scale, max_iter=500, restart=20, precond=M, dot=sp.gs.dot)
+        results.append(info)
+        assert info.iterations == want_its
+    assert A._gmres_graphs.graphs          # captured steps exist and were reused
+    monkeypatch.setenv("SEMFLOW_B200_GRAPHS", "0")
+    plain = krylov.gmres(A, rhs, tol=1e-8, max_iter=500, restart=20, precond=M, dot=sp.gs.dot)
+    assert torch.equal(plain.x, results[0].x) and torch.equal(plain.x, results[2].x)
