@@ -36,15 +36,12 @@ __device__ __forceinline__ void ref_derivs(const DM2<N>& D, const double* __rest
   }
 }
 
-// physical derivative d/dx_l from reference derivatives (operators.py:64-65)
+// physical derivative d/dx_l from reference derivatives (operators.py:64-65);
+// r[s][l] = rx[s, l] at this point, loaded before the shared-memory barrier so
+// the nine metric loads overlap the element staging instead of stalling here
 template <bool EX>
-__device__ __forceinline__ double chain(const double* __restrict__ rx, long long PT, long long p, int l,
-                                        double ar, double as, double at) {
-  // rx[s, l] plane index = (s*3 + l)
-  const double r0 = __ldg(rx + (0 * 3 + l) * PT + p);
-  const double r1 = __ldg(rx + (1 * 3 + l) * PT + p);
-  const double r2 = __ldg(rx + (2 * 3 + l) * PT + p);
-  return add<EX>(add<EX>(mul<EX>(r0, ar), mul<EX>(r1, as)), mul<EX>(r2, at));
+__device__ __forceinline__ double chain(const double (&r)[3][3], int l, double ar, double as, double at) {
+  return add<EX>(add<EX>(mul<EX>(r[0][l], ar), mul<EX>(r[1][l], as)), mul<EX>(r[2][l], at));
 }
 
 enum DerivOp { OP_GRAD = 0, OP_DIV = 1, OP_CURL = 2, OP_ADVECT = 3 };
@@ -67,20 +64,29 @@ deriv_kernel(DM2<N> D, const double* __restrict__ in, const double* __restrict__
   const long long p = e * NNN + x;
 #pragma unroll
   for (int f = 0; f < NF; ++f) ue[f][x] = __ldg(in + f * PT + p);
+  double r[3][3];
+#pragma unroll
+  for (int sl = 0; sl < 9; ++sl) r[sl / 3][sl % 3] = __ldg(rx + sl * PT + p);
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+  if constexpr (OP == OP_ADVECT) {
+    c0 = __ldg(c + p);
+    c1 = __ldg(c + PT + p);
+    c2 = __ldg(c + 2 * PT + p);
+  }
   __syncthreads();
   const int i = x / NN, j = (x / N) % N, k = x % N;
   if constexpr (OP == OP_GRAD) {
     double ar, as, at;
     ref_derivs<N, EX>(D, ue[0], i, j, k, ar, as, at);
 #pragma unroll
-    for (int l = 0; l < 3; ++l) out[l * PT + p] = chain<EX>(rx, PT, p, l, ar, as, at);
+    for (int l = 0; l < 3; ++l) out[l * PT + p] = chain<EX>(r, l, ar, as, at);
   } else if constexpr (OP == OP_DIV) {
     double acc = 0.0;
 #pragma unroll
     for (int l = 0; l < 3; ++l) {
       double ar, as, at;
       ref_derivs<N, EX>(D, ue[l], i, j, k, ar, as, at);
-      acc = add<EX>(acc, chain<EX>(rx, PT, p, l, ar, as, at));
+      acc = add<EX>(acc, chain<EX>(r, l, ar, as, at));
     }
     out[p] = acc;
   } else if constexpr (OP == OP_CURL) {
@@ -91,20 +97,19 @@ deriv_kernel(DM2<N> D, const double* __restrict__ in, const double* __restrict__
       double ar, as, at;
       ref_derivs<N, EX>(D, ue[f], i, j, k, ar, as, at);
 #pragma unroll
-      for (int m = 0; m < 3; ++m) g[f][m] = (m == f) ? 0.0 : chain<EX>(rx, PT, p, m, ar, as, at);
+      for (int m = 0; m < 3; ++m) g[f][m] = (m == f) ? 0.0 : chain<EX>(r, m, ar, as, at);
     }
     out[0 * PT + p] = sub<EX>(g[2][1], g[1][2]);
     out[1 * PT + p] = sub<EX>(g[0][2], g[2][0]);
     out[2 * PT + p] = sub<EX>(g[1][0], g[0][1]);
   } else {  // OP_ADVECT
-    const double c0 = __ldg(c + p), c1 = __ldg(c + PT + p), c2 = __ldg(c + 2 * PT + p);
 #pragma unroll
     for (int f = 0; f < 3; ++f) {
       double ar, as, at;
       ref_derivs<N, EX>(D, ue[f], i, j, k, ar, as, at);
-      const double g0 = chain<EX>(rx, PT, p, 0, ar, as, at);
-      const double g1 = chain<EX>(rx, PT, p, 1, ar, as, at);
-      const double g2 = chain<EX>(rx, PT, p, 2, ar, as, at);
+      const double g0 = chain<EX>(r, 0, ar, as, at);
+      const double g1 = chain<EX>(r, 1, ar, as, at);
+      const double g2 = chain<EX>(r, 2, ar, as, at);
       const double a = add<EX>(add<EX>(mul<EX>(c0, g0), mul<EX>(c1, g1)), mul<EX>(c2, g2));
       out[f * PT + p] = sign * a;  // sign is +-1: exact
     }
