@@ -482,6 +482,13 @@ def bench_tgv(args, world, rank, dev):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     clk = ClockSampler(torch.cuda.current_device())
+    # setup objects (meshes, maps, operators) are long-lived: move them out of the
+    # collector's generations so a full collection during a step stays cheap
+    import gc
+
+    if os.environ.get("SEMFLOW_B200_GC_FREEZE", "1") != "0":
+        gc.collect()
+        gc.freeze()
     clk.start()
     barrier(world)
     torch.cuda.synchronize()
