@@ -108,6 +108,10 @@ def dist_setup():
     if world > 1:
         import torch.distributed as dist
 
+        # NCCL prints its version banner on stdout at the VERSION and WARN levels;
+        # the driver expects exactly one JSON line there
+        if os.environ.get("NCCL_DEBUG", "WARN").upper() in ("WARN", "VERSION"):
+            os.environ["NCCL_DEBUG"] = "NONE"
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:

@@ -93,6 +93,14 @@ int sf_ax_masked_f64(const double* d_host, int n, const double* g, const double*
                      const double* u, double* w, long long E, double lam_visc, double lam_mass,
                      const uint32_t* inmask, const uint32_t* outsel, int exact, void* stream);
 
+/* The element operator (plain / masked / pre-scaled) on elements [e0, e1) of an
+ * E-element field (n = 8; e0 even, e1 even or E; geometry strides use E): the
+ * multi-GPU operator computes the halo elements first, posts the NVLink halo
+ * exchange, then the interior.  pre, inmask/outsel optional. */
+int sf_ax_range_f64(const double* d_host, int n, const double* g, const double* b, const double* u,
+                    const double* pre, double* w, long long E, long long e0, long long e1, double lam_visc,
+                    double lam_mass, const uint32_t* inmask, const uint32_t* outsel, int exact, void* stream);
+
 /* In-place dssum (QQ^T) over the shared part of the gather-scatter map:
  * offsets (n_shared+1) / perm (int32 local indices) of the gids with
  * multiplicity > 1, grouped by gid with ascending local index (space.py:303-305).

@@ -154,9 +154,9 @@ __global__ void __launch_bounds__(128, SF_AX8S_MINB)
 ax_helm8s_kernel(DMat<8> D, const double* __restrict__ g, const double* __restrict__ b,
                  const double* __restrict__ u, double* __restrict__ w, long long E, double lv,
                  double lm, const uint32_t* __restrict__ inmask, const uint32_t* __restrict__ outsel,
-                 const double* __restrict__ pre = nullptr) {
-  ax8s_pair<EX, MASK, PRE, MASS>(D, g, b, u, w, E, lv, lm, inmask, outsel, (long long)blockIdx.x, nullptr,
-                                 pre);
+                 const double* __restrict__ pre = nullptr, long long pair0 = 0) {
+  ax8s_pair<EX, MASK, PRE, MASS>(D, g, b, u, w, E, lv, lm, inmask, outsel, (long long)blockIdx.x + pair0,
+                                 nullptr, pre);
 }
 
 // Poisson-type operators (lam_mass == 0) run the variant without the mass term:
@@ -164,11 +164,45 @@ ax_helm8s_kernel(DMat<8> D, const double* __restrict__ g, const double* __restri
 template <bool EX, bool MASK, bool PRE>
 static void launch8s(dim3 grid, cudaStream_t st, const DMat<8>& D, const double* g, const double* b,
                      const double* u, double* w, long long E, double lv, double lm, const uint32_t* inmask,
-                     const uint32_t* outsel, const double* pre) {
+                     const uint32_t* outsel, const double* pre, long long pair0 = 0) {
   if (lm != 0.0)
-    ax_helm8s_kernel<EX, MASK, PRE, true><<<grid, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel, pre);
+    ax_helm8s_kernel<EX, MASK, PRE, true><<<grid, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel, pre,
+                                                                pair0);
   else
-    ax_helm8s_kernel<EX, MASK, PRE, false><<<grid, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel, pre);
+    ax_helm8s_kernel<EX, MASK, PRE, false><<<grid, 128, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel, pre,
+                                                                 pair0);
+}
+
+// Elements [e0, e1) of an E-element field (e0 even; strides use E): the boundary /
+// interior split that lets the multi-GPU operator post its halo exchange before
+// the interior elements are computed.
+int ax_helm8_range(const double* d_host, const double* g, const double* b, const double* u, const double* pre,
+                   double* w, long long E, long long e0, long long e1, double lv, double lm,
+                   const uint32_t* inmask, const uint32_t* outsel, int exact, cudaStream_t st) {
+  if (e0 < 0 || e1 > E || e0 > e1 || (e0 & 1) || ((e1 & 1) && e1 != E)) {
+    set_error("ax_range: bad element range [%lld, %lld) of %lld (ends must be even or E)", e0, e1, E);
+    return SF_ERR_ARG;
+  }
+  if ((inmask == nullptr) != (outsel == nullptr)) {
+    set_error("ax_range: inmask and outsel must both be given or both be null");
+    return SF_ERR_ARG;
+  }
+  if (e1 == e0) return SF_OK;
+  DMat<8> D;
+  for (int x = 0; x < 64; ++x) D.v[x] = d_host[x];
+  const long long p0 = e0 / 2, p1 = (e1 + 1) / 2;
+  dim3 grid((unsigned)(p1 - p0));
+  const bool masked = inmask != nullptr;
+#define R(EXV, MV, PV) launch8s<EXV, MV, PV>(grid, st, D, g, b, u, w, E, lv, lm, inmask, outsel, pre, p0)
+  if (exact) {
+    if (pre) { if (masked) R(true, true, true); else R(true, false, true); }
+    else { if (masked) R(true, true, false); else R(true, false, false); }
+  } else {
+    if (pre) { if (masked) R(false, true, true); else R(false, false, true); }
+    else { if (masked) R(false, true, false); else R(false, false, false); }
+  }
+#undef R
+  return check_launch("ax_range");
 }
 
 // K1 for n = 8, two pencils per thread (experimental, -DSF_AX_PENCIL2; measured

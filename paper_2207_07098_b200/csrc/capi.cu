@@ -48,6 +48,8 @@ int gather(double*, const double*, const int*, long long, cudaStream_t);
 int dssum_cls(double*, const int*, int, int, int, const int*, int, int, const double*, const double*,
               int, cudaStream_t);
 int rank_sum(const double*, int, int, double*, cudaStream_t);
+int ax_helm8_range(const double*, const double*, const double*, const double*, const double*, double*, long long,
+                   long long, long long, double, double, const uint32_t*, const uint32_t*, int, cudaStream_t);
 int dssum_blk(double*, const int*, int, int, int, const int*, const int*, int, int, const double*,
               const double*, const double*, int, cudaStream_t);
 int ax_dssum8(const double*, const double*, const double*, const double*, double*, long long, double,
@@ -149,6 +151,17 @@ int sf_ax_pre_f64(const double* d_host, int n, const double* g, const double* b,
   }
   return ax_helm(d_host, n, g, b, u, w, E, lam_visc, lam_mass, inmask, outsel, exact,
                  as_stream(stream), pre);
+}
+
+int sf_ax_range_f64(const double* d_host, int n, const double* g, const double* b, const double* u,
+                    const double* pre, double* w, long long E, long long e0, long long e1, double lam_visc,
+                    double lam_mass, const uint32_t* inmask, const uint32_t* outsel, int exact, void* stream) {
+  if (n != 8) {
+    set_error("sf_ax_range_f64: element ranges are implemented for n = 8 (got %d)", n);
+    return SF_ERR_UNSUPPORTED;
+  }
+  return ax_helm8_range(d_host, g, b, u, pre, w, E, e0, e1, lam_visc, lam_mass, inmask, outsel, exact,
+                        as_stream(stream));
 }
 
 int sf_dssum_f64(double* v, const int* offsets, const int* perm, int n_shared, int mode,

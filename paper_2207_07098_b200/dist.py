@@ -257,16 +257,27 @@ class HaloIPC:
         torch.cuda.synchronize()
         comm.dist.barrier(group=comm.group)
 
-    def exchange(self, v):
+    def put(self, v):
+        """Enqueue the NVLink stores of this rank's interface copies (call sequence +1)."""
+        if self.n_peers == 0:
+            return
+        self.seq += 1
+        _lib.call("sf_halo_put_f64", _lib.ptr(v), _lib.ptr(self.plan.send_all), self.n_peers, self.peer_rank,
+                  self.seg, self.dst, self.stride, self.flag, self.seq, _lib.ptr(self.counter),
+                  _lib.stream_ptr(v.device))
+
+    def wait(self, device):
+        """Enqueue the wait for the peers' copies of the last put; returns the inbox bank."""
         if self.n_peers == 0:
             return None
-        self.seq += 1
-        st = _lib.stream_ptr(v.device)
-        _lib.call("sf_halo_put_f64", _lib.ptr(v), _lib.ptr(self.plan.send_all), self.n_peers, self.peer_rank,
-                  self.seg, self.dst, self.stride, self.flag, self.seq, _lib.ptr(self.counter), st)
-        _lib.call("sf_halo_wait", self.own, self.n_peers, self.peer_rank, self.seq, _lib.ptr(self.error), st)
+        _lib.call("sf_halo_wait", self.own, self.n_peers, self.peer_rank, self.seq, _lib.ptr(self.error),
+                  _lib.stream_ptr(device))
         self.comm.collectives += 1
         return _RawPtr(self.own + 8 * (self.HEADER + (self.seq & 1) * self.n_recv))
+
+    def exchange(self, v):
+        self.put(v)
+        return self.wait(v.device)
 
     def check(self):
         if int(self.error.item()):

@@ -23,6 +23,10 @@ def _ex():
     return 1 if _device.EXACT else 0
 
 
+#: multi-GPU operator: compute halo elements, post the exchange, then the interior
+_OVERLAP = os.environ.get("SEMFLOW_B200_OVERLAP", "1") != "0"
+
+
 def _ax_local(space, u, lam_visc, lam_mass, out=None):
     _lib.require_cuda(u)
     u = u.contiguous()
@@ -96,6 +100,29 @@ class GlobalOp:
         gs = sp.gs
         st = _lib.stream_ptr(sp.device)
         E = sp.n_elements
+        split = gs.interior_range() if (sp.n == 8 and _OVERLAP) else None
+        if split is not None:
+            # halo elements first, post the NVLink exchange, interior while it
+            # travels, then the wait and the dssum
+            lo, hi = split
+            args = (_lib.ptr(self.inmask) if self.masked else None, _lib.ptr(self.outsel) if self.masked else None,
+                    _ex(), st)
+
+            def rng(e0, e1):
+                _lib.call("sf_ax_range_f64", sp.dmat.ctypes.data, sp.n, _lib.ptr(sp.geom), _lib.ptr(sp.bm),
+                          _lib.ptr(u), _lib.ptr(pre), _lib.ptr(w), E, e0, e1, self.lam_visc, self.lam_mass, *args)
+
+            rng(0, lo)
+            rng(hi, E)
+            gs.halo_put(w)
+            rng(lo, hi)
+            recv = gs.halo_wait()
+            if self.masked:
+                gs.dssum_into(w, 2, u=u, perm=self.sh_perm, pre=pre, recv=recv)
+            else:
+                gs.dssum_into(w, 0, recv=recv)
+            self.launches += 5
+            return w
         if pre is not None:
             if sp.n != 8:
                 return self.apply_into(pre * u, w)

@@ -169,6 +169,36 @@ class GatherScatter:
         return int(self.sh_perm.numel())
 
     # ------------------------------------------------------------ kernels
+    def interior_range(self):
+        """(lo, hi): the longest run of local elements with no interface copy (even
+        bounds), computed once -- the operator computes [0, lo) and [hi, E) first,
+        posts the halo exchange, then computes [lo, hi) while it travels.  None
+        when there is no such run (single rank, NCCL path, tiny partitions)."""
+        if getattr(self, "_interior", False) is not False:
+            return self._interior
+        self._interior = None
+        if self.plan is None or not self.plan.peers or self._ipc is None:
+            return None
+        E = self.shape[0]
+        nnn = self.P // E
+        iface = torch.unique(self.plan.send_all.long() // nnn).cpu().numpy()
+        edges = np.concatenate([[-1], iface, [E]])
+        gaps = edges[1:] - edges[:-1] - 1
+        k = int(np.argmax(gaps))
+        lo = int(edges[k]) + 1
+        hi = int(edges[k + 1])
+        lo += lo & 1                       # even start
+        hi = hi if hi == E else hi - (hi & 1)
+        if hi - lo >= 2:
+            self._interior = (lo, hi)
+        return self._interior
+
+    def halo_put(self, v):
+        self._ipc.put(v)
+
+    def halo_wait(self):
+        return self._ipc.wait(self.device)
+
     def halo_exchange(self, v):
         """Send this rank's interface copies of field v, receive the peers' (raw values).
         Returns the receive buffer (None on a single rank)."""
@@ -349,11 +379,13 @@ class GatherScatter:
         meta = np.array([len(sched), cp, K] + offs, dtype=np.int64)
         return FusedPlan(plan, meta, torch.zeros(K + 1, dtype=torch.int64, device=dev), len(sched))
 
-    def dssum_into(self, v, mode, u=None, perm=None, pre=None):
+    def dssum_into(self, v, mode, u=None, perm=None, pre=None, recv=False):
         """In-place dssum of one scalar row v (mode 0 add / 1 avg / 2 masked with u).
         ``perm``: a flagged copy of ``cls_perm`` (masked operators); ``pre``: the
-        masked copies receive pre * u (operator applied with sf_ax_pre_f64)."""
-        recv = self.halo_exchange(v)
+        masked copies receive pre * u (operator applied with sf_ax_pre_f64);
+        ``recv``: the receive buffer of an exchange the caller already posted."""
+        if recv is False:
+            recv = self.halo_exchange(v)
         if not hasattr(self, "cls_perm"):
             self._build_classes()
         n2, n4, n8 = self.cls_n
