@@ -2,9 +2,9 @@
 # Round-end evidence on one B200 (run under gpurun from the repo root):
 #   1. the default bench line (the driver's command), then
 #   2. the ncu launch list of the same bench (per-launch gpu__time_duration), then
-#   3. one ncu --set full capture of the dominant kernel (GMRES MGS pass) and of
-#      Ax / dssum at the bench's size.
-# Outputs land in gpurun_out/ (copied to profiles/ by hand).
+#   3. ncu --set full captures of the dominant kernel (GMRES MGS pass), the Ax
+#      kernel and the dssum kernel at the bench's size.
+# Outputs land in gpurun_out/ (summaries copied to profiles/ by hand).
 set -u
 mkdir -p gpurun_out
 timeout 1500 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
@@ -17,7 +17,11 @@ timeout 1800 ncu --set full --clock-control none --import-source on -k regex:mgs
   -o gpurun_out/mgs_full --force-overwrite \
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_mgs.log 2>&1
 echo "mgs capture rc=$?"
-timeout 1800 ncu --set full --clock-control none --import-source on -k regex:"ax_helm8s|dssum_cls" -c 4 \
-  -o gpurun_out/axdss_full --force-overwrite \
-  python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_axdss.log 2>&1
-echo "ax/dssum capture rc=$?"
+timeout 1800 ncu --set full --clock-control none --import-source on -k regex:ax_helm8s -c 2 \
+  -o gpurun_out/ax_full --force-overwrite \
+  python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_ax.log 2>&1
+echo "ax capture rc=$?"
+timeout 1800 ncu --set full --clock-control none --import-source on -k regex:dssum_blk -s 8 -c 2 \
+  -o gpurun_out/dssum_full --force-overwrite \
+  python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_dssum.log 2>&1
+echo "dssum capture rc=$?"
