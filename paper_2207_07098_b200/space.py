@@ -57,6 +57,19 @@ def pack_bits(flags):
 
 # --------------------------------------------------------------------------- gather-scatter
 
+def interior_run(iface, E):
+    """Longest run [lo, hi) of elements 0..E-1 containing none of the sorted
+    element ids ``iface``, with an even start and an even (or E) end -- the
+    interior computed while a halo exchange travels; None if shorter than 2."""
+    edges = np.concatenate([[-1], np.asarray(iface, dtype=np.int64), [E]])
+    gaps = edges[1:] - edges[:-1] - 1
+    k = int(np.argmax(gaps))
+    lo, hi = int(edges[k]) + 1, int(edges[k + 1])
+    lo += lo & 1
+    hi = hi if hi == E else hi - (hi & 1)
+    return (lo, hi) if hi - lo >= 2 else None
+
+
 class FusedPlan:
     """Device schedule of sf_ax_dssum8_f64 (see GatherScatter.fused_plan)."""
 
@@ -181,16 +194,7 @@ class GatherScatter:
             return None
         E = self.shape[0]
         nnn = self.P // E
-        iface = torch.unique(self.plan.send_all.long() // nnn).cpu().numpy()
-        edges = np.concatenate([[-1], iface, [E]])
-        gaps = edges[1:] - edges[:-1] - 1
-        k = int(np.argmax(gaps))
-        lo = int(edges[k]) + 1
-        hi = int(edges[k + 1])
-        lo += lo & 1                       # even start
-        hi = hi if hi == E else hi - (hi & 1)
-        if hi - lo >= 2:
-            self._interior = (lo, hi)
+        self._interior = interior_run(torch.unique(self.plan.send_all.long() // nnn).cpu().numpy(), E)
         return self._interior
 
     def halo_put(self, v):

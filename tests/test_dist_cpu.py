@@ -136,3 +136,18 @@ def test_gloo_halo_exchange_world2(oracle, world):
     for r in range(world):
         assert np.array_equal(res[r][1], np.array([3.0, 0.5]))
     assert starts[-1] == E
+
+
+def test_interior_run():
+    """Element range computed while the halo travels (space.interior_run)."""
+    from paper_2207_07098_b200.space import interior_run
+
+    E = 64
+    # z-slab middle rank: first and last 16-element layers hold interface copies
+    iface = list(range(0, 16)) + list(range(48, 64))
+    assert interior_run(iface, E) == (16, 48)
+    assert interior_run(list(range(48, 64)), E) == (0, 48)          # first rank
+    assert interior_run(list(range(0, 16)), E) == (16, 64)          # last rank
+    assert interior_run([3, 50], E) == (4, 50)                       # even bounds
+    assert interior_run(list(range(E)), E) is None
+    assert interior_run([0, 2], 3) is None
