@@ -338,6 +338,7 @@ class _GraphBuffers:
         self.host = torch.zeros((restart, S), dtype=torch.float64, pin_memory=True)
         self.z = torch.empty_like(b)
         self.graphs = {}
+        self.counts = {}          # library launches recorded in each captured step
         self.pool = torch.cuda.graph_pool_handle()
 
 
@@ -406,12 +407,16 @@ def _gmres_pipelined(F, op, b, tol, max_iter, restart):
             if g is None:
                 g = torch.cuda.CUDAGraph()
                 st_saved = F.st
+                n0 = _lib.LAUNCHES
                 with torch.cuda.graph(g, pool=gb.pool):
                     F.st = _lib.stream_ptr(dev)
                     body(j, V)
                 F.st = st_saved
+                gb.counts[j] = _lib.LAUNCHES - n0       # captured, not launched: counted per replay
+                _lib.LAUNCHES = n0
                 gb.graphs[j] = g
             g.replay()
+            _lib.LAUNCHES += gb.counts[j]
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream(dev))
             V.append(Vbuf[j + 1])
