@@ -12,7 +12,9 @@ import sys
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size",
         "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "l1tex__throughput.avg.pct_of_peak_sustained_active", "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
+        "l1tex__throughput.avg.pct_of_peak_sustained_active", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "TPC.TriageCompute.sm__pipe_fp64_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"]
 
 
 def rows(rep):
@@ -46,8 +48,8 @@ def main():
     with open(dst, "w") as fh:
         json.dump({"launches": launches}, fh, indent=1)
     for it in launches:
-        print(it["kernel"][:60], it.get("gpu__time_duration.sum [us]"), it.get("dram__bytes_read.sum [Gbyte]"),
-              it.get("dram__bytes_write.sum [Gbyte]"), it["top_stalls_per_issue"][:2])
+        print(it["kernel"][:48], {k.split(".")[0].split("__")[-1]: v for k, v in it.items()
+                                   if "fp64" in k or "dram__bytes" in k or "duration" in k})
 
 
 if __name__ == "__main__":
