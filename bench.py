@@ -131,6 +131,33 @@ def barrier_max(value, world):
     return float(t.item())
 
 
+def all_sum(values, world):
+    """sum over ranks of a list of host floats"""
+    if world == 1:
+        return list(values)
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(list(values), dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.tolist()
+
+
+def step_traffic(bytes_sum, gate, t, steps, world, peak):
+    """Step-level roofline (SURVEY 8(d) "Time step"): the algorithmic bytes of every
+    library call in the timed steps (traffic.py; gated second-sweep MGS passes
+    credited with the measured fire fraction), summed over ranks, per step and
+    divided by the step time.  torch's own elementwise kernels are not credited."""
+    from paper_2207_07098_b200 import traffic
+
+    fire = gate[0] / gate[1] if gate[1] else 1.0
+    per_step = (bytes_sum[0] + fire * bytes_sum[1]) / steps
+    ach = per_step / (t / steps) / 1e9
+    return {"algorithmic_bytes_per_step": per_step, "achieved": ach, "peak": peak * world, "unit": "GB/s",
+            "frac": ach / (peak * world), "second_sweep_fire_fraction": fire,
+            "uncredited": sorted(traffic.UNMODELED) + ["torch elementwise kernels"]}
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -304,6 +331,8 @@ def bench_poisson(args, world, rank, dev):
     barrier(world)
     torch.cuda.synchronize()
     l0 = _lib.LAUNCHES
+    _lib.BYTES[:] = [0, 0]
+    _lib.ACCOUNT = True
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     its = 0
@@ -311,9 +340,11 @@ def bench_poisson(args, world, rank, dev):
         info = solve(rhs)
         its += info.iterations
     e1.record(st)
+    _lib.ACCOUNT = False
     torch.cuda.synchronize()
     barrier(world)
     launches = _lib.LAUNCHES - l0
+    traffic_sum = all_sum(list(_lib.BYTES), world)
     clk.stop()
     t = barrier_max(e0.elapsed_time(e1) * 1e-3, world)
     value = world * P * its / t / 1e9
@@ -351,7 +382,8 @@ def bench_poisson(args, world, rank, dev):
                      "kernel": "ax_dssum8_kernel (fused masked Ax+dssum)" if "fused" in kt
                      else "ax_helm(masked)+dssum",
                      "algorithmic_bytes": nbytes, "us": t_op * 1e6, "ax_us": kt["ax"] * 1e6,
-                     "dssum_us": kt["dssum"] * 1e6, "peak_source": src},
+                     "dssum_us": kt["dssum"] * 1e6, "peak_source": src,
+                     "step": step_traffic(traffic_sum, [0, 0], t, args.steps, world, pk["hbm_gbs"])},
         "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
     }
     return line
@@ -493,10 +525,15 @@ def bench_tgv(args, world, rank, dev):
     if os.environ.get("SEMFLOW_B200_GC_FREEZE", "1") != "0":
         gc.collect()
         gc.freeze()
+    from paper_2207_07098_b200 import krylov as _kry
+
     clk.start()
     barrier(world)
     torch.cuda.synchronize()
     l0 = _lib.LAUNCHES
+    _lib.BYTES[:] = [0, 0]
+    _kry.GATE_STATS[:] = [0, 0]
+    _lib.ACCOUNT = True
     p_its, v_its = [], []
     t0 = time.perf_counter()
     for k in range(args.steps):
@@ -512,9 +549,11 @@ def bench_tgv(args, world, rank, dev):
         p_its.append(d.p_iterations)
         v_its.append(list(d.v_iterations))
     te_local = time.perf_counter() - t0
+    _lib.ACCOUNT = False
     torch.cuda.synchronize()
     barrier(world)
     launches = _lib.LAUNCHES - l0
+    traffic_sum = all_sum(list(_lib.BYTES) + list(_kry.GATE_STATS), world)
     clk.stop()
     t = barrier_max(sum(a.elapsed_time(b) for a, b in evs) * 1e-3, world)
     te = barrier_max(te_local, world)
@@ -572,7 +611,9 @@ def bench_tgv(args, world, rank, dev):
                                   "algorithmic_bytes": nbytes, "us": t_op * 1e6, "ax_us": kt["ax"] * 1e6,
                                   "dssum_us": kt["dssum"] * 1e6,
                                   "kernel": ("ax_dssum8_kernel, fused" if "fused" in kt else "ax_helm + dssum")
-                                  + " (pressure Poisson operator)"}},
+                                  + " (pressure Poisson operator)"},
+                     "step": step_traffic(traffic_sum[:2], traffic_sum[2:], t, args.steps, world,
+                                          pk["hbm_gbs"])},
         "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
     }
 

@@ -101,12 +101,21 @@ def load(path=LIB_PATH):
 #: number of library entry-point calls that launch kernels (bench.py's gpu_launches)
 LAUNCHES = 0
 
+#: algorithmic HBM bytes of the calls made while ACCOUNT is set, [ungated, gated
+#: MGS passes] (traffic.py; bench.py's step roofline)
+ACCOUNT = False
+BYTES = [0, 0]
+
 
 def call(name, *args):
     """Invoke an entry point and raise LibraryError on a nonzero status."""
     global LAUNCHES
     lib = _lib if _lib is not None else load()
     LAUNCHES += 1
+    if ACCOUNT:
+        from . import traffic
+
+        traffic.account(name, args, BYTES)
     st = getattr(lib, name)(*args)
     if st != 0:
         msg = lib.sf_last_error().decode(errors="replace")

@@ -314,6 +314,11 @@ def _gmres_generic(apply_a, b, tol, max_iter, restart, precond, dot, x0):
     return SolveInfo(x, total, beta, res0, converged)
 
 
+#: [Arnoldi steps whose second Gram-Schmidt sweep fired, steps] of the look-ahead
+#: GMRES (its second sweep is gated on the device; bench.py's step accounting)
+GATE_STATS = [0, 0]
+
+
 def _pipelinable(F, b):
     """The pipelined GMRES needs the gated (vectorised) MGS kernels and, across
     ranks, the fused peer reduction.  It pays off where the host round trip per
@@ -339,6 +344,7 @@ class _GraphBuffers:
         self.z = torch.empty_like(b)
         self.graphs = {}
         self.counts = {}          # library launches recorded in each captured step
+        self.bytes = {}           # and their algorithmic bytes (traffic.py)
         self.pool = torch.cuda.graph_pool_handle()
 
 
@@ -407,16 +413,23 @@ def _gmres_pipelined(F, op, b, tol, max_iter, restart):
             if g is None:
                 g = torch.cuda.CUDAGraph()
                 st_saved = F.st
-                n0 = _lib.LAUNCHES
+                n0, b0 = _lib.LAUNCHES, list(_lib.BYTES)
+                acc, _lib.ACCOUNT = _lib.ACCOUNT, True
                 with torch.cuda.graph(g, pool=gb.pool):
                     F.st = _lib.stream_ptr(dev)
                     body(j, V)
                 F.st = st_saved
-                gb.counts[j] = _lib.LAUNCHES - n0       # captured, not launched: counted per replay
-                _lib.LAUNCHES = n0
+                _lib.ACCOUNT = acc
+                # captured, not launched: launches and bytes are counted per replay
+                gb.counts[j] = _lib.LAUNCHES - n0
+                gb.bytes[j] = [a - c for a, c in zip(_lib.BYTES, b0)]
+                _lib.LAUNCHES, _lib.BYTES[:] = n0, b0
                 gb.graphs[j] = g
             g.replay()
             _lib.LAUNCHES += gb.counts[j]
+            if _lib.ACCOUNT:
+                _lib.BYTES[0] += gb.bytes[j][0]
+                _lib.BYTES[1] += gb.bytes[j][1]
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream(dev))
             V.append(Vbuf[j + 1])
@@ -475,7 +488,9 @@ def _gmres_pipelined(F, op, b, tol, max_iter, restart):
             for i in range(j + 1):
                 hcol[i] = vals[2 * i]
             norm_after = math.sqrt(vals[2 * (j + 1) + 1])
+            GATE_STATS[1] += 1
             if norm_after < 0.7071 * norm_before:
+                GATE_STATS[0] += 1
                 for i in range(j + 1):
                     hcol[i] += vals[o2 + 2 * i]
                 norm_after = math.sqrt(vals[o2 + 2 * (j + 1) + 1])

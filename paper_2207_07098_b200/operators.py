@@ -143,6 +143,7 @@ class GlobalOp:
                       _lib.ptr(self.inmask) if self.masked else None,
                       _lib.ptr(self.outsel) if self.masked else None, 2 if self.masked else 0,
                       *pl.launch_args(), _ex(), st)
+            gs.account_dssum()
             self.launches += 1
             return w
         if self.masked:

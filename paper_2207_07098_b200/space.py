@@ -26,7 +26,7 @@ import math
 import numpy as np
 import torch
 
-from . import _device, _lib
+from . import _device, _lib, traffic
 from .errors import ConfigError, GeometryError, TopologyError
 
 _FACE_NORMAL_SIGN = (-1.0, 1.0, 1.0, -1.0, -1.0, 1.0)
@@ -247,6 +247,9 @@ class GatherScatter:
         self.cls_n = (n[2], n[4], n[8])
         self.cls_gen_off = gen_off.to(torch.int32).contiguous()
         self.cls_n_gen = int(other.numel())
+        n_all = sum(int(t.numel()) for t in parts)
+        n_loc = sum(int((t < self.P).sum()) for t in parts)
+        self.dss_bytes = traffic.dssum_bytes(n_loc, n_all - n_loc, n[2] + n[4] + n[8] + self.cls_n_gen)
         # element-range blocks for sf_dssum_blk_f64: every class's items are ordered
         # by lowest local copy, so a block's items are one contiguous run per class
         E = self.shape[0]
@@ -394,6 +397,7 @@ class GatherScatter:
             self._build_classes()
         n2, n4, n8 = self.cls_n
         pm = self.cls_perm if perm is None else perm
+        self.account_dssum()
         if _DSSUM_KERNEL == "cls" and pre is None:
             _lib.call("sf_dssum_cls_f64", _lib.ptr(v), _lib.ptr(pm), n2, n4, n8, _lib.ptr(self.cls_gen_off),
                       self.cls_n_gen, mode, _lib.ptr(u), _lib.ptr(recv), self.P, _lib.stream_ptr(self.device))
@@ -401,6 +405,13 @@ class GatherScatter:
             _lib.call("sf_dssum_blk_f64", _lib.ptr(v), _lib.ptr(pm), n2, n4, n8, _lib.ptr(self.cls_gen_off),
                       _lib.ptr(self.cls_bstart), self.cls_nb, mode, _lib.ptr(u), _lib.ptr(pre), _lib.ptr(recv),
                       self.P, _lib.stream_ptr(self.device))
+
+    def account_dssum(self):
+        """Credit one dssum's algorithmic bytes to the step accounting (traffic.py)."""
+        if _lib.ACCOUNT:
+            if not hasattr(self, "cls_perm"):
+                self._build_classes()
+            _lib.BYTES[0] += self.dss_bytes
 
     def _dssum_rows(self, flat, mode, u=None):
         for row in range(flat.shape[0]):
