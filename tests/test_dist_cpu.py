@@ -27,7 +27,7 @@ def _space(oracle, counts=(3, 4, 5), order=4, perturb=True):
     return oracle.build_space(m, oracle.make_basis(order))
 
 
-@pytest.mark.parametrize("world", [2, 3, 5])
+@pytest.mark.parametrize("world", [2, 3, 5, 8])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_partitioned_dssum_is_bitwise_single_rank(oracle, world, mode):
     sp = _space(oracle)
@@ -107,8 +107,8 @@ def _worker(rank, world, port, payload, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_gloo_halo_exchange_world2(oracle, world):
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_halo_exchange(oracle, world):
     sp = _space(oracle, counts=(2, 3, 4), order=3)
     gs = sp.gs
     nnn = sp.n ** 3
@@ -134,7 +134,7 @@ def test_gloo_halo_exchange_world2(oracle, world):
     got = np.concatenate([res[r][0] for r in range(world)])
     assert np.array_equal(got, want)
     for r in range(world):
-        assert np.array_equal(res[r][1], np.array([3.0, 0.5]))
+        assert np.array_equal(res[r][1], np.array([world * (world + 1) / 2, 0.25 * world * (world - 1)]))
     assert starts[-1] == E
 
 
