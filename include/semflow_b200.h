@@ -208,7 +208,9 @@ int sf_mgs_step_f64(double* w, const double* vprev, const double* hprev, const d
 /* GMRES Arnoldi bookkeeping on the device (krylov.py:110-123): blk holds the
  * iteration's scalars (first sweep pairs at 2i, second sweep at o2 + 2i);
  * phase 0 writes blk[o3] = (norm_after < 0.7071 norm_before) and blk[o3+1] =
- * norm_after, phase 1 replaces blk[o3+1] by the second sweep's norm if blk[o3]. */
+ * norm_after, phase 1 replaces blk[o3+1] by the second sweep's norm if blk[o3];
+ * phase 2 is phase 0 plus blk[o2] = blk[2(j+1)] (the first sweep's last pass
+ * also computed <w, v_0>, the second sweep's first coefficient). */
 int sf_gmres_gate_f64(double* blk, int j, int o2, int o3, int phase, void* stream);
 
 /* x = x0 + sum_i coef[i] * M v[i] accumulated in i order; v is a DEVICE array

@@ -378,14 +378,19 @@ int mgs_step(double* w, const double* vprev, const double* hprev, const double* 
 // at o2 + 2i, and [o3] = reorthogonalise flag, [o3+1] = final norm.
 //   phase 0: flag = sqrt(na2) < 0.7071 * sqrt(nb2); norm = sqrt(na2)
 //   phase 1: if flag, norm = sqrt(na2 of the second sweep)
+//   phase 2: phase 0, and the second sweep's first coefficient <w, v_0> is taken
+//            from [2(j+1)], where the first sweep's last pass left it (that pass
+//            also dotted the updated w with v_0: the same per-point products and
+//            reduction tree as a separate pass, one read of w fewer)
 // (IEEE sqrt and the same comparison the host evaluates: identical decision.)
 __global__ void gmres_gate_kernel(double* blk, int j, int o2, int o3, int phase) {
   if (threadIdx.x != 0) return;
-  if (phase == 0) {
+  if (phase == 0 || phase == 2) {
     const double nb = sqrt(blk[1]);
     const double na = sqrt(blk[2 * (j + 1) + 1]);
     blk[o3] = (na < 0.7071 * nb) ? 1.0 : 0.0;
     blk[o3 + 1] = na;
+    if (phase == 2) blk[o2] = blk[2 * (j + 1)];
   } else if (blk[o3] != 0.0) {
     blk[o3 + 1] = sqrt(blk[o2 + 2 * (j + 1) + 1]);
   }

@@ -446,10 +446,13 @@ def _gmres_pipelined(F, op, b, tol, max_iter, restart):
         for i in range(1, j + 1):
             F.mgs(bl[2 * i:2 * i + 2], _lib.ptr(w), _lib.ptr(V[i - 1]), bp(2 * (i - 1)), _lib.ptr(V[i]),
                   None, None, mult, 0)
-        F.mgs(bl[2 * (j + 1):2 * (j + 2)], _lib.ptr(w), _lib.ptr(V[j]), bp(2 * j), None, None, None, mult, 1)
-        _lib.call("sf_gmres_gate_f64", bl.data_ptr(), j, o2, o3, 0, F.st)
+        # the first sweep's last pass also dots the updated w with v_0: the second
+        # sweep's first coefficient (bit-identical to a separate pass, which
+        # would re-read w), moved into place by the gate kernel (phase 2)
+        F.mgs(bl[2 * (j + 1):2 * (j + 2)], _lib.ptr(w), _lib.ptr(V[j]), bp(2 * j), _lib.ptr(V[0]), None, None,
+              mult, 1)
+        _lib.call("sf_gmres_gate_f64", bl.data_ptr(), j, o2, o3, 2, F.st)
         g8 = bp(o3)
-        F.mgs(bl[o2:o2 + 2], _lib.ptr(w), None, None, _lib.ptr(V[0]), None, None, mult, 0, gate=g8)
         for i in range(1, j + 1):
             F.mgs(bl[o2 + 2 * i:o2 + 2 * i + 2], _lib.ptr(w), _lib.ptr(V[i - 1]), bp(o2 + 2 * (i - 1)),
                   _lib.ptr(V[i]), None, None, mult, 0, gate=g8)
