@@ -12,7 +12,11 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2207_07098_b200", "variants")
-VARIANTS = {}   # e.g. {"minb5": "-DSF_AX8S_MINB=5"}: MINB 3/5 and unroll 1/4 measured slower
+# e.g. {"minb5": "-DSF_AX8S_MINB=5"}: MINB 3/5 and unroll 1/4 measured slower; so
+# was a register-resident r-flux (f1 contracted into 8 per-thread accumulators as
+# each layer is formed, bit-identical output): 275 / 255 (unroll 1) vs 234 us
+# masked at 32^3, 2141 vs 1774 us at 64^3
+VARIANTS = {}
 
 
 def build():
@@ -52,7 +56,8 @@ def run(ne):
     P = sp.n_points
     gs = sp.gs
     paths = [_lib.LIB_PATH] if os.environ.get("AX_MAIN_ONLY") else \
-        sorted(glob.glob(os.path.join(VDIR, "lib_*.so"))) + [_lib.LIB_PATH]
+        [_lib.LIB_PATH] + sorted(glob.glob(os.path.join(VDIR, "lib_*.so")))
+    ref_out = {}   # the main library's outputs: every variant must match them bit for bit
     for path in paths:
         L = ctypes.CDLL(path)
         for name, args in _lib._SIGS.items():
@@ -89,6 +94,12 @@ def run(ne):
             for _ in range(3):
                 fn()
             torch.cuda.synchronize()
+            if kind in ("masked", "plain", "helm"):
+                if kind not in ref_out:
+                    ref_out[kind] = w.clone()
+                elif not torch.equal(ref_out[kind], w):
+                    print("   ", kind, "MISMATCH vs main library, max diff",
+                          float((ref_out[kind] - w).abs().max()), flush=True)
             err = L.sf_last_error()
             if err:
                 print("   ", kind, "error:", err)
