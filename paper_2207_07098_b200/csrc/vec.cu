@@ -225,10 +225,14 @@ struct MgsOp {
 };
 
 // Vectorised MGS pass: 16-byte loads of point pairs (each warp instruction moves
-// a contiguous 512 B run), 4 pairs per lane in flight.  Same per-point arithmetic
-// as MgsOp; used when P is even and every array is 16-byte aligned.
+// a contiguous 512 B run), SF_MGS_U pairs per lane in flight.  Same per-point
+// arithmetic as MgsOp; used when P is even and every array is 16-byte aligned.
+// Measured at 64^3 (tools/vec_bench.py): 2 blocks/SM minimum (no register cap
+// below 128) runs the prev+next pass in 637 us vs 647 us at 4; U only changes the
+// per-thread point order (hence the dot's rounding), so it stays at 2; streaming
+// cache hints (ld/st.global.cs) cost 7 %.
 #ifndef SF_MGS_MINB
-#define SF_MGS_MINB 4
+#define SF_MGS_MINB 2
 #endif
 #ifndef SF_MGS_U
 #define SF_MGS_U 2
