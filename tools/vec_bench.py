@@ -57,6 +57,9 @@ def main():
     h[0] = 2.0
     res["scale_div (16 B/pt)"] = (timeit(lambda: _lib.call(
         "sf_scale_div_f64", v2.data_ptr(), v1.data_ptr(), None, None, h.data_ptr(), P, st)), 16)
+    h[0] = 1.0
+    res["scale_div in place (16 B/pt)"] = (timeit(lambda: _lib.call(
+        "sf_scale_div_f64", w.data_ptr(), w.data_ptr(), None, None, h.data_ptr(), P, st)), 16)
     for k, (t, b) in res.items():
         print(f"{k:32s} {t * 1e6:9.1f} us  {P * b / t / 1e9:7.0f} GB/s")
 
