@@ -506,6 +506,10 @@ def bench_tgv(args, world, rank, dev):
         P = ne ** 3 * sp.n ** 3            # global points: strong scaling, fixed total work
     for _ in range(args.warmup):
         state, d = st.step(state)
+    # the projection bases grow by one (x, Ax) pair per solve: reserve the timed
+    # steps' slots up front (setup-time allocation, as Neko's projection init)
+    if not args.no_reserve:
+        st.reserve_projection(args.steps)
     stream = torch.cuda.current_stream()
     # one timed loop gives both numbers over the SAME K steps:
     #   value: device time of each step (CUDA events on the launching stream),
@@ -635,6 +639,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--no-reserve", action="store_true",
+                    help="grow the projection bases inside the timed steps (A/B of the slot reservation)")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--workload", default="tgv", choices=("tgv", "poisson", "channel", "cylinder"))
     ap.add_argument("--ne", type=int, default=0)

@@ -637,6 +637,22 @@ class ProjectionSpace:
         self.xs = []
         self.axs = []
         self._solves = 0
+        self._slots = []
+
+    def reserve(self, like, pairs):
+        """Preallocate `pairs` (x, Ax) basis slots shaped like `like`; `absorb` fills
+        them before growing the device heap.  Neko allocates its projection basis at
+        init; growing it inside the time loop costs one multi-GB cudaMalloc per new
+        vector (tens of ms of host time each at 64^3, with the device idle)."""
+        for _ in range(int(pairs)):
+            self._slots.append((torch.empty_like(like), torch.empty_like(like)))
+
+    def _slot(self, like):
+        while self._slots:
+            x, ax = self._slots.pop()
+            if x.shape == like.shape and x.dtype == like.dtype and x.device == like.device:
+                return x, ax
+        return torch.empty_like(like), torch.empty_like(like)
 
     @property
     def count(self):
@@ -722,8 +738,7 @@ class ProjectionSpace:
             return
         nrm = math.sqrt(nrm2)
         s[0:1].fill_(nrm)
-        xn = torch.empty_like(d)
-        axn = torch.empty_like(ad)
+        xn, axn = self._slot(d)
         _lib.call("sf_scale_div_f64", _lib.ptr(xn), _lib.ptr(d), _lib.ptr(axn), _lib.ptr(ad), sp(0), F.P, F.st)
         self.xs.append(xn)
         self.axs.append(axn)

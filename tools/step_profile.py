@@ -30,6 +30,7 @@ def main():
     torch.cuda.synchronize()
     from torch.profiler import ProfilerActivity, profile
 
+    m0 = torch.cuda.memory_stats()
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         for _ in range(steps):
             state, d = st.step(state)
@@ -38,6 +39,9 @@ def main():
         torch.cuda.synchronize()
     if comm.rank != 0:
         return
+    m1 = torch.cuda.memory_stats()
+    print("allocator over the profiled steps:", {k: m1.get(k, 0) - m0.get(k, 0) for k in
+          ("num_device_alloc", "num_device_free", "num_alloc_retries", "num_sync_all_streams")})
     agg = {}
     total = 0.0
     for ev in prof.events():
@@ -52,6 +56,26 @@ def main():
     print(f"total device time {total / 1e3:.2f} ms over {steps} step(s), {sum(v[1] for v in agg.values())} kernels")
     for name, (t, n) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:25]:
         print(f"{t / 1e3:10.3f} ms {100 * t / total:6.1f}%  {n:6d}x  {t / n:9.1f} us  {name}")
+    # device idle gaps between consecutive kernels (host-side stalls)
+    spans = sorted((ev.time_range.start, ev.time_range.end, ev.name.split("(")[0][:50])
+                   for ev in prof.events() if ev.device_type.name == "CUDA")
+    gaps = []
+    for a, b in zip(spans, spans[1:]):
+        g = b[0] - max(a[1], 0)
+        if g > 0:
+            gaps.append((g, a[2], b[2]))
+    if spans:
+        busy_span = spans[-1][1] - spans[0][0]
+        print(f"device span {busy_span / 1e3:.2f} ms, idle {sum(g for g, _, _ in gaps) / 1e3:.2f} ms "
+              f"in {len(gaps)} gaps ({sum(g for g, _, _ in gaps if g > 100) / 1e3:.2f} ms in gaps > 100 us)")
+        by = {}
+        for g, a, b in gaps:
+            k = (a, b)
+            c = by.setdefault(k, [0.0, 0])
+            c[0] += g
+            c[1] += 1
+        for (a, b), (t, n) in sorted(by.items(), key=lambda kv: -kv[1][0])[:15]:
+            print(f"  gap {t / 1e3:8.2f} ms {n:5d}x  after {a}  before {b}")
 
 
 if __name__ == "__main__":
