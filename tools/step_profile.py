@@ -30,6 +30,9 @@ def main():
     torch.cuda.synchronize()
     from torch.profiler import ProfilerActivity, profile
 
+    if os.environ.get("RESERVE", "1") == "1":
+        st.reserve_projection(steps)     # as bench.py does after its warm-up
+    torch.cuda.synchronize()
     m0 = torch.cuda.memory_stats()
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         for _ in range(steps):
