@@ -59,6 +59,8 @@ def main():
     print(f"total device time {total / 1e3:.2f} ms over {steps} step(s), {sum(v[1] for v in agg.values())} kernels")
     for name, (t, n) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:25]:
         print(f"{t / 1e3:10.3f} ms {100 * t / total:6.1f}%  {n:6d}x  {t / n:9.1f} us  {name}")
+    if os.environ.get("CPU_TABLE", "0") == "1":
+        print(prof.key_averages().table(sort_by="self_cpu_time_total", row_limit=20))
     # device idle gaps between consecutive kernels (host-side stalls)
     spans = sorted((ev.time_range.start, ev.time_range.end, ev.name.split("(")[0][:50])
                    for ev in prof.events() if ev.device_type.name == "CUDA")
