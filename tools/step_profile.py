@@ -34,6 +34,8 @@ def main():
         st.reserve_projection(steps)     # as bench.py does after its warm-up
     torch.cuda.synchronize()
     m0 = torch.cuda.memory_stats()
+    if os.environ.get("MEMHIST", "0") == "1":
+        torch.cuda.memory._record_memory_history(max_entries=200000)
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         for _ in range(steps):
             state, d = st.step(state)
@@ -43,6 +45,14 @@ def main():
     if comm.rank != 0:
         return
     m1 = torch.cuda.memory_stats()
+    if os.environ.get("MEMHIST", "0") == "1":
+        snap = torch.cuda.memory._snapshot()
+        for tr in snap["device_traces"]:
+            for e in tr:
+                if e["action"] == "segment_alloc":
+                    fr = [f"{f['filename'].split('/')[-1]}:{f['line']}:{f['name']}" for f in e.get("frames", [])
+                          if "paper_2207" in f["filename"] or "step_profile" in f["filename"]]
+                    print(f"segment_alloc {e['size'] / 2**30:.3f} GiB <- {' < '.join(fr[:6])}")
     print("allocator over the profiled steps:", {k: m1.get(k, 0) - m0.get(k, 0) for k in
           ("num_device_alloc", "num_device_free", "num_alloc_retries", "num_sync_all_streams")})
     agg = {}
