@@ -134,10 +134,14 @@ int sf_dssum_cls_f64(double* v, const int* perm, int n2, int n4, int n8, const i
  * item offsets, one row per class (pairs, quads, octets, generic), each relative
  * to its class.  Same modes, flags, halo convention and per-gid order as
  * sf_dssum_f64 (bit-identical results).  pre (optional, mode 2): masked copies
- * receive pre[p] * u[p] -- the input of an operator applied by sf_ax_pre_f64. */
+ * receive pre[p] * u[p] -- the input of an operator applied by sf_ax_pre_f64.
+ * recv_seq (optional, device): the receive buffer is double-banked (NVLink halo
+ * inbox, sf_halo_put_f64) and the copies are read from
+ * recv + (*recv_seq & 1) * recv_bank -- the bank of the current exchange. */
 int sf_dssum_blk_f64(double* v, const int* perm, int n2, int n4, int n8, const int* gen_offsets,
                      const int* block_start, int n_blocks, int mode, const double* u, const double* pre,
-                     const double* recv, int n_local, void* stream);
+                     const double* recv, int n_local, const unsigned long long* recv_seq,
+                     long long recv_bank, void* stream);
 
 /* Ax_helm of the Jacobi-scaled vector pre .* u without materialising it
  * (`z = precond(v); w = apply_a(z)`, krylov.py:106-107 with BlockJacobi,
@@ -267,9 +271,12 @@ int sf_ipc_open_handle(const unsigned char* handle, void** dev_ptr_out);
 int sf_ipc_close_handle(void* dev_ptr);
 /* out[0..k) = sum over ranks (rank order) of every rank's in[0..k), k <= 4.
  * boxes: HOST array of `world` mailbox pointers (own + IPC-opened peers);
- * seq: call number, strictly increasing by 1 per call on every rank; error: device
- * flag set to 1 if a peer did not arrive within 5 s.  in and out may alias. */
-int sf_peer_allreduce_f64(double* const* boxes, int world, int rank, unsigned long long seq,
+ * seq: DEVICE uint64 counting the reductions this rank has executed (zero
+ * before the first; each call exchanges *seq + 1 and advances it, so a gated
+ * pass that skips consumes no number and graph-captured calls stay in step);
+ * error: device flag set to 1 if a peer did not arrive within 5 s -- then out is
+ * NaN, and every later call returns NaN at once.  in and out may alias. */
+int sf_peer_allreduce_f64(double* const* boxes, int world, int rank, unsigned long long* seq,
                           unsigned* error, const double* in, int k, double* out, void* stream);
 
 /* Fused compute + collective: sf_mgs_step_f64 / the weighted glsc3 whose last
@@ -279,31 +286,35 @@ int sf_peer_allreduce_f64(double* const* boxes, int world, int rank, unsigned lo
 int sf_mgs_step_peer_f64(double* w, const double* vprev, const double* hprev, const double* vnext,
                          double* w2, const double* v2prev, const uint8_t* mult, int want_norm,
                          long long P, double* partials, unsigned* counter, double* out,
-                         double* const* boxes, int world, int rank, unsigned long long seq,
+                         double* const* boxes, int world, int rank, unsigned long long* seq,
                          unsigned* error, const double* gate, void* stream);
 int sf_glsc3_peer_f64(const double* a, const double* b, const uint8_t* mult, long long P,
                       double* partials, unsigned* counter, double* out, double* const* boxes,
-                      int world, int rank, unsigned long long seq, unsigned* error, void* stream);
+                      int world, int rank, unsigned long long* seq, unsigned* error, void* stream);
 
 /* NVLink halo exchange of the multi-GPU dssum (replaces the NCCL send/recv of
  * the interface copies; SURVEY 8e collective C1).  Each rank owns an IPC-exported
  * inbox of sf_halo_inbox_doubles(n_recv) doubles: 32 header doubles (uint64 flag
  * per sender rank), then two banks of n_recv values (bank = seq & 1) laid out as
- * the dssum's receive buffer.
+ * the dssum's receive buffer.  Header word 16 is the rank's exchange counter
+ * (device memory, zero at allocation): the call number seq = counter + 1.
  *   sf_halo_put_f64: v[send_idx[i]] for peer q's segment [seg[q], seg[q+1]) is
  *     stored at peer_dst[q][bank * peer_stride[q] + i - seg[q]] (NVLink stores);
- *     after a system-scope fence the last block writes seq to peer_flag[q]
- *     (release).  counter: a zeroed device uint32, re-armed by the kernel.
+ *     after a system-scope fence the last block advances own_inbox's counter and
+ *     writes seq to peer_flag[q] (release).  counter: a zeroed device uint32,
+ *     re-armed by the kernel.  No-op once *error is set.
  *   sf_halo_wait: one warp waits (acquire) until own_flags[peer_rank[q]] >= seq
  *     for every peer; sets *error after 5 s instead of hanging.
- * Both are stream-ordered; the dssum that follows reads the inbox bank. */
+ * Both are stream-ordered and take the same arguments on every call (CUDA-graph
+ * capturable); the dssum that follows reads the bank through recv_seq. */
 int sf_halo_inbox_doubles(long long n_recv);
+int sf_halo_header_doubles(void);
 int sf_halo_put_f64(const double* v, const int* send_idx, int n_peers, const int* peer_rank,
                     const long long* seg, double* const* peer_dst, const long long* peer_stride,
-                    unsigned long long* const* peer_flag, unsigned long long seq, unsigned* counter,
-                    void* stream);
+                    unsigned long long* const* peer_flag, unsigned long long* own_inbox,
+                    unsigned* counter, const unsigned* error, void* stream);
 int sf_halo_wait(const unsigned long long* own_flags, int n_peers, const int* peer_rank,
-                 unsigned long long seq, unsigned* error, void* stream);
+                 unsigned* error, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Function-space setup (space.py:182-245), bit-identical to build_space

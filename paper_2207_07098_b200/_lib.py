@@ -34,7 +34,7 @@ _SIGS = {
     "sf_ax_masked_f64": [_vp, _i, _vp, _vp, _vp, _vp, _ll, _d, _d, _vp, _vp, _i, _vp],
     "sf_dssum_f64": [_vp, _vp, _vp, _i, _i, _vp, _vp, _i, _vp],
     "sf_dssum_cls_f64": [_vp, _vp, _i, _i, _i, _vp, _i, _i, _vp, _vp, _i, _vp],
-    "sf_dssum_blk_f64": [_vp, _vp, _i, _i, _i, _vp, _vp, _i, _i, _vp, _vp, _vp, _i, _vp],
+    "sf_dssum_blk_f64": [_vp, _vp, _i, _i, _i, _vp, _vp, _i, _i, _vp, _vp, _vp, _i, _vp, _ll, _vp],
     "sf_ax_pre_f64": [_vp, _i, _vp, _vp, _vp, _vp, _vp, _ll, _d, _d, _vp, _vp, _i, _vp],
     "sf_ax_range_f64": [_vp, _i, _vp, _vp, _vp, _vp, _vp, _ll, _ll, _ll, _d, _d, _vp, _vp, _i, _vp],
     "sf_ax_dssum8_f64": [_vp, _vp, _vp, _vp, _vp, _ll, _d, _d, _vp, _vp, _i, _vp, _vp, _vp,
@@ -61,13 +61,14 @@ _SIGS = {
     "sf_ipc_get_handle": [_vp, ctypes.c_char_p],
     "sf_ipc_open_handle": [ctypes.c_char_p, ctypes.POINTER(_vp)],
     "sf_ipc_close_handle": [_vp],
-    "sf_peer_allreduce_f64": [_vp, _i, _i, ctypes.c_ulonglong, _vp, _vp, _i, _vp, _vp],
+    "sf_peer_allreduce_f64": [_vp, _i, _i, _vp, _vp, _vp, _i, _vp, _vp],
     "sf_mgs_step_peer_f64": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _ll, _vp, _vp, _vp,
-                             _vp, _i, _i, ctypes.c_ulonglong, _vp, _vp, _vp],
-    "sf_glsc3_peer_f64": [_vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp, _i, _i, ctypes.c_ulonglong, _vp, _vp],
+                             _vp, _i, _i, _vp, _vp, _vp, _vp],
+    "sf_glsc3_peer_f64": [_vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp],
     "sf_halo_inbox_doubles": [_ll],
-    "sf_halo_put_f64": [_vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, ctypes.c_ulonglong, _vp, _vp],
-    "sf_halo_wait": [_vp, _i, _vp, ctypes.c_ulonglong, _vp, _vp],
+    "sf_halo_header_doubles": [],
+    "sf_halo_put_f64": [_vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "sf_halo_wait": [_vp, _i, _vp, _vp, _vp],
     "sf_trilinear_coords_f64": [_vp, _vp, _i, _ll, _vp, _vp],
     "sf_metrics_f64": [_vp, _vp, _i, _vp, _ll, _vp, _vp, _vp, _vp, _vp],
 }

@@ -51,7 +51,7 @@ int rank_sum(const double*, int, int, double*, cudaStream_t);
 int ax_helm8_range(const double*, const double*, const double*, const double*, const double*, double*, long long,
                    long long, long long, double, double, const uint32_t*, const uint32_t*, int, cudaStream_t);
 int dssum_blk(double*, const int*, int, int, int, const int*, const int*, int, int, const double*,
-              const double*, const double*, int, cudaStream_t);
+              const double*, const double*, int, const unsigned long long*, long long, cudaStream_t);
 int ax_dssum8(const double*, const double*, const double*, const double*, double*, long long, double,
               double, const uint32_t*, const uint32_t*, int, const int*, const long long*,
               unsigned long long*, unsigned long long, int, cudaStream_t);
@@ -177,9 +177,10 @@ int sf_dssum_cls_f64(double* v, const int* perm, int n2, int n4, int n8, const i
 
 int sf_dssum_blk_f64(double* v, const int* perm, int n2, int n4, int n8, const int* gen_offsets,
                      const int* block_start, int n_blocks, int mode, const double* u, const double* pre,
-                     const double* recv, int n_local, void* stream) {
+                     const double* recv, int n_local, const unsigned long long* recv_seq,
+                     long long recv_bank, void* stream) {
   return dssum_blk(v, perm, n2, n4, n8, gen_offsets, block_start, n_blocks, mode, u, pre, recv, n_local,
-                   as_stream(stream));
+                   recv_seq, recv_bank, as_stream(stream));
 }
 
 int sf_ax_dssum8_f64(const double* d_host, const double* g, const double* b, const double* u,
@@ -234,7 +235,7 @@ int sf_gmres_gate_f64(double* blk, int j, int o2, int o3, int phase, void* strea
   return gmres_gate(blk, j, o2, o3, phase, as_stream(stream));
 }
 
-static int make_peer(PeerCtx& c, double* const* boxes, int world, int rank, unsigned long long seq,
+static int make_peer(PeerCtx& c, double* const* boxes, int world, int rank, unsigned long long* seq,
                      unsigned* error) {
   if (world < 1 || world > PEER_MAX_RANKS || rank < 0 || rank >= world) {
     set_error("peer context: bad world/rank %d/%d", world, rank);
@@ -252,7 +253,7 @@ static int make_peer(PeerCtx& c, double* const* boxes, int world, int rank, unsi
 int sf_mgs_step_peer_f64(double* w, const double* vprev, const double* hprev, const double* vnext,
                          double* w2, const double* v2prev, const uint8_t* mult, int want_norm,
                          long long P, double* partials, unsigned* counter, double* out,
-                         double* const* boxes, int world, int rank, unsigned long long seq,
+                         double* const* boxes, int world, int rank, unsigned long long* seq,
                          unsigned* error, const double* gate, void* stream) {
   PeerCtx c;
   int st = make_peer(c, boxes, world, rank, seq, error);
@@ -263,7 +264,7 @@ int sf_mgs_step_peer_f64(double* w, const double* vprev, const double* hprev, co
 
 int sf_glsc3_peer_f64(const double* a, const double* b, const uint8_t* mult, long long P,
                       double* partials, unsigned* counter, double* out, double* const* boxes,
-                      int world, int rank, unsigned long long seq, unsigned* error, void* stream) {
+                      int world, int rank, unsigned long long* seq, unsigned* error, void* stream) {
   PeerCtx c;
   int st = make_peer(c, boxes, world, rank, seq, error);
   if (st != SF_OK) return st;

@@ -185,8 +185,12 @@ __global__ void __launch_bounds__(256)
 dssum_blk_kernel(double* __restrict__ v, const int* __restrict__ perm, int n2, int n4, int n8,
                  const int* __restrict__ gen_off, const int* __restrict__ bstart, int nb,
                  const double* __restrict__ u, const double* __restrict__ pre,
-                 const double* __restrict__ recv, int n_local) {
+                 const double* __restrict__ recv, int n_local,
+                 const unsigned long long* __restrict__ recv_seq, long long recv_bank) {
   const int b = blockIdx.x;
+  // NVLink halo inbox: the bank of the current exchange is chosen by the call
+  // number in device memory (halo.cu), so the launch arguments never change
+  if (recv_seq != nullptr) recv += (long long)(*recv_seq & 1ull) * recv_bank;
   const int2* p2 = reinterpret_cast<const int2*>(perm);
   const int4* p4 = reinterpret_cast<const int4*>(perm + pairs_span(n2));
   const int4* p8 = reinterpret_cast<const int4*>(perm + pairs_span(n2) + 4LL * n4);
@@ -339,15 +343,18 @@ int dssum_cls(double* v, const int* perm, int n2, int n4, int n8, const int* gen
 
 int dssum_blk(double* v, const int* perm, int n2, int n4, int n8, const int* gen_off, const int* bstart,
               int nb, int mode, const double* u, const double* pre, const double* recv, int n_local,
-              cudaStream_t st) {
+              const unsigned long long* recv_seq, long long recv_bank, cudaStream_t st) {
   if (nb <= 0) return SF_OK;
-  if (recv == nullptr) n_local = 0x7fffffff;
+  if (recv == nullptr) {
+    n_local = 0x7fffffff;
+    recv_seq = nullptr;
+  }
   switch (mode) {
-    case 0: dssum_blk_kernel<0><<<nb, 256, 0, st>>>(v, perm, n2, n4, n8, gen_off, bstart, nb, nullptr, nullptr, recv, n_local); break;
-    case 1: dssum_blk_kernel<1><<<nb, 256, 0, st>>>(v, perm, n2, n4, n8, gen_off, bstart, nb, nullptr, nullptr, recv, n_local); break;
+    case 0: dssum_blk_kernel<0><<<nb, 256, 0, st>>>(v, perm, n2, n4, n8, gen_off, bstart, nb, nullptr, nullptr, recv, n_local, recv_seq, recv_bank); break;
+    case 1: dssum_blk_kernel<1><<<nb, 256, 0, st>>>(v, perm, n2, n4, n8, gen_off, bstart, nb, nullptr, nullptr, recv, n_local, recv_seq, recv_bank); break;
     case 2:
       if (u == nullptr) { set_error("dssum_blk: masked mode needs u"); return SF_ERR_ARG; }
-      dssum_blk_kernel<2><<<nb, 256, 0, st>>>(v, perm, n2, n4, n8, gen_off, bstart, nb, u, pre, recv, n_local);
+      dssum_blk_kernel<2><<<nb, 256, 0, st>>>(v, perm, n2, n4, n8, gen_off, bstart, nb, u, pre, recv, n_local, recv_seq, recv_bank);
       break;
     default: set_error("dssum_blk: bad mode %d", mode); return SF_ERR_ARG;
   }

@@ -18,13 +18,21 @@
 // order on the peer).  The summation order of the dssum is unchanged, so the
 // result is bitwise the same as with NCCL.
 //
-// Inbox layout (doubles): [flags: PEER_MAX_RANKS uint64][pad to 32][bank 0:
-// n_recv][bank 1: n_recv]; rank r's data goes at its recv offset in each bank.
+// The call number lives in DEVICE memory (a word in the rank's own inbox header,
+// advanced by the put's last block), not in a kernel argument: halo_wait and the
+// dssum read it to pick the flag value and the bank.  Kernel arguments are then
+// identical from call to call, so an operator application that contains an
+// exchange can be captured once in a CUDA graph and replayed.
+//
+// Inbox layout (doubles): [flags: PEER_MAX_RANKS uint64][call number at
+// HALO_SEQ][pad to 32][bank 0: n_recv][bank 1: n_recv]; rank r's data goes at its
+// recv offset in each bank.
 #include "peer.cuh"
 
 namespace sf {
 
 constexpr int HALO_HEADER = 32;  // doubles before bank 0
+constexpr int HALO_SEQ = 16;     // header word holding the rank's call number
 
 struct HaloPeers {
   int n;                                        // peers
@@ -36,8 +44,13 @@ struct HaloPeers {
 };
 
 __global__ void halo_put_kernel(const double* __restrict__ v, const int* __restrict__ send_idx,
-                                HaloPeers hp, int bank, unsigned long long seq,
-                                unsigned* __restrict__ counter) {
+                                HaloPeers hp, unsigned long long* __restrict__ seqp,
+                                unsigned* __restrict__ counter, const unsigned* __restrict__ error) {
+  // after a peer failure every exchange is a no-op (the host raises at its next check)
+  if (*(volatile const unsigned*)error != 0u) return;
+  // every block reads the call number before the last block advances it
+  const unsigned long long seq = *(volatile const unsigned long long*)seqp + 1ull;
+  const int bank = (int)(seq & 1ull);
   const long long total = hp.start[hp.n];
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -50,6 +63,7 @@ __global__ void halo_put_kernel(const double* __restrict__ v, const int* __restr
   if (threadIdx.x == 0) {
     if (atomicAdd(counter, 1u) == gridDim.x - 1u) {
       *counter = 0u;  // rearm for the next call on this stream
+      *seqp = seq;
       __threadfence_system();
       for (int q = 0; q < hp.n; ++q) st_release_sys(hp.flag[q], seq);
     }
@@ -57,8 +71,10 @@ __global__ void halo_put_kernel(const double* __restrict__ v, const int* __restr
 }
 
 __global__ void halo_wait_kernel(const unsigned long long* __restrict__ flags, HaloPeers hp,
-                                 unsigned long long seq, unsigned* __restrict__ error) {
+                                 unsigned* __restrict__ error) {
   const int lane = threadIdx.x;
+  if (*(volatile const unsigned*)error != 0u) return;
+  const unsigned long long seq = *(volatile const unsigned long long*)(flags + HALO_SEQ);
   bool ok = true;
   if (lane < hp.n) {
     const unsigned long long* f = flags + hp.rank[lane];
@@ -76,16 +92,19 @@ extern "C" {
 
 int sf_halo_inbox_doubles(long long n_recv) { return (int)(sf::HALO_HEADER + 2 * n_recv); }
 
-// Push this rank's interface copies to every peer and publish `seq`.
+int sf_halo_header_doubles(void) { return sf::HALO_HEADER; }
+
+// Push this rank's interface copies to every peer and publish the next call
+// number (own_inbox[HALO_SEQ] + 1, advanced in device memory).
 //   send_idx: concatenated local indices, peer q's segment = [seg[q], seg[q+1])
 //   peer_rank / peer_dst / peer_stride / peer_flag: per peer (n_peers <= 8)
 int sf_halo_put_f64(const double* v, const int* send_idx, int n_peers, const int* peer_rank,
                     const long long* seg, double* const* peer_dst, const long long* peer_stride,
-                    unsigned long long* const* peer_flag, unsigned long long seq, unsigned* counter,
-                    void* stream) {
+                    unsigned long long* const* peer_flag, unsigned long long* own_inbox, unsigned* counter,
+                    const unsigned* error, void* stream) {
   using namespace sf;
   if (n_peers <= 0) return SF_OK;
-  if (n_peers > PEER_MAX_RANKS || !v || !send_idx || !counter) {
+  if (n_peers > PEER_MAX_RANKS || !v || !send_idx || !counter || !own_inbox || !error) {
     set_error("sf_halo_put_f64: bad arguments (n_peers=%d)", n_peers);
     return SF_ERR_ARG;
   }
@@ -104,14 +123,15 @@ int sf_halo_put_f64(const double* v, const int* send_idx, int n_peers, const int
   long long blocks = (total + 255) / 256;
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 4) blocks = 148 * 4;
-  halo_put_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(v, send_idx, hp, (int)(seq & 1ull), seq,
-                                                                  counter);
+  halo_put_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(v, send_idx, hp, own_inbox + HALO_SEQ,
+                                                                  counter, error);
   return check_launch("halo_put");
 }
 
-// Wait (on the stream) until every peer published `seq` into this rank's flags.
+// Wait (on the stream) until every peer published the current call number
+// (own_flags[HALO_SEQ], advanced by this rank's put) into this rank's flags.
 int sf_halo_wait(const unsigned long long* own_flags, int n_peers, const int* peer_rank,
-                 unsigned long long seq, unsigned* error, void* stream) {
+                 unsigned* error, void* stream) {
   using namespace sf;
   if (n_peers <= 0) return SF_OK;
   if (n_peers > PEER_MAX_RANKS || !own_flags || !error) {
@@ -122,7 +142,7 @@ int sf_halo_wait(const unsigned long long* own_flags, int n_peers, const int* pe
   std::memset(&hp, 0, sizeof(hp));
   hp.n = n_peers;
   for (int q = 0; q < n_peers; ++q) hp.rank[q] = peer_rank[q];
-  halo_wait_kernel<<<1, 32, 0, as_stream(stream)>>>(own_flags, hp, seq, error);
+  halo_wait_kernel<<<1, 32, 0, as_stream(stream)>>>(own_flags, hp, error);
   return check_launch("halo_wait");
 }
 

@@ -99,7 +99,7 @@ int sf_ipc_close_handle(void* dev_ptr) {
   return sf::SF_OK;
 }
 
-int sf_peer_allreduce_f64(double* const* boxes, int world, int rank, unsigned long long seq,
+int sf_peer_allreduce_f64(double* const* boxes, int world, int rank, unsigned long long* seq,
                           unsigned* error, const double* in, int k, double* out, void* stream) {
   if (world < 1 || world > PEER_MAX_RANKS || rank < 0 || rank >= world) {
     sf::set_error("sf_peer_allreduce_f64: bad world/rank %d/%d", world, rank);

@@ -500,11 +500,13 @@ struct ScaleDivOp {
 
 // Vectorised y = x / s (and y2 = x2 / s): 16-byte pair loads/stores, a warp
 // moves contiguous 512 B runs, SD_U pairs per lane in flight; the same IEEE
-// division per point as ScaleDivOp.
+// division per point as ScaleDivOp.  GMRES normalises in place (y == x), so the
+// vector pointers carry no __restrict__ (each thread loads its pairs before it
+// stores them, which is all in-place use needs).
 constexpr int SD_U = 2;
 __global__ void __launch_bounds__(RED_THREADS)
-scale_div2_kernel(double2* __restrict__ y, const double2* __restrict__ x, double2* __restrict__ y2,
-                  const double2* __restrict__ x2, const double* __restrict__ s, long long P2) {
+scale_div2_kernel(double2* y, const double2* x, double2* y2, const double2* x2,
+                  const double* __restrict__ s, long long P2) {
   const double sv = *s;
   const int lane = threadIdx.x & 31;
   const long long gwarp = ((long long)blockIdx.x * RED_THREADS + threadIdx.x) >> 5;

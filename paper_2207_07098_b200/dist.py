@@ -164,23 +164,31 @@ class _PeerReducer:
             ptrs.append(p.value)
         self.boxes = (ctypes.c_void_p * comm.world)(*ptrs)
         self.error = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        self.seq = 0
+        # reductions executed so far, advanced on the device by each call that
+        # really exchanges (a gated pass that skips leaves it alone): the call
+        # number and the mailbox bank are never kernel arguments, so every call
+        # has the same arguments and graph-captured reductions stay in step
+        self.seq = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.calls = 0          # host count of enqueued reductions (statistics only)
         torch.cuda.synchronize()
         comm.dist.barrier(group=comm.group)
 
     def fused_args(self):
         """(boxes, world, rank, seq, error) for one fused kernel+collective call."""
-        self.seq += 1
-        return (self.boxes, self.comm.world, self.comm.rank, self.seq, _lib.ptr(self.error))
+        self.calls += 1
+        return (self.boxes, self.comm.world, self.comm.rank, _lib.ptr(self.seq), _lib.ptr(self.error))
 
     def allreduce_(self, t):
-        self.seq += 1
-        _lib.call("sf_peer_allreduce_f64", self.boxes, self.comm.world, self.comm.rank, self.seq,
+        self.calls += 1
+        _lib.call("sf_peer_allreduce_f64", self.boxes, self.comm.world, self.comm.rank, _lib.ptr(self.seq),
                   _lib.ptr(self.error), _lib.ptr(t), t.numel(), _lib.ptr(t), _lib.stream_ptr(t.device))
 
+    def failed(self):
+        return bool(int(self.error.item()))
+
     def check(self):
-        if int(self.error.item()):
-            raise RuntimeError("peer allreduce timed out (a rank did not arrive within 5 s)")
+        if self.failed():
+            raise RuntimeError("peer allreduce / halo exchange timed out (a rank did not arrive within 5 s)")
 
     def close(self):
         for p in self.opened:
@@ -200,6 +208,17 @@ class _RawPtr:
 
     def data_ptr(self):
         return self.p
+
+
+class BankedRecv(_RawPtr):
+    """The receive buffer of an NVLink halo exchange: bank 0 of the inbox, plus the
+    device call counter and bank stride from which the dssum picks the bank of
+    the current exchange (sf_dssum_blk_f64 recv_seq / recv_bank)."""
+
+    def __init__(self, p, seq_ptr, bank):
+        super().__init__(p)
+        self.seq_ptr = seq_ptr
+        self.bank = bank
 
 
 class HaloIPC:
@@ -253,27 +272,35 @@ class HaloIPC:
         dev = torch.device("cuda", torch.cuda.current_device())
         self.counter = torch.zeros(1, dtype=torch.int32, device=dev)
         self.error = comm.peer.error if comm.peer is not None else torch.zeros(1, dtype=torch.int32, device=dev)
-        self.seq = 0
+        # the exchange counter is header word SEQ of the own inbox (zeroed at
+        # allocation, advanced by halo_put on the device); the receive buffer
+        # handed to the dssum names both banks and that counter
+        self.recv = BankedRecv(self.own + 8 * self.HEADER, self.own + 8 * self.SEQ, self.n_recv)
+        self.calls = 0
         torch.cuda.synchronize()
         comm.dist.barrier(group=comm.group)
 
+    SEQ = 16
+
     def put(self, v):
-        """Enqueue the NVLink stores of this rank's interface copies (call sequence +1)."""
+        """Enqueue the NVLink stores of this rank's interface copies (the call
+        number advances on the device)."""
         if self.n_peers == 0:
             return
-        self.seq += 1
+        self.calls += 1
         _lib.call("sf_halo_put_f64", _lib.ptr(v), _lib.ptr(self.plan.send_all), self.n_peers, self.peer_rank,
-                  self.seg, self.dst, self.stride, self.flag, self.seq, _lib.ptr(self.counter),
-                  _lib.stream_ptr(v.device))
+                  self.seg, self.dst, self.stride, self.flag, self.own, _lib.ptr(self.counter),
+                  _lib.ptr(self.error), _lib.stream_ptr(v.device))
 
     def wait(self, device):
-        """Enqueue the wait for the peers' copies of the last put; returns the inbox bank."""
+        """Enqueue the wait for the peers' copies of the last put; returns the
+        receive buffer (both inbox banks + the device call counter)."""
         if self.n_peers == 0:
             return None
-        _lib.call("sf_halo_wait", self.own, self.n_peers, self.peer_rank, self.seq, _lib.ptr(self.error),
+        _lib.call("sf_halo_wait", self.own, self.n_peers, self.peer_rank, _lib.ptr(self.error),
                   _lib.stream_ptr(device))
         self.comm.collectives += 1
-        return _RawPtr(self.own + 8 * (self.HEADER + (self.seq & 1) * self.n_recv))
+        return self.recv
 
     def exchange(self, v):
         self.put(v)

@@ -97,8 +97,14 @@ class _Fused:
             raise RuntimeError("gated MGS passes across ranks need the peer reducer")
 
     def read(self, t):
-        h = t.to("cpu", non_blocking=False)
-        return h.tolist()
+        return self.checked(t.to("cpu", non_blocking=False).tolist())
+
+    def checked(self, vals):
+        """Host values of a reduction; NaN across ranks may mean a peer timed out
+        (the NVLink kernels then return NaN at once): raise instead of iterating."""
+        if self.comm.peer is not None and any(v != v for v in vals):
+            self.comm.check()
+        return vals
 
     def precond_into(self, v, z):
         if self.invdiag is None:
@@ -349,9 +355,14 @@ class _GraphBuffers:
 
 
 def _graph_buffers(F, op, b, restart, S):
-    """Graph replay applies on one rank (the fused NVLink reductions take a per-call
-    sequence number) unless SEMFLOW_B200_GRAPHS=0."""
-    if F.comm.world > 1 or os.environ.get("SEMFLOW_B200_GRAPHS", "1") == "0":
+    """Graph replay of the Arnoldi steps unless SEMFLOW_B200_GRAPHS=0.  Across ranks
+    the captured NVLink reductions and halo exchanges take their call numbers and
+    mailbox banks from device counters (peer.cuh, halo.cu), so a replay is the
+    same launch sequence as an eager step.  The opt-in fused Ax+dssum launch
+    (axdss.cu) takes a host-side epoch and is never captured."""
+    if os.environ.get("SEMFLOW_B200_GRAPHS", "1") == "0" or getattr(op, "fused", False):
+        return None
+    if F.comm.world > 1 and F.comm.peer is None:
         return None
     # every device address a captured step reads: the graphs stay valid only while
     # these are the same tensors (the buffers below are held alive by the cache)
@@ -485,7 +496,7 @@ def _gmres_pipelined(F, op, b, tol, max_iter, restart):
             if j + 1 < m and j + 1 not in evs and abs(g[j]) > 10.0 * tol:
                 evs[j + 1] = launch(j + 1, V)
             evs[j].synchronize()
-            vals = host[j].tolist()
+            vals = F.checked(host[j].tolist())
             norm_before = math.sqrt(vals[1])
             hcol = np.zeros(j + 2)
             for i in range(j + 1):

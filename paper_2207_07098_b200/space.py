@@ -139,6 +139,10 @@ class GatherScatter:
                 self._ipc = _dist.HaloIPC(self.comm, plan)
             self._masked_perm = {}
             self._mult = None
+            # every host-synchronising derivation done now: an operator application
+            # may first run inside a CUDA-graph capture (krylov._graph_buffers)
+            self._build_classes()
+            self.interior_range()
             return
         self.gid = gid
         self.perm = perm
@@ -165,6 +169,8 @@ class GatherScatter:
         self.shared_bits = pack_bits((self.mult8 > 1).view(E, nnn)) if E else None
         self._masked_perm = {}
         self._mult = None
+        if self.device.type == "cuda":
+            self._build_classes()
 
     # ------------------------------------------------------------ properties
     @property
@@ -398,13 +404,14 @@ class GatherScatter:
         n2, n4, n8 = self.cls_n
         pm = self.cls_perm if perm is None else perm
         self.account_dssum()
-        if _DSSUM_KERNEL == "cls" and pre is None:
+        seq_ptr = getattr(recv, "seq_ptr", None)        # banked NVLink inbox (dist.BankedRecv)
+        if _DSSUM_KERNEL == "cls" and pre is None and seq_ptr is None:
             _lib.call("sf_dssum_cls_f64", _lib.ptr(v), _lib.ptr(pm), n2, n4, n8, _lib.ptr(self.cls_gen_off),
                       self.cls_n_gen, mode, _lib.ptr(u), _lib.ptr(recv), self.P, _lib.stream_ptr(self.device))
         else:
             _lib.call("sf_dssum_blk_f64", _lib.ptr(v), _lib.ptr(pm), n2, n4, n8, _lib.ptr(self.cls_gen_off),
                       _lib.ptr(self.cls_bstart), self.cls_nb, mode, _lib.ptr(u), _lib.ptr(pre), _lib.ptr(recv),
-                      self.P, _lib.stream_ptr(self.device))
+                      self.P, seq_ptr, getattr(recv, "bank", 0), _lib.stream_ptr(self.device))
 
     def account_dssum(self):
         """Credit one dssum's algorithmic bytes to the step accounting (traffic.py)."""

@@ -6,7 +6,15 @@
    bitwise identical to the single-GPU result, on every rank;
 2. partitioned glsc3 equals the single-GPU value to rounding;
 3. the TGV step on the partitioned mesh reproduces the reference's iteration
-   counts and kinetic energy (tests/golden/solvers.json) when ne is 4 or 8.
+   counts and kinetic energy (tests/golden/solvers.json) when ne is 4 or 8 --
+   with the look-ahead GMRES replaying its Arnoldi steps from CUDA graphs that
+   contain the fused NVLink reductions and halo exchanges;
+4. stress: 10^4 back-to-back fused MGS reductions, a pseudo-random third of them
+   gated off on the device, no halo exchange and no host sync in between, with
+   integer-valued data so every sum is exact: each result equals the 1-GPU value
+   bit for bit (the mailbox banks follow the executed calls only);
+5. a graph-captured dssum with its halo exchange, replayed 64 times on changing
+   input, bitwise equal to the single-GPU dssum.
 Rank 0 prints one JSON line and exits nonzero on failure.
 """
 
@@ -37,6 +45,7 @@ def main():
     mesh = gen_box_mesh((0, L, 0, L, 0, L), (ne, ne, ne))
     basis = make_basis(7)
     full = build_space(mesh, basis, device=dev)                 # single-GPU reference on each rank
+    _FULL["space"] = full
     part = build_space(mesh, basis, device=dev, comm=comm)
     e0, e1 = part.e_range
     g = torch.Generator(device="cpu").manual_seed(5)
@@ -72,6 +81,7 @@ def main():
     del rfull, rpart
     del full
     torch.cuda.empty_cache()
+    ok.update(stress_checks(part, dev, comm))
     res = {"world": W, "ne": ne, "checks": ok}
     if ne in (4, 8):
         with open(os.path.join(ROOT, "tests", "golden", "solvers.json")) as fh:
@@ -92,6 +102,78 @@ def main():
         print(json.dumps(res), flush=True)
     torch.distributed.destroy_process_group()
     sys.exit(0 if res["ok"] else 1)
+
+
+def stress_checks(part, dev, comm, n_calls=10000):
+    """Sections 4 and 5 of the module docstring."""
+    from paper_2207_07098_b200 import _device, _lib
+
+    ok = {}
+    r, W = comm.rank, comm.world
+    P = 1 << 15
+    g = torch.Generator(device="cpu").manual_seed(11)
+    # global integer data; rank r owns rows [r*P, (r+1)*P)
+    wg = torch.randint(-8, 9, (W * P,), generator=g, dtype=torch.int64).to(torch.float64)
+    vg = torch.randint(-8, 9, (4, W * P), generator=g, dtype=torch.int64).to(torch.float64)
+    w = wg[r * P:(r + 1) * P].contiguous().to(dev)
+    V = vg[:, r * P:(r + 1) * P].contiguous().to(dev)
+    mult = torch.ones(P, dtype=torch.uint8, device=dev)
+    gates = torch.rand(n_calls, generator=g) > 1.0 / 3.0            # same pattern on every rank
+    gate_dev = gates.to(torch.float64).to(dev)
+    out = torch.full((n_calls, 2), -1.0, dtype=torch.float64, device=dev)
+    wk = _device.workspace(dev).args()
+    st = _lib.stream_ptr(dev)
+    peer = comm.peer
+    torch.cuda.synchronize()
+    for k in range(n_calls):
+        _lib.call("sf_mgs_step_peer_f64", _lib.ptr(w), None, None, _lib.ptr(V[k % 4]), None, None, _lib.ptr(mult),
+                  1, P, *wk, out.data_ptr() + 16 * k, *peer.fused_args(), gate_dev.data_ptr() + 8 * k, st)
+    got = out.cpu()
+    want = torch.full((n_calls, 2), -1.0, dtype=torch.float64)
+    dots = (vg * wg).sum(dim=1)                                      # exact: |values| < 2^53
+    nrm = (wg * wg).sum()
+    for k in range(n_calls):
+        if gates[k]:
+            want[k, 0] = dots[k % 4]
+            want[k, 1] = nrm
+    ok["stress_gated_reductions"] = bool(torch.equal(got, want))
+    ok["stress_calls"] = n_calls
+    ok["stress_executed"] = int(gates.sum())
+    ok["stress_seq"] = int(peer.seq.item())
+    ok["stress_seq_ok"] = ok["stress_seq"] >= ok["stress_executed"]
+    # graph-captured dssum + halo exchange, replayed on changing input
+    if part.gs._ipc is not None:
+        u_static = torch.empty(part.shape, dtype=torch.float64, device=dev)
+        u_static.copy_(torch.randn(part.shape, generator=g, dtype=torch.float64).to(dev))
+        part.gs.add(u_static)                      # warm-up (eager)
+        gr = torch.cuda.CUDAGraph()
+        s2 = torch.cuda.Stream(dev)
+        s2.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s2):
+            part.gs.add(u_static)
+        torch.cuda.current_stream(dev).wait_stream(s2)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(gr):
+            res_static = part.gs.add(u_static)
+        good = True
+        e0, e1 = part.e_range
+        for k in range(64):
+            ug = torch.randn(_FULL["space"].shape, generator=g, dtype=torch.float64)
+            u_static.copy_(ug[e0:e1].to(dev))
+            gr.replay()
+            want_k = _single_dssum(ug, dev)[e0:e1]
+            good &= bool(torch.equal(res_static, want_k))
+        ok["graph_halo_dssum"] = good
+    comm.check()
+    return ok
+
+
+_FULL = {}
+
+
+def _single_dssum(ug, dev):
+    sp = _FULL["space"]
+    return sp.gs.add(ug.to(dev))
 
 
 if __name__ == "__main__":
