@@ -93,6 +93,12 @@ int sf_ax_masked_f64(const double* d_host, int n, const double* g, const double*
                      const double* u, double* w, long long E, double lam_visc, double lam_mass,
                      const uint32_t* inmask, const uint32_t* outsel, int exact, void* stream);
 
+/* Selects the n = 8 Ax_helm kernel behind sf_ax_helm_f64 / sf_ax_masked_f64 /
+ * sf_ax_pre_f64 / sf_ax_range_f64: 1 (default) = persistent kernel fed by bulk
+ * asynchronous copies into a shared-memory ring, 0 = register-prefetch kernel.
+ * Both are bit-identical; process-wide switch for A/B measurements. */
+int sf_set_ax_kernel(int which);
+
 /* The element operator (plain / masked / pre-scaled) on elements [e0, e1) of an
  * E-element field (n = 8; e0 even, e1 even or E; geometry strides use E): the
  * multi-GPU operator computes the halo elements first, posts the NVLink halo

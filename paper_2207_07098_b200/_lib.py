@@ -25,6 +25,7 @@ _SIGS = {
     "sf_version": [],
     "sf_last_error": [],
     "sf_red_workspace_doubles": [],
+    "sf_set_ax_kernel": [_i],
     "sf_apply_axis_f64": [_i, _vp, _i, _i, _vp, _vp, _ll, _i, _vp],
     "sf_apply_axis3_f64": [_i, _vp, _i, _i, _i, _i, _vp, _vp, _ll, _i, _vp],
     "sf_grad_ref_f64": [_vp, _i, _vp, _vp, _vp, _vp, _ll, _i, _vp],

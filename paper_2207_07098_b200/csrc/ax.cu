@@ -173,6 +173,13 @@ static void launch8s(dim3 grid, cudaStream_t st, const DMat<8>& D, const double*
                                                                  pair0);
 }
 
+// n = 8 production kernel: bulk-copy-fed persistent Ax (ax8t.cu); 0 selects the
+// register-prefetch kernel below (ax8s.cuh) -- sf_set_ax_kernel, for A/B runs.
+int ax_helm8t(const DMat<8>& D, const double* g, const double* b, const double* u, double* w, long long E,
+              long long e0, long long e1, double lv, double lm, const uint32_t* inmask, const uint32_t* outsel,
+              const double* pre, int exact, cudaStream_t st);
+int g_ax_kernel = 1;
+
 // Elements [e0, e1) of an E-element field (e0 even; strides use E): the boundary /
 // interior split that lets the multi-GPU operator post its halo exchange before
 // the interior elements are computed.
@@ -190,6 +197,10 @@ int ax_helm8_range(const double* d_host, const double* g, const double* b, const
   if (e1 == e0) return SF_OK;
   DMat<8> D;
   for (int x = 0; x < 64; ++x) D.v[x] = d_host[x];
+  if (g_ax_kernel == 1) {
+    const int r = ax_helm8t(D, g, b, u, w, E, e0, e1, lv, lm, inmask, outsel, pre, exact, st);
+    if (r != SF_ERR_UNSUPPORTED) return r;
+  }
   const long long p0 = e0 / 2, p1 = (e1 + 1) / 2;
   dim3 grid((unsigned)(p1 - p0));
   const bool masked = inmask != nullptr;
@@ -476,6 +487,12 @@ static int launch_ax(const double* d_host, const double* g, const double* b, con
   DMat<N> D = load_dmat<N>(d_host);
   dim3 grid((unsigned)((E + C::EPB - 1) / C::EPB));
   const bool masked = inmask != nullptr;
+  if constexpr (N == 8) {
+    if (g_ax_kernel == 1) {
+      const int r = ax_helm8t(D, g, b, u, w, E, 0, E, lv, lm, inmask, outsel, pre, exact, st);
+      if (r != SF_ERR_UNSUPPORTED) return r;
+    }
+  }
   if (pre != nullptr) {
     // fused Jacobi scaling: n = 8 swizzled kernel only
     if constexpr (N == 8) {

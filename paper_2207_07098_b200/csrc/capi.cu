@@ -87,6 +87,7 @@ int bdf_ext(double*, double*, const double* const*, const double* const*, const 
 int trilinear_coords(const double*, const double*, int, long long, double*, cudaStream_t);
 int metrics(const double*, const double*, int, const double*, long long, double*, double*, double*,
             double*, cudaStream_t);
+extern int g_ax_kernel;
 
 }  // namespace sf
 
@@ -98,6 +99,17 @@ const char* sf_version(void) { return "semflow_b200 0.1.0 (sm_100a, fp64)"; }
 const char* sf_last_error(void) { return g_err; }
 
 int sf_red_workspace_doubles(void) { return K_MAX * RED_BLOCKS; }
+
+// n = 8 Ax kernel: 1 = bulk-copy-fed persistent kernel (default), 0 = register-
+// prefetch kernel.  Process-wide; for A/B measurements (tools/ax_variants.py).
+int sf_set_ax_kernel(int which) {
+  if (which != 0 && which != 1) {
+    set_error("sf_set_ax_kernel: expected 0 or 1, got %d", which);
+    return SF_ERR_ARG;
+  }
+  g_ax_kernel = which;
+  return SF_OK;
+}
 
 int sf_apply_axis_f64(int axis, const double* a, int m, int n, const double* u, double* out,
                       long long E, int exact, void* stream) {
