@@ -218,12 +218,7 @@ def time_kernels(sp, op, u, reps=20):
         else:
             gs.dssum_into(w, 0)
 
-    def fused():
-        op.apply_into(u, w)
-
     jobs = [("ax", ax), ("dssum", dss)]
-    if getattr(op, "fused", False):
-        jobs.append(("fused", fused))
     res = {}
     for name, fn in jobs:
         for _ in range(3):
@@ -367,7 +362,7 @@ def bench_poisson(args, world, rank, dev):
     kt = time_kernels(sp, A, torch.randn(sp.shape, dtype=torch.float64, device=dev))
     pk, src = peaks()
     nbytes = ax_dssum_bytes(sp, True)
-    t_op = kt.get("fused", kt["ax"] + kt["dssum"])
+    t_op = kt["ax"] + kt["dssum"]
     achieved = nbytes / t_op / 1e9
     line = {
         "metric": "GDOF/s per PCG iteration (config 2: Poisson Ax+dssum+Jacobi-CG, 32^3 lx=8)",
@@ -379,8 +374,7 @@ def bench_poisson(args, world, rank, dev):
                    "parallelism": f"replicas x{world}" if world > 1 else "single"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": None,
-                     "kernel": "ax_dssum8_kernel (fused masked Ax+dssum)" if "fused" in kt
-                     else "ax_helm(masked)+dssum",
+                     "kernel": "ax8t_kernel (masked) + dssum_blk_kernel",
                      "algorithmic_bytes": nbytes, "us": t_op * 1e6, "ax_us": kt["ax"] * 1e6,
                      "dssum_us": kt["dssum"] * 1e6, "peak_source": src,
                      "step": step_traffic(traffic_sum, [0, 0], t, args.steps, world, pk["hbm_gbs"])},
@@ -570,7 +564,7 @@ def bench_tgv(args, world, rank, dev):
     kt = time_kernels(sp, op, probe)
     pk, src = peaks()
     nbytes = ax_dssum_bytes(sp, op.masked)
-    t_op = kt.get("fused", kt["ax"] + kt["dssum"])
+    t_op = kt["ax"] + kt["dssum"]
     achieved = nbytes / t_op / 1e9
     # dominant kernel of the step: the GMRES modified-Gram-Schmidt pass
     # (w -= h v_{i-1}; <w, v_i>) -- ~70 % of the step at 64^3 (profiles/)
@@ -614,8 +608,7 @@ def bench_tgv(args, world, rank, dev):
                      "ax_dssum": {"achieved": achieved, "frac": achieved / pk["hbm_gbs"],
                                   "algorithmic_bytes": nbytes, "us": t_op * 1e6, "ax_us": kt["ax"] * 1e6,
                                   "dssum_us": kt["dssum"] * 1e6,
-                                  "kernel": ("ax_dssum8_kernel, fused" if "fused" in kt else "ax_helm + dssum")
-                                  + " (pressure Poisson operator)"},
+                                  "kernel": "ax8t_kernel + dssum_blk_kernel (pressure Poisson operator)"},
                      "step": step_traffic(traffic_sum[:2], traffic_sum[2:], t, args.steps, world,
                                           pk["hbm_gbs"])},
         "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),

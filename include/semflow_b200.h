@@ -158,23 +158,6 @@ int sf_ax_pre_f64(const double* d_host, int n, const double* g, const double* b,
                   const double* pre, double* w, long long E, double lam_visc, double lam_mass,
                   const uint32_t* inmask, const uint32_t* outsel, int exact, void* stream);
 
-/* Fused global operator for n = 8, single rank: sf_ax_helm_f64 / sf_ax_masked_f64
- * followed by sf_dssum_cls_f64 in ONE launch (the whole make_global_op closure,
- * operators.py:51-54, mode 0 = unmasked add, 2 = masked).  `plan` is the int32
- * device schedule built by GatherScatter.fused_plan: Ax element pairs cut into
- * chunks, the shared gids grouped by the chunk of their highest element, and
- * dssum blocks interleaved after the next Ax chunk; `meta` (host, 12 int64) =
- * {n_blocks, chunk_pairs, n_chunks, offsets of sched, dtab, need, lo, pairs,
- * quads, octets, generic offsets, generic perm}.  `sync` is a device array of
- * n_chunks + 1 uint64, zero before the first launch and never reset: `epoch` is
- * the number of earlier launches with the same sync array (0, 1, 2, ...).
- * Bit-identical to the two-kernel sequence. */
-int sf_ax_dssum8_f64(const double* d_host, const double* g, const double* b, const double* u,
-                     double* w, long long E, double lam_visc, double lam_mass,
-                     const uint32_t* inmask, const uint32_t* outsel, int mode, const int* plan,
-                     const long long* meta, unsigned long long* sync, unsigned long long epoch,
-                     int exact, void* stream);
-
 /* out[i] = v[idx[i]] -- packs a rank's interface values for the halo exchange. */
 int sf_gather_f64(double* out, const double* v, const int* idx, long long n, void* stream);
 

@@ -38,8 +38,6 @@ _SIGS = {
     "sf_dssum_blk_f64": [_vp, _vp, _i, _i, _i, _vp, _vp, _i, _i, _vp, _vp, _vp, _i, _vp, _ll, _vp],
     "sf_ax_pre_f64": [_vp, _i, _vp, _vp, _vp, _vp, _vp, _ll, _d, _d, _vp, _vp, _i, _vp],
     "sf_ax_range_f64": [_vp, _i, _vp, _vp, _vp, _vp, _vp, _ll, _ll, _ll, _d, _d, _vp, _vp, _i, _vp],
-    "sf_ax_dssum8_f64": [_vp, _vp, _vp, _vp, _vp, _ll, _d, _d, _vp, _vp, _i, _vp, _vp, _vp,
-                         ctypes.c_ulonglong, _i, _vp],
     "sf_gather_f64": [_vp, _vp, _vp, _ll, _vp],
     "sf_rank_sum_f64": [_vp, _i, _i, _vp, _vp],
     "sf_glsc3_f64": [_i, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp],

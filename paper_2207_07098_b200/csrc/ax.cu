@@ -216,179 +216,6 @@ int ax_helm8_range(const double* d_host, const double* g, const double* b, const
   return check_launch("ax_range");
 }
 
-// K1 for n = 8, two pencils per thread (experimental, -DSF_AX_PENCIL2; measured
-// 305 us vs 246 us for the one-pencil kernel at 32^3, kept for further tuning).  One warp owns one element; lane (j, kk)
-// owns the r-pencils (j, 2kk) and (j, 2kk+1).  Global accesses are 16-byte
-// vectors (a warp moves one contiguous 512 B element layer per instruction).  In
-// shared memory the s-derivative pair and the t-derivative row are fetched once
-// for both pencils (LDS.128), roughly halving the shared-memory wavefronts per
-// point against the one-pencil kernel, which is what bounds it (ncu: l1tex 72 %,
-// short-scoreboard stalls).  The layer loops are not unrolled so the live state
-// stays ~100 registers.  Each element is private to its warp: __syncwarp only.
-// Per-point arithmetic and accumulation order are identical to ax_helm_kernel.
-#ifndef SF_AX8_MINB
-#define SF_AX8_MINB 7
-#endif
-#ifndef SF_AX8_EPB
-#define SF_AX8_EPB 2
-#endif
-constexpr int AX8_EPB = SF_AX8_EPB;  // elements (warps) per block
-
-template <bool EX, bool MASK>
-__global__ void __launch_bounds__(32 * AX8_EPB, SF_AX8_MINB)
-ax_helm_n8_kernel(DMat<8> D, const double* __restrict__ g, const double* __restrict__ b,
-                  const double* __restrict__ u, double* __restrict__ w, long long E, double lv,
-                  double lm, const uint32_t* __restrict__ inmask,
-                  const uint32_t* __restrict__ outsel) {
-  constexpr int N = 8, NN = 64, NNN = 512;
-  constexpr int PJ = 10, LAY = N * PJ, VOL = N * LAY;  // padded smem rows: conflict-free LDS.128
-  // us_: element u, layer i overwritten by f3 once every lane is past layer i
-  __shared__ __align__(16) double us_[AX8_EPB][VOL];
-  __shared__ __align__(16) double f1s[AX8_EPB][VOL];
-  __shared__ __align__(16) double f2s[AX8_EPB][VOL];
-  __shared__ __align__(16) double Dr[N * PJ];   // D row-major, padded rows
-  __shared__ __align__(16) double Dc[N * PJ];   // D^T row-major, padded rows
-  for (int x = threadIdx.x; x < NN; x += blockDim.x) {
-    Dr[(x >> 3) * PJ + (x & 7)] = D.v[x];
-    Dc[(x >> 3) * PJ + (x & 7)] = D.v[(x & 7) * N + (x >> 3)];
-  }
-  __syncthreads();
-  const int le = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int j = lane >> 2, k0 = (lane & 3) * 2;
-  const long long e = (long long)blockIdx.x * AX8_EPB + le;
-  if (e >= E) return;  // whole warp exits together; no block barrier below
-  const int jk = j * N + k0;        // global layer offset
-  const int sjk = j * PJ + k0;      // shared layer offset
-  const long long base = e * NNN + jk;
-  const long long gstride = E * (long long)NNN;
-  const int wsel = j >> 2, bsh = (j & 3) * 8 + k0;  // mask word offset / bit within a layer
-  double* su = us_[le];
-  double* s1 = f1s[le];
-  double* s2 = f2s[le];
-
-  double um0[N], um1[N];
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    double2 v = __ldg(reinterpret_cast<const double2*>(u + base + i * NN));
-    if constexpr (MASK) {
-      const uint32_t wd = __ldg(inmask + e * 16 + 2 * i + wsel) >> bsh;
-      if (!(wd & 1u)) v.x = 0.0;
-      if (!(wd & 2u)) v.y = 0.0;
-    }
-    um0[i] = v.x;
-    um1[i] = v.y;
-    *reinterpret_cast<double2*>(su + i * LAY + sjk) = v;
-  }
-  double dj[N];
-#pragma unroll
-  for (int q = 0; q < N; ++q) dj[q] = Dr[j * PJ + q];
-  const double* gp = g + base;
-  double2 gn[6];
-#pragma unroll
-  for (int m = 0; m < 6; ++m) gn[m] = __ldg(reinterpret_cast<const double2*>(gp + m * gstride));
-  __syncwarp();
-
-#pragma unroll 1
-  for (int i = 0; i < N; ++i) {
-    double2 gv[6];
-#pragma unroll
-    for (int m = 0; m < 6; ++m) gv[m] = gn[m];
-    if (i + 1 < N) {
-#pragma unroll
-      for (int m = 0; m < 6; ++m)
-        gn[m] = __ldg(reinterpret_cast<const double2*>(gp + (i + 1) * NN + m * gstride));
-    }
-    double ar0 = 0.0, ar1 = 0.0, as0 = 0.0, as1 = 0.0, at0 = 0.0, at1 = 0.0;
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-      const double dq = Dr[i * PJ + q];
-      ar0 = mac<EX>(ar0, dq, um0[q]);
-      ar1 = mac<EX>(ar1, dq, um1[q]);
-      const double2 sv = *reinterpret_cast<const double2*>(su + i * LAY + q * PJ + k0);
-      as0 = mac<EX>(as0, dj[q], sv.x);
-      as1 = mac<EX>(as1, dj[q], sv.y);
-    }
-#pragma unroll
-    for (int q = 0; q < N; q += 2) {
-      const double2 tv = *reinterpret_cast<const double2*>(su + i * LAY + j * PJ + q);
-      const double2 da = *reinterpret_cast<const double2*>(Dr + k0 * PJ + q);
-      const double2 db = *reinterpret_cast<const double2*>(Dr + (k0 + 1) * PJ + q);
-      at0 = mac<EX>(at0, da.x, tv.x);
-      at1 = mac<EX>(at1, db.x, tv.x);
-      at0 = mac<EX>(at0, da.y, tv.y);
-      at1 = mac<EX>(at1, db.y, tv.y);
-    }
-    double2 v1, v2, v3;
-    v1.x = add<EX>(add<EX>(mul<EX>(gv[0].x, ar0), mul<EX>(gv[1].x, as0)), mul<EX>(gv[2].x, at0));
-    v1.y = add<EX>(add<EX>(mul<EX>(gv[0].y, ar1), mul<EX>(gv[1].y, as1)), mul<EX>(gv[2].y, at1));
-    v2.x = add<EX>(add<EX>(mul<EX>(gv[1].x, ar0), mul<EX>(gv[3].x, as0)), mul<EX>(gv[4].x, at0));
-    v2.y = add<EX>(add<EX>(mul<EX>(gv[1].y, ar1), mul<EX>(gv[3].y, as1)), mul<EX>(gv[4].y, at1));
-    v3.x = add<EX>(add<EX>(mul<EX>(gv[2].x, ar0), mul<EX>(gv[4].x, as0)), mul<EX>(gv[5].x, at0));
-    v3.y = add<EX>(add<EX>(mul<EX>(gv[2].y, ar1), mul<EX>(gv[4].y, as1)), mul<EX>(gv[5].y, at1));
-    *reinterpret_cast<double2*>(s1 + i * LAY + sjk) = v1;
-    *reinterpret_cast<double2*>(s2 + i * LAY + sjk) = v2;
-    __syncwarp();  // every lane has read u layer i
-    *reinterpret_cast<double2*>(su + i * LAY + sjk) = v3;
-  }
-#pragma unroll
-  for (int q = 0; q < N; ++q) dj[q] = Dc[j * PJ + q];  // column j of D
-  __syncwarp();
-
-  const bool mass = lm != 0.0;
-#pragma unroll 1
-  for (int i = 0; i < N; ++i) {
-    double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-    for (int q = 0; q < N; q += 2) {
-      const double2 t3 = *reinterpret_cast<const double2*>(su + i * LAY + j * PJ + q);
-      const double2 ca = *reinterpret_cast<const double2*>(Dc + k0 * PJ + q);        // D[q..q+1][k0]
-      const double2 cb = *reinterpret_cast<const double2*>(Dc + (k0 + 1) * PJ + q);  // D[q..q+1][k0+1]
-      const double2 ci = *reinterpret_cast<const double2*>(Dc + i * PJ + q);         // D[q..q+1][i]
-      const double2 ra = *reinterpret_cast<const double2*>(s1 + q * LAY + sjk);
-      const double2 rb = *reinterpret_cast<const double2*>(s1 + (q + 1) * LAY + sjk);
-      const double2 sa = *reinterpret_cast<const double2*>(s2 + i * LAY + q * PJ + k0);
-      const double2 sb = *reinterpret_cast<const double2*>(s2 + i * LAY + (q + 1) * PJ + k0);
-      acc0 = mac<EX>(acc0, ci.x, ra.x);
-      acc1 = mac<EX>(acc1, ci.x, ra.y);
-      acc0 = mac<EX>(acc0, dj[q], sa.x);
-      acc1 = mac<EX>(acc1, dj[q], sa.y);
-      acc0 = mac<EX>(acc0, ca.x, t3.x);
-      acc1 = mac<EX>(acc1, cb.x, t3.x);
-      acc0 = mac<EX>(acc0, ci.y, rb.x);
-      acc1 = mac<EX>(acc1, ci.y, rb.y);
-      acc0 = mac<EX>(acc0, dj[q + 1], sb.x);
-      acc1 = mac<EX>(acc1, dj[q + 1], sb.y);
-      acc0 = mac<EX>(acc0, ca.y, t3.y);
-      acc1 = mac<EX>(acc1, cb.y, t3.y);
-    }
-    double2 wv;
-    wv.x = mul<EX>(lv, acc0);
-    wv.y = mul<EX>(lv, acc1);
-    if (mass) {
-      const double2 bv = __ldg(reinterpret_cast<const double2*>(b + base + i * NN));
-      const double2 uv = *reinterpret_cast<const double2*>(u + base + i * NN);
-      double u0 = uv.x, u1 = uv.y;
-      if constexpr (MASK) {
-        const uint32_t wd = __ldg(inmask + e * 16 + 2 * i + wsel) >> bsh;
-        if (!(wd & 1u)) u0 = 0.0;
-        if (!(wd & 2u)) u1 = 0.0;
-      }
-      wv.x = add<EX>(wv.x, mul<EX>(mul<EX>(lm, bv.x), u0));
-      wv.y = add<EX>(wv.y, mul<EX>(mul<EX>(lm, bv.y), u1));
-    }
-    if constexpr (MASK) {
-      const uint32_t sel = __ldg(outsel + e * 16 + 2 * i + wsel) >> bsh;
-      if ((sel & 3u) != 3u) {
-        const double2 uv = __ldg(reinterpret_cast<const double2*>(u + base + i * NN));
-        if (!(sel & 1u)) wv.x = uv.x;
-        if (!(sel & 2u)) wv.y = uv.y;
-      }
-    }
-    *reinterpret_cast<double2*>(w + base + i * NN) = wv;
-  }
-}
-
 // grad_ref: three reference derivatives with separate sequential accumulators
 // (`_numba.py:63-83`).
 template <int N, bool EX>
@@ -511,17 +338,7 @@ static int launch_ax(const double* d_host, const double* g, const double* b, con
     }
   }
   if constexpr (N == 8) {
-#ifdef SF_AX_PENCIL2
-    dim3 g8((unsigned)((E + AX8_EPB - 1) / AX8_EPB));
-    if (exact) {
-      if (masked) ax_helm_n8_kernel<true, true><<<g8, 32 * AX8_EPB, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel);
-      else ax_helm_n8_kernel<true, false><<<g8, 32 * AX8_EPB, 0, st>>>(D, g, b, u, w, E, lv, lm, nullptr, nullptr);
-    } else {
-      if (masked) ax_helm_n8_kernel<false, true><<<g8, 32 * AX8_EPB, 0, st>>>(D, g, b, u, w, E, lv, lm, inmask, outsel);
-      else ax_helm_n8_kernel<false, false><<<g8, 32 * AX8_EPB, 0, st>>>(D, g, b, u, w, E, lv, lm, nullptr, nullptr);
-    }
-    return check_launch("ax_helm_n8");
-#elif !defined(SF_AX8_UNSWIZZLED)
+#if !defined(SF_AX8_UNSWIZZLED)
     dim3 g8((unsigned)((E + 1) / 2));
     if (exact) {
       if (masked) launch8s<true, true, false>(g8, st, D, g, b, u, w, E, lv, lm, inmask, outsel, nullptr);

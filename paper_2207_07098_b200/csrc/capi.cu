@@ -52,9 +52,6 @@ int ax_helm8_range(const double*, const double*, const double*, const double*, c
                    long long, long long, double, double, const uint32_t*, const uint32_t*, int, cudaStream_t);
 int dssum_blk(double*, const int*, int, int, int, const int*, const int*, int, int, const double*,
               const double*, const double*, int, const unsigned long long*, long long, cudaStream_t);
-int ax_dssum8(const double*, const double*, const double*, const double*, double*, long long, double,
-              double, const uint32_t*, const uint32_t*, int, const int*, const long long*,
-              unsigned long long*, unsigned long long, int, cudaStream_t);
 int dot_multi(int, const double* const*, const double* const*, const uint8_t*, long long, RedWork,
               double*, cudaStream_t);
 int cg_init(const double*, const double*, double*, const uint8_t*, long long, RedWork, double*,
@@ -193,15 +190,6 @@ int sf_dssum_blk_f64(double* v, const int* perm, int n2, int n4, int n8, const i
                      long long recv_bank, void* stream) {
   return dssum_blk(v, perm, n2, n4, n8, gen_offsets, block_start, n_blocks, mode, u, pre, recv, n_local,
                    recv_seq, recv_bank, as_stream(stream));
-}
-
-int sf_ax_dssum8_f64(const double* d_host, const double* g, const double* b, const double* u,
-                     double* w, long long E, double lam_visc, double lam_mass,
-                     const uint32_t* inmask, const uint32_t* outsel, int mode, const int* plan,
-                     const long long* meta, unsigned long long* sync, unsigned long long epoch,
-                     int exact, void* stream) {
-  return ax_dssum8(d_host, g, b, u, w, E, lam_visc, lam_mass, inmask, outsel, mode, plan, meta, sync,
-                   epoch, exact, as_stream(stream));
 }
 
 int sf_gather_f64(double* out, const double* v, const int* idx, long long n, void* stream) {

@@ -81,16 +81,6 @@ class GlobalOp:
         else:
             self.mask = None
         self.launches = 0
-        # n = 8 on one rank: K1 and K2 as one launch (csrc/axdss.cu), opt-in: measured
-        # no faster than the two kernels (see the header of axdss.cu)
-        self.fused = (n == 8 and gs.comm.world == 1 and E > 0
-                      and os.environ.get("SEMFLOW_B200_FUSED", "0") == "1")
-        self._plan = None
-
-    def fused_plan(self):
-        if self._plan is None:
-            self._plan = self.space.gs.fused_plan(self.sh_perm if self.masked else None)
-        return self._plan
 
     def apply_into(self, u, w, pre=None):
         """w <- A u (w must not alias u).  With ``pre`` (n = 8): w <- A (pre * u),
@@ -135,16 +125,6 @@ class GlobalOp:
             else:
                 gs.dssum_into(w, 0)
             self.launches += 2
-            return w
-        if self.fused:
-            pl = self.fused_plan()
-            _lib.call("sf_ax_dssum8_f64", sp.dmat.ctypes.data, _lib.ptr(sp.geom), _lib.ptr(sp.bm),
-                      _lib.ptr(u), _lib.ptr(w), E, self.lam_visc, self.lam_mass,
-                      _lib.ptr(self.inmask) if self.masked else None,
-                      _lib.ptr(self.outsel) if self.masked else None, 2 if self.masked else 0,
-                      *pl.launch_args(), _ex(), st)
-            gs.account_dssum()
-            self.launches += 1
             return w
         if self.masked:
             _lib.call("sf_ax_masked_f64", sp.dmat.ctypes.data, sp.n, _lib.ptr(sp.geom), _lib.ptr(sp.bm),

@@ -70,23 +70,6 @@ def interior_run(iface, E):
     return (lo, hi) if hi - lo >= 2 else None
 
 
-class FusedPlan:
-    """Device schedule of sf_ax_dssum8_f64 (see GatherScatter.fused_plan)."""
-
-    def __init__(self, plan, meta, sync, n_jobs):
-        self.plan = plan              # int32 device words
-        self.meta = meta              # host int64[12]
-        self.sync = sync              # int64 device counters (reserved + one per chunk), never reset
-        self.n_jobs = n_jobs
-        self.epoch = 0                # launches issued with this sync array
-
-    def launch_args(self):
-        """(plan, meta, sync, epoch) for the next sf_ax_dssum8_f64 launch."""
-        ep = self.epoch
-        self.epoch += 1
-        return _lib.ptr(self.plan), self.meta.ctypes.data, _lib.ptr(self.sync), ep
-
-
 class GatherScatter:
     """Direct-stiffness summation QQ^T on device (reference space.py:20-76).
 
@@ -281,116 +264,6 @@ class GatherScatter:
         self.cls_nb, self.cls_eb = nb, eb
         self.cls_bstart = torch.cat([torch.searchsorted(k.contiguous(), edges) for k in keys]).to(torch.int32) \
             if nb else torch.zeros(4, dtype=torch.int32, device=dev)
-
-    def fused_plan(self, perm=None, chunk_pairs=None, lag=None):
-        """Schedule for the fused Ax+dssum kernel (sf_ax_dssum8_f64), single rank.
-
-        Ax work is cut into chunks of ``chunk_pairs`` element pairs (default one
-        half a wave: 148 SMs x 2 blocks).  Every shared gid goes to the chunk of its
-        highest element; within a (chunk, class) the items keep the order of
-        ``perm`` (a cls_perm layout, optionally flagged).  Dssum jobs of chunk c
-        are scheduled right after the Ax jobs of chunk c + lag (default 2)."""
-        import os
-
-        if chunk_pairs is None:
-            chunk_pairs = int(os.environ.get("SEMFLOW_B200_FUSED_CHUNK", 148 * 2))
-        if lag is None:
-            lag = int(os.environ.get("SEMFLOW_B200_FUSED_LAG", 2))
-        lag = max(1, int(lag))
-        if self.comm.world > 1:
-            raise ConfigError("fused Ax+dssum is single-rank (the halo exchange sits between K1 and K2)")
-        if not hasattr(self, "cls_perm"):
-            self._build_classes()
-        perm = self.cls_perm if perm is None else perm
-        dev = self.device
-        E = self.shape[0]
-        nnn = self.P // E
-        cp = int(chunk_pairs or 148 * 4)
-        npairs = (E + 1) // 2
-        K = max(1, (npairs + cp - 1) // cp)
-        ce = 2 * cp                                       # elements per chunk
-        n2, n4, n8 = self.cls_n
-        flat = perm.long() & 0x7fffffff
-        parts, counts, los = [], [], []
-        ITEMS = {2: 1024, 4: 512, 8: 256, 0: 128}
-        o = 0
-        for c, n in ((2, n2), (4, n4), (8, n8)):
-            blk = flat[o:o + c * n].view(n, c)
-            chunk_hi = (blk.max(dim=1).values // nnn) // ce
-            chunk_lo = (blk.min(dim=1).values // nnn) // ce
-            order = torch.sort(chunk_hi, stable=True).indices
-            parts.append(perm[o:o + c * n].view(n, c)[order].reshape(-1))
-            counts.append(torch.bincount(chunk_hi, minlength=K)[:K])
-            los.append(torch.full((K,), 2**31 - 1, dtype=torch.int64, device=dev).scatter_reduce(
-                0, chunk_hi, chunk_lo, "amin"))
-            o += c * n + (self.cls_pad2 if c == 2 else 0)
-        goff = self.cls_gen_off.long()
-        ng = self.cls_n_gen
-        gflat = flat[o:]
-        gcnt = goff[1:] - goff[:-1]
-        item = torch.repeat_interleave(torch.arange(ng, device=dev), gcnt)
-        el = gflat // nnn
-        hi = torch.zeros(ng, dtype=torch.int64, device=dev).scatter_reduce(0, item, el, "amax", include_self=False)
-        lo = torch.zeros(ng, dtype=torch.int64, device=dev).scatter_reduce(0, item, el, "amin", include_self=False)
-        ghi, glo = hi // ce, lo // ce
-        gorder = torch.sort(ghi, stable=True).indices
-        gc = gcnt[gorder]
-        new_off = torch.zeros(ng + 1, dtype=torch.int64, device=dev)
-        if ng:
-            new_off[1:] = torch.cumsum(gc, 0)
-        src = torch.repeat_interleave(goff[:-1][gorder], gc) + (
-            torch.arange(int(new_off[-1]), device=dev) - torch.repeat_interleave(new_off[:-1], gc))
-        gperm = perm[o:][src] if ng else perm[o:o]
-        counts.append(torch.bincount(ghi, minlength=K)[:K])
-        los.append(torch.full((K,), 2**31 - 1, dtype=torch.int64, device=dev).scatter_reduce(0, ghi, glo, "amin"))
-
-        cnt = torch.stack(counts).cpu().numpy()                 # (4, K): pairs, quads, octets, generic
-        lo_c = torch.stack(los).min(dim=0).values.cpu().numpy()
-        lo_c = np.minimum(lo_c, np.arange(K))                    # empty chunks wait on themselves only
-        first = np.concatenate([np.zeros((4, 1), np.int64), np.cumsum(cnt, axis=1)], axis=1)
-        dtab = []
-        dblocks = [[] for _ in range(K)]
-        for ci, cls in enumerate((2, 4, 8, 0)):
-            step = ITEMS[cls]
-            for k in range(K):
-                for s in range(int(first[ci, k]), int(first[ci, k + 1]), step):
-                    dblocks[k].append(len(dtab))
-                    dtab.append((k, cls, s, min(step, int(first[ci, k + 1]) - s)))
-        need = np.array([min(cp, npairs - k * cp) for k in range(K)], dtype=np.int64)
-        sched = []
-
-        def a_chunk(k):
-            sched.extend(range(k * cp, min((k + 1) * cp, npairs)))
-
-        def d_chunk(k):
-            sched.extend(-1 - d for d in dblocks[k])
-
-        for k in range(K):
-            a_chunk(k)
-            if k >= lag:
-                d_chunk(k - lag)
-        for k in range(max(0, K - lag), K):
-            d_chunk(k)
-        segs = [np.asarray(sched, np.int64), np.asarray(dtab, np.int64).reshape(-1), need, lo_c.astype(np.int64)]
-        dev_segs = [parts[0], parts[1], parts[2], new_off.to(torch.int32), gperm]
-        offs, pos = [], 0
-        for a in segs:
-            offs.append(pos)
-            pos += int(a.size)
-            pos += (-pos) % 4                                   # 16-byte alignment for int4 views
-        for t in dev_segs:
-            offs.append(pos)
-            pos += int(t.numel())
-            pos += (-pos) % 4
-        plan = torch.zeros(max(pos, 4), dtype=torch.int32, device=dev)
-        for a, off in zip(segs, offs[:4]):
-            if a.size:
-                plan[off:off + a.size] = torch.from_numpy(a.astype(np.int32)).to(dev)
-        for t, off in zip(dev_segs, offs[4:]):
-            if t.numel():
-                plan[off:off + t.numel()] = t.to(torch.int32)
-        meta = np.array([len(sched), cp, K] + offs, dtype=np.int64)
-        return FusedPlan(plan, meta, torch.zeros(K + 1, dtype=torch.int64, device=dev), len(sched))
 
     def dssum_into(self, v, mode, u=None, perm=None, pre=None, recv=False):
         """In-place dssum of one scalar row v (mode 0 add / 1 avg / 2 masked with u).

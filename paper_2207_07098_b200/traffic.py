@@ -66,7 +66,6 @@ MODELS = {
     "sf_ax_masked_f64": lambda a: _ax(a[6], a[1], a[8], None),
     "sf_ax_pre_f64": lambda a: _ax(a[7], a[1], a[9], a[5]),
     "sf_ax_range_f64": lambda a: _ax(a[9] - a[8], a[1], a[11], a[5]),
-    "sf_ax_dssum8_f64": lambda a: _ax(a[5], 8, a[7], None),      # + the plan's dssum (space.account)
     "sf_mgs_step_f64": lambda a: _mgs(a, 12),
     "sf_mgs_step_peer_f64": lambda a: _mgs(a, 17),
     "sf_glsc3_f64": _glsc3,

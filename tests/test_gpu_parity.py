@@ -180,42 +180,6 @@ def test_ax_dssum_config1_size(cuda, oracle, tgv8):
     assert np.array_equal(sp.gs.add(w).cpu().numpy(), osp.gs.add(w.cpu().numpy()))   # dssum bit-exact
 
 
-@pytest.mark.parametrize("key", ["tgv8", "rotor"])
-@pytest.mark.parametrize("chunk_pairs", [None, 3, 40])
-def test_fused_ax_dssum_bitwise(cuda, golden_spaces, tgv8, key, chunk_pairs):
-    """One-launch Ax+dssum (csrc/axdss.cu) == Ax then dssum, bit for bit, for
-    plain and masked operators, any chunking (rotor: multiplicities up to 10,
-    the generic CSR class)."""
-    from paper_2207_07098_b200 import operators as ops
-    from paper_2207_07098_b200.basis import make_basis
-    from paper_2207_07098_b200.space import build_space
-
-    if key == "tgv8":
-        sp = tgv8
-    else:   # the rotor topology with straight-sided elements at lx = 8
-        import dataclasses
-
-        m = mesh_from_golden(golden_spaces, key)
-        m = dataclasses.replace(m, curved_elem=np.zeros(0, dtype=np.int64),
-                                curved_coords=np.zeros((0,) + m.curved_coords.shape[1:]), geom_order=None)
-        sp = build_space(m, make_basis(7), device="cuda:0")
-        sp.gs._build_classes()
-        assert sp.gs.cls_n_gen > 0
-    g = torch.Generator(device="cuda:0").manual_seed(5)
-    u = torch.randn(sp.shape, dtype=torch.float64, device="cuda:0", generator=g)
-    mask = torch.ones(sp.shape, dtype=torch.float64, device="cuda:0")
-    mask.view(-1)[sp.facet_flat.reshape(-1)] = 0.0
-    for lv, lm, mk in ((1.0, 0.0, None), (1.0, 0.0, mask), (0.01, 50.0, mask)):
-        op = ops.make_global_op(sp, lv, lm, mk)
-        op.fused = True                    # opt-in path (SEMFLOW_B200_FUSED=1)
-        op._plan = sp.gs.fused_plan(op.sh_perm if op.masked else None, chunk_pairs=chunk_pairs)
-        got1 = op(u)
-        got2 = op(u)                       # the counters re-arm between launches
-        op.fused = False
-        want = op(u)
-        assert torch.equal(got1, want) and torch.equal(got2, want)
-
-
 def test_operator_is_deterministic(cuda, tgv8):
     from paper_2207_07098_b200 import operators as ops
 
