@@ -196,8 +196,18 @@ class BoundarySet:
         return axis
 
     def _values(self, fn, xs, t):
+        """Boundary values at time t, evaluated on the host coordinates as the
+        reference does (its evaluators are host numpy callables); the last time's
+        upload is reused -- a step asks for the same t up to three times."""
+        cache = self.__dict__.setdefault("_vcache", {})
+        key = (id(fn), float(t))
+        hit = cache.get(id(fn))
+        if hit is not None and hit[0] == key:
+            return hit[1]
         g = np.asarray(fn(xs[0], xs[1], xs[2], t), dtype=np.float64)
-        return torch.from_numpy(np.ascontiguousarray(g.reshape(3, -1))).to(self.space.device)
+        val = torch.from_numpy(np.ascontiguousarray(g.reshape(3, -1))).to(self.space.device)
+        cache[id(fn)] = (key, val)
+        return val
 
     def apply_dirichlet(self, vel, t):
         """Overwrite constrained velocity points with boundary values (bc.py:218-229)."""
@@ -210,15 +220,19 @@ class BoundarySet:
                 flat[l][pts] = g[l]
         return vel
 
-    def dirichlet_field(self, t):
-        g = torch.zeros((3,) + self.space.shape, dtype=torch.float64, device=self.space.device)
+    def dirichlet_field(self, t, out=None):
+        if out is None:
+            g = torch.zeros((3,) + self.space.shape, dtype=torch.float64, device=self.space.device)
+        else:
+            g = out.zero_()
         self.apply_dirichlet(g, t)
         return g
 
-    def pressure_surface_rhs(self, t):
+    def pressure_surface_rhs(self, t, out=None):
         """sum over Dirichlet facets of phi_i (g . n) dA (bc.py:237-253)."""
         sp = self.space
-        out = torch.zeros(sp.n_points, dtype=torch.float64, device=sp.device)
+        out = torch.zeros(sp.n_points, dtype=torch.float64, device=sp.device) if out is None \
+            else out.view(-1).zero_()
         for (_, it, fn, pts, xs), sc in zip(self.dirichlet, self._dir_scatter):
             g = self._values(fn, xs, t).view(3, *sp.facet_flat[it].shape)
             nrm = sp.facet_normal[it].permute(3, 0, 1, 2)
@@ -226,10 +240,11 @@ class BoundarySet:
             sc.add_into(out, gn.reshape(-1))
         return out.view(sp.shape)
 
-    def surface_flux_rhs(self, field):
+    def surface_flux_rhs(self, field, out=None):
         """sum over velocity-BC facets of phi_i (F . n) dA (bc.py:255-270)."""
         sp = self.space
-        out = torch.zeros(sp.n_points, dtype=torch.float64, device=sp.device)
+        out = torch.zeros(sp.n_points, dtype=torch.float64, device=sp.device) if out is None \
+            else out.view(-1).zero_()
         flat = field.reshape(3, -1)
         for it, sc in zip(self._neumann, self._neu_scatter):
             pts = sp.facet_flat[it]

@@ -188,8 +188,13 @@ def _pcg_fused(op, b, tol, max_iter, precond, dot, x0):
     F = _Fused(op, precond, dot)
     P = F.P
     b = b.contiguous()
+    ws = _device.field_work(op.space)      # work vectors kept across solves (no in-step cudaMalloc)
     x = torch.zeros_like(b) if x0 is None else x0.clone()
-    r = b.clone() if x0 is None else b - op(x)
+    r = ws.like("kr_r", b)
+    if x0 is None:
+        r.copy_(b)
+    else:
+        torch.sub(b, op(x, out=ws.like("kr_ax", b)), out=r)
     # scalar slots: 0 rr, 1-2 rz (ping-pong), 3 pap, 4-5 update outputs (rr, rz_new)
     s = torch.zeros(8, dtype=torch.float64, device=F.dev)
     F.dot(r, r, s[0:1])
@@ -197,8 +202,8 @@ def _pcg_fused(op, b, tol, max_iter, precond, dot, x0):
     res = res0
     if res <= tol:
         return SolveInfo(x, 0, res, res0, True)
-    p = torch.empty_like(b)
-    ap = torch.empty_like(b)
+    p = ws.like("kr_p", b)
+    ap = ws.like("kr_ax", b)
     inv = _lib.ptr(F.invdiag)
     mult = F.mult
     wk = F.w.args()
@@ -394,8 +399,9 @@ def _gmres_pipelined(F, op, b, tol, max_iter, restart):
     dev = F.dev
     mult = F.mult
     wk = F.w.args()
+    ws = _device.field_work(op.space)
     x = torch.zeros_like(b)
-    r = b.clone()
+    r = ws.like("kr_r", b).copy_(b)
     s0 = torch.zeros(4, dtype=torch.float64, device=dev)
     F.dot(r, r, s0[0:1])
     beta = math.sqrt(F.read(s0[0:1])[0])
@@ -520,7 +526,7 @@ def _gmres_pipelined(F, op, b, tol, max_iter, restart):
                 evs[j + 1] = launch(j + 1, V)
         y = _back_substitute(h, g, j_end)
         _lincomb(x, x, V[:j_end], y, F.invdiag, P, dev, F.st)
-        ax = op(x)
+        ax = op(x, out=ws.like("kr_ax", b))
         _lib.call("sf_residual_f64", _lib.ptr(r), _lib.ptr(b), _lib.ptr(ax), mult, P, *wk, _lib.ptr(s0[0:1]), F.st)
         F.comm.sum_(s0[0:1])
         beta = math.sqrt(F.read(s0[0:1])[0])
@@ -536,8 +542,15 @@ def _gmres_fused(op, b, tol, max_iter, restart, precond, dot, x0):
     P = F.P
     dev = F.dev
     b = b.contiguous()
+    ws = _device.field_work(op.space)
     x = torch.zeros_like(b) if x0 is None else x0.clone()
-    r = b.clone() if x0 is None else b - op(x)
+    r = ws.like("kr_r", b)
+    if x0 is None:
+        r.copy_(b)
+    else:
+        torch.sub(b, op(x, out=ws.like("kr_ax", b)), out=r)
+    # Krylov basis kept across solves: restart + 1 fields
+    Vblk = ws.get("gm_V", (restart + 1,) + tuple(b.shape))
     mult = F.mult
     wk = F.w.args()
     inv = _lib.ptr(F.invdiag)
@@ -553,12 +566,12 @@ def _gmres_fused(op, b, tol, max_iter, restart, precond, dot, x0):
     hs = torch.zeros(2 * nh + 4, dtype=torch.float64, device=dev)
     sc = 2 * nh
     hp = lambda i: hs.data_ptr() + 8 * i
-    z = torch.empty_like(b)
+    z = ws.like("kr_p", b)
     total = 0
     converged = False
     while total < max_iter and not converged:
         m = min(restart, max_iter - total)
-        v0 = torch.empty_like(b)
+        v0 = Vblk[0]
         hs[sc:sc + 1].fill_(beta)
         _lib.call("sf_scale_div_f64", _lib.ptr(v0), _lib.ptr(r), None, None, hp(sc), P, F.st)
         vs = [v0]
@@ -567,7 +580,7 @@ def _gmres_fused(op, b, tol, max_iter, restart, precond, dot, x0):
         g[0] = beta
         j_end = 0
         for j in range(m):
-            w = torch.empty_like(b)
+            w = Vblk[j + 1]
             F.apply_precond(vs[j], w, z)
             # MGS sweep: pass 0 = (<w,v0>, <w,w>), pass i = (w -= h_{i-1} v_{i-1}; <w,v_i>),
             # last = (w -= h_j v_j; <w,w>)
@@ -608,7 +621,7 @@ def _gmres_fused(op, b, tol, max_iter, restart, precond, dot, x0):
             vs.append(w)
         y = _back_substitute(h, g, j_end)
         _lincomb(x, x, vs[:j_end], y, F.invdiag, P, dev, F.st)
-        ax = op(x)
+        ax = op(x, out=ws.like("kr_ax", b))
         _lib.call("sf_residual_f64", _lib.ptr(r), _lib.ptr(b), _lib.ptr(ax), mult, P, *wk, _lib.ptr(s0[0:1]), F.st)
         F.comm.sum_(s0[0:1])
         beta = math.sqrt(F.read(s0[0:1])[0])
@@ -689,9 +702,13 @@ class ProjectionSpace:
             self.xs = []
             self.axs = []
             self._solves = 1
-        if not self.xs:
-            return torch.zeros_like(rhs), rhs.clone()
         F = self._fused(apply_a)
+        if not self.xs:
+            if F is None:
+                return torch.zeros_like(rhs), rhs.clone()
+            # the right-hand side handed to the solver lives in the space's work
+            # buffers (valid until the next prepare); x0 is returned fresh
+            return torch.zeros_like(rhs), _device.field_work(F.sp).like("proj_b", rhs).copy_(rhs)
         if F is None:
             x0 = torch.zeros_like(rhs)
             for xi in self.xs:
@@ -702,15 +719,21 @@ class ProjectionSpace:
         F.dots([(xi, rhs) for xi in self.xs], coef)
         x0 = torch.empty_like(rhs)
         _lincomb(x0, None, self.xs, coef, None, F.P, F.dev, F.st)
-        return x0, rhs - apply_a(x0)
+        ws = _device.field_work(F.sp)
+        return x0, torch.sub(rhs, apply_a(x0, out=ws.like("proj_ad", rhs)), out=ws.like("proj_b", rhs))
 
     def absorb(self, dx, apply_a):
         if len(self.xs) >= self.capacity:
             self.xs = []
             self.axs = []
         F = self._fused(apply_a)
-        d = dx.clone()
-        ad = apply_a(d)
+        if F is None:
+            d = dx.clone()
+            ad = apply_a(d)
+        else:
+            ws = _device.field_work(F.sp)
+            d = ws.like("proj_d", dx).copy_(dx)
+            ad = apply_a(d, out=ws.like("proj_ad", dx))
         if F is None:
             a0 = self.dot(d, ad)
             if a0 <= 0.0:

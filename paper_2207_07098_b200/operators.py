@@ -38,18 +38,18 @@ def _ax_local(space, u, lam_visc, lam_mass, out=None):
     return w
 
 
-def laplace_local(space, u):
+def laplace_local(space, u, out=None):
     """Element-local D^T G D u (operators.py:16-18)."""
-    return _ax_local(space, u, 1.0, 0.0)
+    return _ax_local(space, u, 1.0, 0.0, out)
 
 
-def helmholtz_local(space, u, lam_visc, lam_mass):
+def helmholtz_local(space, u, lam_visc, lam_mass, out=None):
     """Element-local lam_visc D^T G D u + lam_mass B u (operators.py:21-29)."""
     if lam_visc <= 0.0:
         raise ValueError(f"lam_visc must be positive, got {lam_visc}")
     if lam_mass < 0.0:
         raise ValueError(f"lam_mass must be non-negative, got {lam_mass}")
-    return _ax_local(space, u, float(lam_visc), float(lam_mass))
+    return _ax_local(space, u, float(lam_visc), float(lam_mass), out)
 
 
 class GlobalOp:
@@ -138,39 +138,40 @@ class GlobalOp:
         self.launches += 2
         return w
 
-    def __call__(self, u):
+    def __call__(self, u, out=None):
         _lib.require_cuda(u)
         u = u.contiguous()
-        return self.apply_into(u, torch.empty_like(u))
+        return self.apply_into(u, torch.empty_like(u) if out is None else out)
 
 
 def make_global_op(space, lam_visc, lam_mass, mask=None):
     return GlobalOp(space, lam_visc, lam_mass, mask)
 
 
-def _deriv(space, op, inp, c=None, sign=1.0, out_comps=3):
+def _deriv(space, op, inp, c=None, sign=1.0, out_comps=3, out=None):
     E, n = space.n_elements, space.n
-    out = torch.empty((out_comps,) + space.shape if out_comps > 1 else space.shape,
-                      dtype=torch.float64, device=space.device)
+    if out is None:
+        out = torch.empty((out_comps,) + space.shape if out_comps > 1 else space.shape,
+                          dtype=torch.float64, device=space.device)
     _lib.call("sf_deriv_f64", op, space.dmat.ctypes.data, n, _lib.ptr(inp.contiguous()),
               _lib.ptr(c.contiguous()) if c is not None else None, _lib.ptr(space.rx), _lib.ptr(out),
               E, float(sign), _ex(), _lib.stream_ptr(space.device))
     return out
 
 
-def grad(space, u):
+def grad(space, u, out=None):
     """Physical gradient (3, E, n, n, n) (operators.py:59-66)."""
-    return _deriv(space, OP_GRAD, u)
+    return _deriv(space, OP_GRAD, u, out=out)
 
 
-def div(space, v):
+def div(space, v, out=None):
     """Pointwise divergence (operators.py:69-76)."""
-    return _deriv(space, OP_DIV, v, out_comps=1)
+    return _deriv(space, OP_DIV, v, out_comps=1, out=out)
 
 
-def curl(space, v):
+def curl(space, v, out=None):
     """Pointwise curl (operators.py:79-88)."""
-    return _deriv(space, OP_CURL, v)
+    return _deriv(space, OP_CURL, v, out=out)
 
 
 def advect_vec(space, c, v, dealias=None, sign=1.0):
@@ -246,9 +247,10 @@ class Dealias:
         return torch.stack([self._advect_fine(cf, v[l]) for l in range(3)])
 
 
-def weak_grad_dot(space, w):
+def weak_grad_dot(space, w, out=None):
     """r_i = (grad phi_i, w) -- Nek cdtp (operators.py:91-105)."""
-    out = torch.empty(space.shape, dtype=torch.float64, device=space.device)
+    if out is None:
+        out = torch.empty(space.shape, dtype=torch.float64, device=space.device)
     _lib.call("sf_cdtp_f64", space.dmat.ctypes.data, space.n, _lib.ptr(w.contiguous()), _lib.ptr(space.rx),
               _lib.ptr(space.bm), _lib.ptr(out), space.n_elements, _ex(), _lib.stream_ptr(space.device))
     return out
