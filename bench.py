@@ -236,7 +236,21 @@ def time_kernels(sp, op, u, reps=20):
 
 #: dram__bytes_read.sum + dram__bytes_write.sum per launch of the MGS pass, from
 #: the ncu --set full capture committed under profiles/ (keyed by mesh size)
-MGS_TRAFFIC = {"64": 4431794000}     # profiles/r1_ncu_full_tgv64.json: 3.355504 + 1.076290 GB
+def _sum_or_none(*xs):
+    return None if any(x is None for x in xs) else sum(xs)
+
+
+def ncu_traffic(kernel, ne):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kernel` on the
+    ne^3 lx=8 box, from the committed ncu --set full summary
+    (profiles/r2_ncu_traffic.json, tools/kernel_probe.py under ncu); None when that
+    size was not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_ncu_traffic.json")) as fh:
+            tab = json.load(fh)["bytes_per_launch"]
+        return tab.get(kernel, {}).get(str(ne))
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def time_mgs(sp, w0, reps=20):
@@ -373,7 +387,9 @@ def bench_poisson(args, world, rank, dev):
                    "points": P, "iterations_per_step": its // args.steps, "l2": "inputs larger than L2",
                    "parallelism": f"replicas x{world}" if world > 1 else "single"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                     "frac": achieved / pk["hbm_gbs"],
+                     "traffic": _sum_or_none(ncu_traffic("ax8t_kernel<0,1,0,0>", ne),
+                                             ncu_traffic("dssum_blk_kernel<2>", ne)),
                      "kernel": "ax8t_kernel (masked) + dssum_blk_kernel",
                      "algorithmic_bytes": nbytes, "us": t_op * 1e6, "ax_us": kt["ax"] * 1e6,
                      "dssum_us": kt["dssum"] * 1e6, "peak_source": src,
@@ -496,7 +512,8 @@ def bench_tgv(args, world, rank, dev):
         P = sp.mesh.n_elements * sp.n ** 3
     else:
         ne = args.ne or (64 if args.warmup + args.steps <= 8 else 48)
-        sp, st, state = tgv_problem(ne, device=dev, comm=comm, precond=args.precond)
+        sp, st, state = tgv_problem(ne, device=dev, comm=comm, precond=args.precond,
+                                    **({"dt": args.dt} if args.dt > 0 else {}))
         P = ne ** 3 * sp.n ** 3            # global points: strong scaling, fixed total work
     for k in range(args.warmup):
         # the projection bases grow by one (x, Ax) pair per solve: reserve the
@@ -610,12 +627,14 @@ def bench_tgv(args, world, rank, dev):
                                       "NCCL halo exchange + all-gather dots")
                                    if world > 1 else "single")},
         "roofline": {"bound": "hbm", "achieved": mgs_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": mgs_gbs / pk["hbm_gbs"], "traffic": MGS_TRAFFIC.get(str(ne)),
+                     "frac": mgs_gbs / pk["hbm_gbs"], "traffic": ncu_traffic("mgs2_kernel<1,1,0,0>", ne),
                      "kernel": "mgs2_kernel<true,true,false,false> (GMRES MGS pass, rank 0)",
                      "algorithmic_bytes": mgs_bytes, "us": t_mgs * 1e6, "peak_source": src,
                      "ax_dssum": {"achieved": achieved, "frac": achieved / pk["hbm_gbs"],
                                   "algorithmic_bytes": nbytes, "us": t_op * 1e6, "ax_us": kt["ax"] * 1e6,
                                   "dssum_us": kt["dssum"] * 1e6,
+                                  "traffic": _sum_or_none(ncu_traffic("ax8t_kernel<0,0,0,0>", ne),
+                                                          ncu_traffic("dssum_blk_kernel<0>", ne)),
                                   "kernel": "ax8t_kernel + dssum_blk_kernel (pressure Poisson operator)"},
                      "step": step_traffic(traffic_sum[:2], traffic_sum[2:], t, args.steps, world,
                                           pk["hbm_gbs"])},
@@ -648,6 +667,10 @@ def main():
     ap.add_argument("--precond", default="jacobi", choices=("jacobi", "schwarz"),
                     help="TGV pressure preconditioner (schwarz: the reference's default, small meshes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dt", type=float, default=0.0,
+                    help="TGV time step (default: the config's literal 1e-2)")
+    ap.add_argument("--no-cfl-matched", action="store_true",
+                    help="skip the second TGV run at the paper's CFL (~0.4)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -681,6 +704,27 @@ def main():
     world, rank, local = dist_setup()
     dev = torch.device("cuda", torch.cuda.current_device())
     line = (bench_poisson if args.workload == "poisson" else bench_tgv)(args, world, rank, dev)
+    if args.workload == "tgv" and not args.no_cfl_matched and args.dt <= 0:
+        # The literal config fixes dt = 1e-2 at every mesh size (CFL 0.2 at 8^3,
+        # ~1.2 at 48^3, ~1.6 at 64^3: past the explicit EXT3 limit, so GMRES hits
+        # its cap).  The same workload at the paper's CFL ~0.4,
+        # dt scaled with the element size, is reported beside it.
+        import gc
+
+        gc.collect()
+        torch.cuda.empty_cache()
+        ne = args.ne or (64 if args.warmup + args.steps <= 8 else 48)
+        a2 = argparse.Namespace(**vars(args))
+        a2.dt = 1e-2 * (0.4 / 0.1985) * 8.0 / ne       # CFL = 0.1985 at 8^3, dt = 1e-2 (golden)
+        l2 = bench_tgv(a2, world, rank, dev)
+        c2 = l2["config"]
+        line["cfl_matched"] = {
+            "dt": a2.dt, "value": l2["value"], "unit": l2["unit"], "ms_per_step": l2["ms_per_step"],
+            "e2e": l2["e2e"], "cfl": c2["cfl"], "p_iterations": c2["p_iterations"],
+            "v_iterations": c2["v_iterations"], "capped_p_solves": c2["capped_p_solves"],
+            "device_allocs_timed_rank0": c2["device_allocs_timed_rank0"], "ke_end": c2["ke_end"],
+            "step_roofline_frac": l2["roofline"]["step"]["frac"], "clocks": l2["clocks"],
+            "note": "same mesh, solver settings and step numbers at dt scaled to CFL ~0.4 (the paper's)"}
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:
             # the same step numbers as the GPU's timed steps, on the 8^3 mesh the
