@@ -45,23 +45,51 @@ def diag_row(d):
                      _fmt(d.div_norm), _fmt(d.wall_time)])
 
 
+class Deferred:
+    """A checkpoint payload produced while the file is written: ``chunks()`` yields
+    host float64 arrays whose concatenation is the array of ``shape``.  Device
+    fields are gathered and copied to the host one chunk at a time, so a
+    checkpoint never holds more than one field on the device or the host."""
+
+    def __init__(self, shape, chunks):
+        self.shape = tuple(int(s) for s in shape)
+        self.chunks = chunks
+
+
+def _host(arr, name):
+    a = arr.detach().cpu().numpy() if isinstance(arr, torch.Tensor) else np.asarray(arr)
+    if a.dtype != np.float64:
+        raise CheckpointError(f"checkpoint arrays must be float64, {name} is {a.dtype}")
+    return np.ascontiguousarray(a, dtype="<f8")
+
+
 def write_checkpoint(path, arrays, meta):
-    """Named float64 arrays + JSON metadata -> checkpoint file (output.py:69-84)."""
-    specs, payload = [], []
+    """Named float64 arrays (or ``Deferred`` payloads) + JSON metadata -> checkpoint
+    file (output.py:69-84).  Payloads are streamed to the file in header order."""
+    specs = []
     for name, arr in arrays.items():
-        a = arr.detach().cpu().numpy() if isinstance(arr, torch.Tensor) else np.asarray(arr)
-        if a.dtype != np.float64:
-            raise CheckpointError(f"checkpoint arrays must be float64, {name} is {a.dtype}")
-        specs.append({"name": name, "shape": list(a.shape)})
-        payload.append(np.ascontiguousarray(a, dtype="<f8"))
+        if not isinstance(arr, Deferred) and not isinstance(arr, torch.Tensor):
+            arr = np.asarray(arr)
+        if not isinstance(arr, Deferred) and arr.dtype not in (np.float64, torch.float64):
+            raise CheckpointError(f"checkpoint arrays must be float64, {name} is {arr.dtype}")
+        specs.append({"name": name, "shape": list(arr.shape)})
     header = json.dumps({"arrays": specs, "meta": meta}, sort_keys=True).encode("utf-8")
     with open(path, "wb") as fh:
         fh.write(MAGIC)
         fh.write(np.array(VERSION, dtype="<u4").tobytes())
         fh.write(np.array(len(header), dtype="<u8").tobytes())
         fh.write(header)
-        for a in payload:
-            fh.write(a.tobytes())
+        for name, arr in arrays.items():
+            if isinstance(arr, Deferred):
+                want, got = int(np.prod(arr.shape)) if arr.shape else 1, 0
+                for chunk in arr.chunks():
+                    a = _host(chunk, name)
+                    got += a.size
+                    fh.write(a.tobytes())
+                if got != want:
+                    raise CheckpointError(f"{name}: produced {got} values for shape {arr.shape}")
+            else:
+                fh.write(_host(arr, name).tobytes())
 
 
 def read_checkpoint(path):
@@ -106,31 +134,42 @@ def _starts(space):
     return _dist.element_ranges(space.mesh.n_elements, space.comm.world)
 
 
-def _global(space, t):
-    return space.comm.gather_elements(t, _starts(space))
-
-
 def _local(space, a):
     e0, e1 = space.e_range
     t = torch.from_numpy(np.ascontiguousarray(a))
     return t[..., e0:e1, :, :, :].contiguous().to(space.device)
 
 
+def _field(sp, t):
+    """Deferred payload of one distributed field: the element slices are gathered to
+    rank 0 (host numpy there, None elsewhere) when the writer reaches it."""
+    shape = tuple(t.shape[:-4]) + (sp.mesh.n_elements,) + tuple(t.shape[-3:])
+    return Deferred(shape, lambda: [sp.comm.gather_to_root(t, _starts(sp))])
+
+
+def _basis(sp, vecs):
+    """Deferred (count, P_global) payload of a projection basis, one vector at a time."""
+    n = sp.mesh.n_elements * int(np.prod(sp.shape[1:]))
+    return Deferred((len(vecs), n),
+                    lambda: (sp.comm.gather_to_root(v, _starts(sp)) for v in vecs))
+
+
 def save_state(path, stepper, state, case="semflow_b200"):
     """Write the runner's checkpoint for (stepper, state) (runner.py:102-126).
-    Collective on several ranks; rank 0 writes the file."""
+    Collective on several ranks: every field is gathered to rank 0 one at a time
+    (never the whole state, never on every rank) and rank 0 streams it to the file."""
     sp = stepper.space
     arrays = {}
     for q, v in enumerate(state.vel_hist):
-        arrays[f"vel_{q}"] = _global(sp, v)
+        arrays[f"vel_{q}"] = _field(sp, v)
     for q, nl in enumerate(state.nl_hist):
-        arrays[f"nl_{q}"] = _global(sp, nl)
-    arrays["prs"] = _global(sp, state.prs)
+        arrays[f"nl_{q}"] = _field(sp, nl)
+    arrays["prs"] = _field(sp, state.prs)
     proj_meta = {}
     for name, proj in stepper._proj.items():
         if proj.xs:
-            arrays[f"proj_{name}_xs"] = torch.stack([_global(sp, x).reshape(-1) for x in proj.xs])
-            arrays[f"proj_{name}_axs"] = torch.stack([_global(sp, a).reshape(-1) for a in proj.axs])
+            arrays[f"proj_{name}_xs"] = _basis(sp, proj.xs)
+            arrays[f"proj_{name}_axs"] = _basis(sp, proj.axs)
         proj_meta[name] = {"count": proj.count, "solves": proj._solves}
     meta = {"case": case, "time": state.time, "nsteps": state.nsteps, "primed": state.primed,
             "n_vel_hist": len(state.vel_hist), "n_nl_hist": len(state.nl_hist),
@@ -138,6 +177,10 @@ def save_state(path, stepper, state, case="semflow_b200"):
             "forcing": stepper.forcing.get_state() if stepper.forcing is not None else None}
     if sp.comm.rank == 0:
         write_checkpoint(path, arrays, meta)
+    else:   # the same gathers, in the writer's order
+        for arr in arrays.values():
+            for _ in arr.chunks():
+                pass
 
 
 def load_state(path, stepper):

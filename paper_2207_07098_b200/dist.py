@@ -110,6 +110,26 @@ class Comm:
         self.dist.all_gather(parts, pad.contiguous(), group=self.group)
         return torch.cat([p[..., :c, :, :, :] for p, c in zip(parts, counts)], dim=-4)
 
+    def gather_to_root(self, t, starts):
+        """Rank 0: the global array (element axis -4) as host numpy; other ranks: None.
+        Only rank 0 receives, and the result goes to the host at once, so a
+        checkpoint holds one global field at a time on rank 0 alone."""
+        if self.world == 1:
+            return t.detach().cpu().numpy()
+        counts = [starts[r + 1] - starts[r] for r in range(self.world)]
+        emax = max(counts)
+        lead = t.shape[:-4]
+        pad = torch.zeros(lead + (emax,) + t.shape[-3:], dtype=t.dtype, device=t.device)
+        pad[..., :t.shape[-4], :, :, :] = t
+        parts = [torch.empty_like(pad) for _ in range(self.world)] if self.rank == 0 else None
+        self.dist.gather(pad, parts, dst=self.dist.get_global_rank(self.group, 0) if self.group else 0,
+                         group=self.group)
+        if self.rank != 0:
+            return None
+        host = [p[..., :c, :, :, :].cpu().numpy() for p, c in zip(parts, counts)]
+        del parts
+        return np.concatenate(host, axis=-4)
+
     def exchange(self, sends, recvs):
         """Post all sends/receives (dict peer -> tensor) and wait (stream-ordered on CUDA)."""
         if self.world == 1 or (not sends and not recvs):

@@ -101,8 +101,11 @@ def _worker(rank, world, port, payload, q):
         # checkpoint gather of element slices (uneven ranges)
         n = round(nnn ** (1.0 / 3.0))
         full = torch.from_numpy(np.stack([u, 2.0 * u, -u]).reshape(3, E, n, n, n))
-        got = comm.gather_elements(full[:, starts[rank]:starts[rank + 1]].contiguous(), starts)
-        q.put((rank, out, part.numpy(), bool(torch.equal(got, full))))
+        mine = full[:, starts[rank]:starts[rank + 1]].contiguous()
+        got = comm.gather_elements(mine, starts)
+        root = comm.gather_to_root(mine, starts)   # checkpoint path: rank 0 only, host numpy
+        ok_root = (root is None) if rank else bool(np.array_equal(root, full.numpy()))
+        q.put((rank, out, part.numpy(), bool(torch.equal(got, full)) and ok_root))
     finally:
         dist.destroy_process_group()
 
