@@ -11,8 +11,9 @@ performance boundary.
 
 Arithmetic is the reference numba lane's, operation for operation and without
 FMA contraction (``exact=1`` in the C ABI), so outputs are bit-identical to
-``semflow.kernels._numba`` (tests/test_lane_parity.py).  Install into the
-reference with :func:`install`.
+``semflow.kernels._numba`` (tests/test_gpu_parity.py lane tests).  Install into
+the reference with :func:`install`; tests/test_ref_hosted.py runs the
+reference's own test suite with this lane installed.
 """
 
 import numpy as np
@@ -135,11 +136,12 @@ def install(kernels_module):
     Returns the previous callables so the caller can restore them.
     """
     saved = {name: getattr(kernels_module, name) for name in _EXPORTS}
-    saved["LANE"] = kernels_module.LANE
+    if hasattr(kernels_module, "LANE"):
+        saved["LANE"] = kernels_module.LANE
+        kernels_module.LANE = LANE
     g = globals()
     for name in _EXPORTS:
         setattr(kernels_module, name, g[name])
-    kernels_module.LANE = LANE
     return saved
 
 

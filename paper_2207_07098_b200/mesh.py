@@ -40,6 +40,13 @@ class Mesh:
     def n_facets(self):
         return self.facet_elem.shape[0]
 
+    def validate(self):
+        """Index ranges, conformity and facet tagging (reference mesh.py:95-147);
+        raises TopologyError, returns self."""
+        from .topology import validate_mesh
+
+        return validate_mesh(self)
+
 
 def gen_box_mesh(extent, counts, tags=None):
     """Cartesian box of affine hexahedra (reference mesh.py:154)."""

@@ -27,6 +27,7 @@ import numpy as np
 import torch
 
 from . import _device, _lib, traffic
+from . import topology as _topo
 from .errors import ConfigError, GeometryError, TopologyError
 
 _FACE_NORMAL_SIGN = (-1.0, 1.0, 1.0, -1.0, -1.0, 1.0)
@@ -425,11 +426,12 @@ def _boundary_point_table(n):
             np.array(cor, dtype=np.int64), np.array(pos, dtype=np.int64))
 
 
-def build_gather_scatter(elements, coords, n):
+def build_gather_scatter(elements, coords, n, tol=None):
     """Bit-exact reference numbering (space.py:265-314) from topology + coordinates.
 
     elements: (E, 8) int64 device tensor of vertex ids; coords: (3, E, n, n, n).
-    """
+    With ``tol`` (the reference's 1e-8 * max element diameter) the topological
+    groups are cross-checked against the geometric tol-pairs (topology.py)."""
     dev = coords.device
     E = elements.shape[0]
     nnn = n ** 3
@@ -490,11 +492,39 @@ def build_gather_scatter(elements, coords, n):
     int_pts = torch.nonzero(is_int).view(-1)
     group[int_pts] = n_bgroups + torch.arange(int_pts.numel(), device=dev)
     n_groups = n_bgroups + int_pts.numel()
+    del is_int, int_pts, grp_of_b, gpt
+    gid = _number_groups(group, n_groups, coords)
+    del group
+    if tol is not None:
+        # the reference groups GEOMETRICALLY (space.py:265-291): raise its
+        # TopologyErrors, and where the topological groups differ from the
+        # tol-graph components (duplicated vertex ids, non-matching curved
+        # faces) number the components instead -- the reference's maps
+        pairs = _topo.coincident_pairs(coords, tol)
+        _topo.check_pairs(pairs, elements, nnn, tol)
+        if not _topo.topology_agrees(gid, pairs, coords, tol):
+            lab = _topo.components(pairs, P)
+            uniq, group = torch.unique(lab, return_inverse=True)
+            gid = _number_groups(group, uniq.numel(), coords)
+            del uniq, group, lab
+        del pairs
+    perm = torch.sort(gid, stable=True).indices
+    n_groups = int(gid.max()) + 1 if gid.numel() else 0
+    counts = torch.bincount(gid, minlength=n_groups)
+    offsets = torch.zeros(n_groups + 1, dtype=torch.int64, device=dev)
+    offsets[1:] = torch.cumsum(counts, 0)
+    return gid, perm, offsets
+
+
+def _number_groups(group, n_groups, coords):
+    """Global ids of point groups in the reference's order (space.py:294-303): the
+    representative of a group is its lowest local point; groups are ordered by
+    representative (the union-find root order), then stably by the exact
+    coordinate bits of the representative, x primary."""
+    dev = group.device
+    P = group.numel()
     rep = torch.full((n_groups,), P, dtype=torch.int64, device=dev)
     rep.scatter_reduce_(0, group, torch.arange(P, device=dev), reduce="amin")
-    del is_int, int_pts, grp_of_b, gpt
-    # order groups by representative (the reference's root order), then a stable
-    # lexsort on the exact coordinate bits of the representative: x primary
     flat = coords.reshape(3, -1)
     order = torch.sort(rep).indices
     for l in (2, 1, 0):
@@ -502,13 +532,7 @@ def build_gather_scatter(elements, coords, n):
         order = order[torch.sort(key, stable=True).indices]
     rank = torch.empty_like(order)
     rank[order] = torch.arange(n_groups, device=dev)
-    gid = rank[group]
-    del rank, order, rep, group
-    perm = torch.sort(gid, stable=True).indices
-    counts = torch.bincount(gid, minlength=n_groups)
-    offsets = torch.zeros(n_groups + 1, dtype=torch.int64, device=dev)
-    offsets[1:] = torch.cumsum(counts, 0)
-    return gid, perm, offsets
+    return rank[group]
 
 
 # --------------------------------------------------------------------------- space
@@ -632,6 +656,7 @@ def build_space(mesh, basis, device=None, comm=None):
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     if dev.type != "cuda":
         raise _lib.LibraryError("build_space needs a CUDA device (no CPU fallback)")
+    _topo.validate_mesh(mesh, dev)                       # space.py:201
     n = basis.n
     E = int(mesh.n_elements)
     nnn = n ** 3
@@ -653,31 +678,38 @@ def build_space(mesh, basis, device=None, comm=None):
         ce = torch.from_numpy(curved).to(dev)
         for l in range(3):
             coords[l][ce] = cc[..., l]
-    # the gather-scatter numbering is global (every rank builds it; it depends on
-    # the exact coordinates of all elements), everything else is per rank
-    gid, perm, offsets = build_gather_scatter(elements, coords, n)
     from . import dist as _dist
 
     comm = comm if comm is not None else _dist.single()
     starts = _dist.element_ranges(E, comm.world)
     e0, e1 = starts[comm.rank], starts[comm.rank + 1]
     El = e1 - e0
-    if comm.world > 1:
-        coords = coords[:, e0:e1].contiguous()
-        torch.cuda.empty_cache()
+    lcoords = coords[:, e0:e1].contiguous() if comm.world > 1 else coords
     rx = torch.empty((3, 3, El, n, n, n), dtype=torch.float64, device=dev)
     jac = torch.empty((El, n, n, n), dtype=torch.float64, device=dev)
     bm = torch.empty_like(jac)
     geom = torch.empty((6, El, n, n, n), dtype=torch.float64, device=dev)
     dh, dptr = _lib.host_f64(basis.dmat)
     wh, wptr = _lib.host_f64(basis.weights)
-    _lib.call("sf_metrics_f64", dptr, wptr, n, _lib.ptr(coords), El, _lib.ptr(rx), _lib.ptr(jac),
+    _lib.call("sf_metrics_f64", dptr, wptr, n, _lib.ptr(lcoords), El, _lib.ptr(rx), _lib.ptr(jac),
               _lib.ptr(bm), _lib.ptr(geom), st)
+    # the reference checks the Jacobian before it numbers the nodes (space.py:224-232)
     bad = jac <= 0.0
-    if bool(bad.any()):
-        e, i, j, k = (int(v) for v in torch.nonzero(bad)[0])
-        raise GeometryError(f"non-positive Jacobian determinant {float(jac[e, i, j, k]):.3e}",
-                            element=e + e0, ref_coords=(basis.points[i], basis.points[j], basis.points[k]))
+    if comm.any(bool(bad.any())):
+        if bool(bad.any()):
+            e, i, j, k = (int(v) for v in torch.nonzero(bad)[0])
+            raise GeometryError(f"non-positive Jacobian determinant {float(jac[e, i, j, k]):.3e}",
+                                element=e + e0,
+                                ref_coords=(basis.points[i], basis.points[j], basis.points[k]))
+        raise GeometryError("non-positive Jacobian determinant on another rank")
+    # the gather-scatter numbering is global (every rank builds it; it depends on
+    # the exact coordinates of all elements), everything else is per rank
+    gid, perm, offsets = build_gather_scatter(elements, coords, n, tol=_topo.gs_tolerance(mesh))
+    del elements
+    if comm.world > 1:
+        coords = lcoords
+        del lcoords
+        torch.cuda.empty_cache()
     gs = GatherScatter(gid, perm, offsets, (El, n, n, n), comm=comm, starts=starts)
     del gid, perm, offsets
     fe = np.asarray(mesh.facet_elem, dtype=np.int64)
