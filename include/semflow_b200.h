@@ -318,6 +318,60 @@ int sf_trilinear_coords_f64(const double* corners, const double* wc, int n, long
 int sf_metrics_f64(const double* d_host, const double* w_host, int n, const double* coords,
                    long long E, double* rx, double* jac, double* bm, double* geom, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Hybrid overlapping Schwarz preconditioner (precond.py:94-250)
+ * ------------------------------------------------------------------------- */
+
+/* Device state of one HybridSchwarz (built by precond.HybridSchwarz; every
+ * pointer is device memory).  G global ids, P local points, nv mesh vertices,
+ * S = padded subdomain size, nnn = n^3. */
+typedef struct SfSchwarz {
+  long long G, P, nv;
+  int nnn, S;
+  const long long* first;       /* (G) local index of each gid's first copy */
+  const long long* gid;         /* (P) */
+  const double* wsqrt;          /* (G) 1 / sqrt(overlap count) */
+  double* rg;                   /* (G) work: gathered residual */
+  double* rw;                   /* (G + 1) work: wsqrt * rg, rw[G] = 0 (padding slot) */
+  const long long* pt_ptr;      /* (nv + 1) restriction rows (vertex -> gids ascending) */
+  const long long* pt_ent;      /* gid * 8 + corner */
+  const double* tw;             /* (nnn, 8) trilinear corner weights */
+  const uint8_t* vfixed;        /* (nv) constrained vertices */
+  double* rc;                   /* (nv) work: restricted residual */
+  int ac_width;                 /* coarse matrix, ELL (nv, ac_width), ascending columns */
+  const int* ac_col;
+  const double* ac_val;
+  const double* ac_inv_diag;
+  double *xc, *cr, *cz, *cp, *cap;   /* (nv) coarse CG vectors; xc = coarse solution */
+  double* cpart;                /* (2 * coarse_blocks) partial sums */
+  unsigned* cbar;               /* (2) grid-barrier words, zero between launches */
+  int coarse_iters, coarse_blocks;
+  const double* inv;            /* (U, S, S) inverses of the distinct subdomain matrices */
+  int n_tiles;                  /* tiles of <= sf_schwarz_tile() same-class subdomains */
+  const int* tile_first;
+  const int* tile_n;
+  const int* tile_cls;
+  const int* order;             /* (E) subdomains grouped by class */
+  const int* sub;               /* (E, S) gids of each subdomain, padded with G */
+  double* sol;                  /* (E, S) work: local solutions */
+  const long long* acc_off;     /* (G + 1) overlap accumulation: gid -> sol slots, */
+  const int* acc_pos;           /*   ascending subdomain */
+  const int* cvert;             /* (E, 8) element corners, ascending vertex id */
+  const uint8_t* ccorn;         /* (E, 8) their corner numbers */
+  const uint8_t* constrained;   /* (G) Dirichlet gids */
+  double* z;                    /* (G) work: assembled correction */
+} SfSchwarz;
+
+/* out = M^-1 r for the hybrid Schwarz preconditioner (HybridSchwarz.__call__,
+ * precond.py:239-250): gather, restriction, fixed-iteration Jacobi-CG coarse
+ * solve (one persistent launch), local subdomain solves, ordered overlap
+ * accumulation + prolongation, scatter.  Stream-ordered, no host sync,
+ * deterministic. */
+int sf_schwarz_apply_f64(const SfSchwarz* s, const double* r, double* out, void* stream);
+/* subdomains per local-solve tile; blocks of the coarse CG launch (= SM count) */
+int sf_schwarz_tile(void);
+int sf_schwarz_coarse_blocks(void);
+
 #ifdef __cplusplus
 }
 #endif

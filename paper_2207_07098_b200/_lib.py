@@ -70,6 +70,9 @@ _SIGS = {
     "sf_halo_wait": [_vp, _i, _vp, _vp, _vp],
     "sf_trilinear_coords_f64": [_vp, _vp, _i, _ll, _vp, _vp],
     "sf_metrics_f64": [_vp, _vp, _i, _vp, _ll, _vp, _vp, _vp, _vp, _vp],
+    "sf_schwarz_apply_f64": [_vp, _vp, _vp, _vp],
+    "sf_schwarz_tile": [],
+    "sf_schwarz_coarse_blocks": [],
 }
 _RESTYPES = {"sf_version": ctypes.c_char_p, "sf_last_error": ctypes.c_char_p}
 
@@ -107,6 +110,39 @@ ACCOUNT = False
 BYTES = [0, 0]
 
 
+#: NVTX ranges around every entry point (SURVEY §5 tracing), named by the
+#: SURVEY §2.2/§2.3 kernel/collective ids: "K2 dssum:sf_dssum_blk_f64".  Off by
+#: default (no host cost); SEMFLOW_B200_NVTX=1 turns them on, e.g. for
+#: ``ncu --nvtx --nvtx-include "K2 dssum/"`` or an nsys timeline.
+NVTX = os.environ.get("SEMFLOW_B200_NVTX", "0") not in ("", "0")
+NVTX_TAGS = {
+    "sf_ax_helm_f64": "K1 ax", "sf_ax_masked_f64": "K1 ax", "sf_ax_pre_f64": "K1 ax",
+    "sf_ax_range_f64": "K1 ax",
+    "sf_dssum_f64": "K2 dssum", "sf_dssum_cls_f64": "K2 dssum", "sf_dssum_blk_f64": "K2 dssum",
+    "sf_gs_gather_f64": "K2 dssum", "sf_gs_scatter_f64": "K2 dssum", "sf_gather_f64": "K2 dssum",
+    "sf_grad_ref_f64": "K3 deriv", "sf_deriv_f64": "K3 deriv", "sf_cfl_f64": "K3 deriv",
+    "sf_cdtp_f64": "K4 cdtp", "sf_apply_axis_f64": "K4 cdtp", "sf_apply_axis3_f64": "K4 cdtp",
+    "sf_glsc3_f64": "K5 glsc3", "sf_glsc3_peer_f64": "K5 glsc3",
+    "sf_cg_init_f64": "K6 pcg", "sf_cg_update_f64": "K6 pcg", "sf_cg_direction_f64": "K6 pcg",
+    "sf_mgs_step_f64": "K7 gmres", "sf_mgs_step_peer_f64": "K7 gmres", "sf_gmres_gate_f64": "K7 gmres",
+    "sf_lincomb_f64": "K7 gmres", "sf_residual_f64": "K7 gmres", "sf_scale_div_f64": "K7 gmres",
+    "sf_bdf_ext_f64": "K8 bdf_ext",
+    "sf_halo_put_f64": "C1 halo", "sf_halo_wait": "C1 halo",
+    "sf_peer_allreduce_f64": "C2 allreduce", "sf_rank_sum_f64": "C2 allreduce",
+    "sf_schwarz_apply_f64": "K9 schwarz",
+}
+
+
+def nvtx_push(label):
+    if NVTX:
+        torch.cuda.nvtx.range_push(label)
+
+
+def nvtx_pop():
+    if NVTX:
+        torch.cuda.nvtx.range_pop()
+
+
 def call(name, *args):
     """Invoke an entry point and raise LibraryError on a nonzero status."""
     global LAUNCHES
@@ -116,7 +152,14 @@ def call(name, *args):
         from . import traffic
 
         traffic.account(name, args, BYTES)
-    st = getattr(lib, name)(*args)
+    if NVTX:
+        torch.cuda.nvtx.range_push(f"{NVTX_TAGS.get(name, 'setup')}:{name}")
+        try:
+            st = getattr(lib, name)(*args)
+        finally:
+            torch.cuda.nvtx.range_pop()
+    else:
+        st = getattr(lib, name)(*args)
     if st != 0:
         msg = lib.sf_last_error().decode(errors="replace")
         raise LibraryError(f"{name} failed (status {st}): {msg}")

@@ -1,0 +1,329 @@
+// Hybrid overlapping Schwarz preconditioner, application (reference
+// precond.py:94-250, HybridSchwarz.__call__ at :239-250).  Five stream-ordered
+// launches, no host synchronisation, CUDA-graph capturable:
+//
+//   gather    rg[g] = r[first copy of g]; rw[g] = wsqrt[g] * rg[g]      (:241-242)
+//   restrict  rc[v] = sum_g (ascending) P[g, v] rg[g]; 0 on fixed v     (:246-247)
+//   coarse    fixed-iteration Jacobi-CG on the vertex problem (:205-230), one
+//             persistent launch with software grid barriers
+//   local     sol_e = A_e^{-1} rw[sub_e] for every subdomain (:243-244): the
+//             explicit inverses of the DISTINCT subdomain matrices (bitwise-equal
+//             matrices are stored once), subdomains of one class in tiles of T
+//             so each inverse row is read once per tile
+//   finalize  z[g] = (sum over subdomains holding g, ascending) sol * wsqrt[g]
+//             + sum_v (ascending) P[g, v] xc[v]; z = rg on constrained g  (:244-249)
+//   scatter   out[p] = z[gid[p]]                                          (:250)
+//
+// The prolongation P (trilinear weights of a point to the corners of its
+// element, precond.py:184-201) is not stored: P[g, v] = tw[p_g, c] with p_g the
+// local index of g's first copy and c the corner of that element at vertex v.
+// All sums run in the reference's order (ascending subdomain / gid / vertex) and
+// in fixed trees for the coarse dots: deterministic, atomics only in the barrier.
+#include <cstring>
+
+#include "common.cuh"
+#include "../../include/semflow_b200.h"
+
+namespace sf {
+
+__global__ void sch_gather_kernel(const double* __restrict__ r, const long long* __restrict__ first,
+                                  const double* __restrict__ wsqrt, long long G, double* __restrict__ rg,
+                                  double* __restrict__ rw) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < G;
+       g += (long long)gridDim.x * blockDim.x) {
+    const double v = r[first[g]];
+    rg[g] = v;
+    rw[g] = __dmul_rn(wsqrt[g], v);
+  }
+}
+
+// rc[v] = sum over entries k of vertex v (gid-ascending) of tw[p_g*8 + c] * rg[g];
+// entry = g * 8 + c.
+__global__ void sch_restrict_kernel(const double* __restrict__ rg, const long long* __restrict__ ptr,
+                                    const long long* __restrict__ ent, const long long* __restrict__ first,
+                                    const double* __restrict__ tw, int nnn, long long nv,
+                                    const uint8_t* __restrict__ vfixed, double* __restrict__ rc) {
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nv;
+       v += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    if (!vfixed[v]) {
+      for (long long k = ptr[v]; k < ptr[v + 1]; ++k) {
+        const long long e = ent[k];
+        const long long g = e >> 3;
+        const int p = (int)(first[g] % nnn);
+        acc = __dadd_rn(acc, __dmul_rn(tw[p * 8 + (int)(e & 7)], rg[g]));
+      }
+    }
+    rc[v] = acc;
+  }
+}
+
+// ----------------------------------------------------------------- coarse CG
+
+struct CoarseArgs {
+  long long nv;
+  int width;                        // ELL row width of the coarse matrix
+  const int* col;                   // (nv, width), padded with the row's own index, value 0
+  const double* val;
+  const double* inv_diag;
+  const double* rc;
+  double* x;                        // output
+  double* r;
+  double* z;
+  double* p;
+  double* ap;
+  double* part;                     // 2 * gridDim partial sums (ping-pong)
+  unsigned* bar;                    // [0] arrivals, [1] exits
+  int iters;
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (true) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+
+// fixed-order block sum of one value per thread; result valid in thread 0
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s = __dadd_rn(s, sh[i]);
+  __syncthreads();
+  return s;
+}
+
+// every block combines the partials of all blocks in block order: the same
+// scalar on every block, a pure function of the data and gridDim
+__device__ __forceinline__ double grid_dot(double mine, double* part, int slot, unsigned* bar,
+                                           unsigned& nbar, double* sh) {
+  const double b = block_sum(mine, sh);
+  if (threadIdx.x == 0) part[slot * gridDim.x + blockIdx.x] = b;
+  nbar += gridDim.x;
+  grid_barrier(bar, nbar);
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (unsigned i = 0; i < gridDim.x; ++i) s = __dadd_rn(s, ((volatile double*)part)[slot * gridDim.x + i]);
+    sh[32] = s;
+  }
+  __syncthreads();
+  const double s = sh[32];
+  __syncthreads();
+  return s;
+}
+
+__global__ void __launch_bounds__(256) sch_coarse_cg_kernel(CoarseArgs a) {
+  __shared__ double sh[33];
+  unsigned nbar = 0;
+  int slot = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  // x = 0; r = rc; z = D r; p = z; rz = <r, z>
+  double loc = 0.0;
+  for (long long v = t0; v < a.nv; v += stride) {
+    const double rv = a.rc[v];
+    const double zv = __dmul_rn(a.inv_diag[v], rv);
+    a.x[v] = 0.0;
+    a.r[v] = rv;
+    a.z[v] = zv;
+    a.p[v] = zv;
+    loc = __dadd_rn(loc, __dmul_rn(rv, zv));
+  }
+  double rz = grid_dot(loc, a.part, slot, a.bar, nbar, sh);
+  slot ^= 1;
+  if (rz > 0.0) {
+    for (int it = 0; it < a.iters; ++it) {
+      // ap = A p; <p, ap>
+      loc = 0.0;
+      for (long long v = t0; v < a.nv; v += stride) {
+        double s = 0.0;
+        const int* c = a.col + v * a.width;
+        const double* w = a.val + v * a.width;
+        for (int k = 0; k < a.width; ++k) s = __dadd_rn(s, __dmul_rn(w[k], __ldcg(a.p + c[k])));
+        a.ap[v] = s;
+        loc = __dadd_rn(loc, __dmul_rn(a.p[v], s));
+      }
+      const double pap = grid_dot(loc, a.part, slot, a.bar, nbar, sh);
+      slot ^= 1;
+      if (!(pap > 0.0)) break;
+      const double alpha = rz / pap;
+      loc = 0.0;
+      for (long long v = t0; v < a.nv; v += stride) {
+        a.x[v] = __dadd_rn(a.x[v], __dmul_rn(alpha, a.p[v]));
+        const double rv = __dsub_rn(a.r[v], __dmul_rn(alpha, a.ap[v]));
+        a.r[v] = rv;
+        const double zv = __dmul_rn(a.inv_diag[v], rv);
+        a.z[v] = zv;
+        loc = __dadd_rn(loc, __dmul_rn(rv, zv));
+      }
+      const double rz_new = grid_dot(loc, a.part, slot, a.bar, nbar, sh);
+      slot ^= 1;
+      if (!(rz_new > 0.0)) break;
+      const double beta = rz_new / rz;
+      for (long long v = t0; v < a.nv; v += stride) a.p[v] = __dadd_rn(a.z[v], __dmul_rn(beta, a.p[v]));
+      rz = rz_new;
+      nbar += gridDim.x;
+      grid_barrier(a.bar, nbar);        // p complete before the next product
+    }
+  }
+  // the last block out resets the barrier words for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(a.bar + 1, 1u) == gridDim.x - 1) {
+      a.bar[0] = 0u;
+      a.bar[1] = 0u;
+      __threadfence();
+    }
+  }
+}
+
+// ----------------------------------------------------------------- local solves
+
+// A tile = up to T subdomains of the same class (same inverse).  order[] lists
+// the subdomains class by class; tile t covers order[tfirst[t] .. +tn[t]).
+template <int T>
+__global__ void __launch_bounds__(256) sch_local_kernel(const double* __restrict__ inv, int S,
+                                                        const int* __restrict__ tfirst,
+                                                        const int* __restrict__ tn,
+                                                        const int* __restrict__ tcls,
+                                                        const int* __restrict__ order,
+                                                        const int* __restrict__ sub,
+                                                        const double* __restrict__ rw,
+                                                        double* __restrict__ sol) {
+  extern __shared__ double rs[];            // T * S
+  const int tile = blockIdx.x;
+  const int n = tn[tile];
+  const int f = tfirst[tile];
+  const double* A = inv + (size_t)tcls[tile] * S * S;
+  for (int idx = threadIdx.x; idx < T * S; idx += blockDim.x) {
+    const int t = idx / S, i = idx - t * S;
+    rs[idx] = t < n ? rw[sub[(size_t)order[f + t] * S + i]] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = warp; i < S; i += nw) {
+    double acc[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) acc[t] = 0.0;
+    const double* row = A + (size_t)i * S;
+    for (int j = lane; j < S; j += 32) {
+      const double aij = row[j];
+#pragma unroll
+      for (int t = 0; t < T; ++t) acc[t] = fma(aij, rs[t * S + j], acc[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+      for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
+    if (lane == 0) {
+#pragma unroll
+      for (int t = 0; t < T; ++t)
+        if (t < n) sol[(size_t)order[f + t] * S + i] = acc[t];
+    }
+  }
+}
+
+// z[g] = con ? rg : (sum_k sol[pos[k]]) * wsqrt + sum over the corners of g's
+// first element in ascending vertex id of tw[p*8+c] * xc[vertex]
+__global__ void sch_finalize_kernel(const double* __restrict__ sol, const long long* __restrict__ off,
+                                    const int* __restrict__ pos, const double* __restrict__ wsqrt,
+                                    const long long* __restrict__ first, int nnn,
+                                    const int* __restrict__ cvert, const uint8_t* __restrict__ ccorn,
+                                    const double* __restrict__ tw, const double* __restrict__ xc,
+                                    const uint8_t* __restrict__ con, const double* __restrict__ rg,
+                                    long long G, double* __restrict__ z) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < G;
+       g += (long long)gridDim.x * blockDim.x) {
+    if (con[g]) { z[g] = rg[g]; continue; }
+    double acc = 0.0;
+    for (long long k = off[g]; k < off[g + 1]; ++k) acc = __dadd_rn(acc, sol[pos[k]]);
+    const long long fp = first[g];
+    const long long e = fp / nnn;
+    const int p = (int)(fp - e * nnn);
+    double pc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c = ccorn[e * 8 + k];
+      pc = __dadd_rn(pc, __dmul_rn(tw[p * 8 + c], xc[cvert[e * 8 + k]]));
+    }
+    z[g] = __dadd_rn(__dmul_rn(acc, wsqrt[g]), pc);
+  }
+}
+
+__global__ void sch_scatter_kernel(const double* __restrict__ z, const long long* __restrict__ gid,
+                                   long long P, double* __restrict__ out) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P;
+       p += (long long)gridDim.x * blockDim.x)
+    out[p] = z[gid[p]];
+}
+
+static unsigned grid_for(long long n) {
+  long long b = (n + 255) / 256;
+  if (b < 1) b = 1;
+  if (b > 148 * 16) b = 148 * 16;
+  return (unsigned)b;
+}
+
+}  // namespace sf
+
+extern "C" {
+
+int sf_schwarz_tile(void) { return 4; }
+
+int sf_schwarz_coarse_blocks(void) {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+int sf_schwarz_apply_f64(const SfSchwarz* s, const double* r, double* out, void* stream) {
+  using namespace sf;
+  if (!s || !r || !out || s->S <= 0 || s->G < 0) {
+    set_error("sf_schwarz_apply_f64: bad arguments");
+    return SF_ERR_ARG;
+  }
+  cudaStream_t st = as_stream(stream);
+  sch_gather_kernel<<<grid_for(s->G), 256, 0, st>>>(r, s->first, s->wsqrt, s->G, s->rg, s->rw);
+  if (int e = check_launch("schwarz gather")) return e;
+  sch_restrict_kernel<<<grid_for(s->nv), 256, 0, st>>>(s->rg, s->pt_ptr, s->pt_ent, s->first, s->tw, s->nnn,
+                                                       s->nv, s->vfixed, s->rc);
+  if (int e = check_launch("schwarz restrict")) return e;
+  CoarseArgs a;
+  a.nv = s->nv; a.width = s->ac_width; a.col = s->ac_col; a.val = s->ac_val; a.inv_diag = s->ac_inv_diag;
+  a.rc = s->rc; a.x = s->xc; a.r = s->cr; a.z = s->cz; a.p = s->cp; a.ap = s->cap; a.part = s->cpart;
+  a.bar = s->cbar; a.iters = s->coarse_iters;
+  sch_coarse_cg_kernel<<<s->coarse_blocks, 256, 0, st>>>(a);
+  if (int e = check_launch("schwarz coarse")) return e;
+  constexpr int T = 4;
+  if (s->n_tiles > 0) {
+    const size_t smem = (size_t)T * s->S * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(sch_local_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      attr = true;
+    }
+    sch_local_kernel<T><<<(unsigned)s->n_tiles, 256, smem, st>>>(s->inv, s->S, s->tile_first, s->tile_n,
+                                                                s->tile_cls, s->order, s->sub, s->rw, s->sol);
+    if (int e = check_launch("schwarz local")) return e;
+  }
+  sch_finalize_kernel<<<grid_for(s->G), 256, 0, st>>>(s->sol, s->acc_off, s->acc_pos, s->wsqrt, s->first,
+                                                      s->nnn, s->cvert, s->ccorn, s->tw, s->xc,
+                                                      s->constrained, s->rg, s->G, s->z);
+  if (int e = check_launch("schwarz finalize")) return e;
+  sch_scatter_kernel<<<grid_for(s->P), 256, 0, st>>>(s->z, s->gid, s->P, out);
+  return check_launch("schwarz scatter");
+}
+
+}  // extern "C"

@@ -69,7 +69,9 @@ class Comm:
             return t
         if t.is_cuda:
             buf = torch.empty(self.world * k, dtype=t.dtype, device=t.device)
+            _lib.nvtx_push("C2 allreduce:all_gather")
             self.dist.all_gather_into_tensor(buf, t.contiguous().view(-1), group=self.group)
+            _lib.nvtx_pop()
             _lib.call("sf_rank_sum_f64", _lib.ptr(buf), self.world, k, _lib.ptr(t), _lib.stream_ptr(t.device))
         else:   # gloo (CPU tests): same rank-order summation
             parts = [torch.empty(k, dtype=t.dtype) for _ in range(self.world)]
@@ -83,7 +85,9 @@ class Comm:
     def max_(self, t):
         if self.world == 1:
             return t
+        _lib.nvtx_push("C3 max:all_reduce")
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        _lib.nvtx_pop()
         self.collectives += 1
         return t
 

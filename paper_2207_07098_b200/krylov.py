@@ -23,7 +23,7 @@ import torch
 from . import _device, _lib
 from .errors import SolverBreakdownError
 from .operators import GlobalOp
-from .precond import BlockJacobi
+from .precond import BlockJacobi, HybridSchwarz
 
 #: Jacobi scaling formed inside the Ax kernel (SEMFLOW_B200_PRE_FUSED=0 materialises z)
 _PRE_FUSED = os.environ.get("SEMFLOW_B200_PRE_FUSED", "1") != "0"
@@ -58,7 +58,10 @@ class _Fused:
         gs = sp.gs
         # weighting: gs.dot -> 1/mult ; None -> plain dot (krylov.py:32-33)
         self.mult = _lib.ptr(gs.mult8) if dot is not None else None
-        self.invdiag = precond.inv_diag if precond is not None else None
+        # a device preconditioner with its own kernels (hybrid Schwarz): z = M v is
+        # formed explicitly and kept per Arnoldi step (flexible GMRES, krylov.py:104-105)
+        self.pc = precond if isinstance(precond, HybridSchwarz) else None
+        self.invdiag = precond.inv_diag if isinstance(precond, BlockJacobi) else None
         self.w = _device.workspace(self.dev)
         self.st = _lib.stream_ptr(self.dev)
         self.comm = sp.comm
@@ -107,6 +110,8 @@ class _Fused:
         return vals
 
     def precond_into(self, v, z):
+        if self.pc is not None:
+            return self.pc.apply_into(v, z)
         if self.invdiag is None:
             z.copy_(v)
         else:
@@ -118,7 +123,10 @@ class _Fused:
         Jacobi at n = 8 the product inv_diag * v is formed inside the Ax kernel as v
         is loaded (same bits, z never written); without a preconditioner A acts on
         v directly (the reference's copy is identical)."""
-        if self.invdiag is None:
+        if self.pc is not None:
+            self.pc.apply_into(v, z)
+            self.op.apply_into(z, w)
+        elif self.invdiag is None:
             self.op.apply_into(v, w)
         elif self.sp.n == 8 and _PRE_FUSED:
             self.op.apply_into(v, w, pre=self.invdiag)
@@ -128,11 +136,16 @@ class _Fused:
         return w
 
 
-def _fusable(apply_a, precond, dot):
+def _fusable(apply_a, precond, dot, device_pc=False):
+    """The fused device path applies: our operator, our inner product, and a
+    Jacobi preconditioner (or, with ``device_pc``, a hybrid Schwarz one) of the
+    same space."""
     if not isinstance(apply_a, GlobalOp):
         return False
-    if precond is not None and not (isinstance(precond, BlockJacobi) and precond.space is apply_a.space):
-        return False
+    if precond is not None:
+        kinds = (BlockJacobi, HybridSchwarz) if device_pc else (BlockJacobi,)
+        if not (isinstance(precond, kinds) and precond.space is apply_a.space):
+            return False
     if dot is not None:
         owner = getattr(dot, "__self__", None)
         if owner is not apply_a.space.gs or getattr(dot, "__name__", "") != "dot":
@@ -239,7 +252,7 @@ def _pcg_fused(op, b, tol, max_iter, precond, dot, x0):
 
 def gmres(apply_a, b, *, tol, max_iter, restart=10, precond=None, dot=None, x0=None):
     """Flexible right-preconditioned restarted GMRES (krylov.py:78-160)."""
-    if _fusable(apply_a, precond, dot):
+    if _fusable(apply_a, precond, dot, device_pc=True):
         return _gmres_fused(apply_a, b, tol, max_iter, restart, precond, dot, x0)
     return _gmres_generic(apply_a, b, tol, max_iter, restart, precond, dot, x0)
 
@@ -347,9 +360,12 @@ class _GraphBuffers:
     """Fixed buffers and the per-step CUDA graphs of the look-ahead GMRES for one
     (operator, preconditioner, restart, size) -- kept on the operator."""
 
-    def __init__(self, b, restart, S, key):
+    def __init__(self, b, restart, S, key, flexible=False):
         self.key = key
         self.V = torch.empty((restart + 1,) + tuple(b.shape), dtype=torch.float64, device=b.device)
+        # flexible GMRES keeps every preconditioned direction z_j (krylov.py:104-105)
+        self.Z = torch.empty((restart,) + tuple(b.shape), dtype=torch.float64, device=b.device) \
+            if flexible else None
         self.blk = torch.zeros((restart, S), dtype=torch.float64, device=b.device)
         self.host = torch.zeros((restart, S), dtype=torch.float64, pin_memory=True)
         self.z = torch.empty_like(b)
@@ -364,7 +380,8 @@ def _graph_buffers(F, op, b, restart, S):
     the captured NVLink reductions and halo exchanges take their call numbers and
     mailbox banks from device counters (peer.cuh, halo.cu), so a replay is the
     same launch sequence as an eager step.  The opt-in fused Ax+dssum launch
-    (axdss.cu) takes a host-side epoch and is never captured."""
+    (axdss.cu) takes a host-side epoch and is never captured.  A hybrid Schwarz
+    preconditioner is captured with the step (its launches take fixed buffers)."""
     if os.environ.get("SEMFLOW_B200_GRAPHS", "1") == "0" or getattr(op, "fused", False):
         return None
     if F.comm.world > 1 and F.comm.peer is None:
@@ -372,11 +389,11 @@ def _graph_buffers(F, op, b, restart, S):
     # every device address a captured step reads: the graphs stay valid only while
     # these are the same tensors (the buffers below are held alive by the cache)
     key = (restart, tuple(b.shape), F.invdiag.data_ptr() if F.invdiag is not None else None, F.mult,
-           F.w.args()[0], _lib.stream_ptr(F.dev))
+           F.w.args()[0], _lib.stream_ptr(F.dev), id(F.pc) if F.pc is not None else None)
     gb = getattr(op, "_gmres_graphs", None)
     if gb is None or gb.key != key:
-        gb = _GraphBuffers(b, restart, S, key)
-        gb.refs = (F.invdiag,)
+        gb = _GraphBuffers(b, restart, S, key, flexible=F.pc is not None)
+        gb.refs = (F.invdiag, F.pc)
         op._gmres_graphs = gb
     return gb
 
@@ -415,12 +432,14 @@ def _gmres_pipelined(F, op, b, tol, max_iter, restart):
     converged = False
     gb = _graph_buffers(F, op, b, restart, S)
     if gb is not None:
-        blk, host, z, Vbuf = gb.blk, gb.host, gb.z, gb.V
+        blk, host, z, Vbuf, Z = gb.blk, gb.host, gb.z, gb.V, gb.Z
     else:
         blk = torch.zeros((restart, S), dtype=torch.float64, device=dev)
         host = torch.zeros((restart, S), dtype=torch.float64, pin_memory=True)
         z = torch.empty_like(b)
         Vbuf = None
+        Z = torch.empty((restart,) + tuple(b.shape), dtype=torch.float64, device=dev) \
+            if F.pc is not None else None
 
     def launch(j, V):
         if gb is not None:
@@ -458,7 +477,7 @@ def _gmres_pipelined(F, op, b, tol, max_iter, restart):
         bl = blk[j]
         bp = lambda i: bl.data_ptr() + 8 * i
         w = torch.empty_like(b) if Vbuf is None else Vbuf[j + 1]
-        F.apply_precond(V[j], w, z)
+        F.apply_precond(V[j], w, z if Z is None else Z[j])
         F.mgs(bl[0:2], _lib.ptr(w), None, None, _lib.ptr(V[0]), None, None, mult, 1)
         for i in range(1, j + 1):
             F.mgs(bl[2 * i:2 * i + 2], _lib.ptr(w), _lib.ptr(V[i - 1]), bp(2 * (i - 1)), _lib.ptr(V[i]),
@@ -525,7 +544,10 @@ def _gmres_pipelined(F, op, b, tol, max_iter, restart):
             if j + 1 < m and j + 1 not in evs:
                 evs[j + 1] = launch(j + 1, V)
         y = _back_substitute(h, g, j_end)
-        _lincomb(x, x, V[:j_end], y, F.invdiag, P, dev, F.st)
+        if Z is None:
+            _lincomb(x, x, V[:j_end], y, F.invdiag, P, dev, F.st)
+        else:                              # x += sum_i y_i z_i (krylov.py:153-154)
+            _lincomb(x, x, [Z[i] for i in range(j_end)], y, None, P, dev, F.st)
         ax = op(x, out=ws.like("kr_ax", b))
         _lib.call("sf_residual_f64", _lib.ptr(r), _lib.ptr(b), _lib.ptr(ax), mult, P, *wk, _lib.ptr(s0[0:1]), F.st)
         F.comm.sum_(s0[0:1])
@@ -567,6 +589,7 @@ def _gmres_fused(op, b, tol, max_iter, restart, precond, dot, x0):
     sc = 2 * nh
     hp = lambda i: hs.data_ptr() + 8 * i
     z = ws.like("kr_p", b)
+    Zblk = ws.get("gm_Z", (restart,) + tuple(b.shape)) if F.pc is not None else None
     total = 0
     converged = False
     while total < max_iter and not converged:
@@ -581,7 +604,7 @@ def _gmres_fused(op, b, tol, max_iter, restart, precond, dot, x0):
         j_end = 0
         for j in range(m):
             w = Vblk[j + 1]
-            F.apply_precond(vs[j], w, z)
+            F.apply_precond(vs[j], w, z if Zblk is None else Zblk[j])
             # MGS sweep: pass 0 = (<w,v0>, <w,w>), pass i = (w -= h_{i-1} v_{i-1}; <w,v_i>),
             # last = (w -= h_j v_j; <w,w>)
             F.mgs(hs[0:2], _lib.ptr(w), None, None, _lib.ptr(vs[0]), None, None, mult, 1)
@@ -620,7 +643,10 @@ def _gmres_fused(op, b, tol, max_iter, restart, precond, dot, x0):
             _lib.call("sf_scale_div_f64", _lib.ptr(w), _lib.ptr(w), None, None, hp(sc), P, F.st)
             vs.append(w)
         y = _back_substitute(h, g, j_end)
-        _lincomb(x, x, vs[:j_end], y, F.invdiag, P, dev, F.st)
+        if Zblk is None:
+            _lincomb(x, x, vs[:j_end], y, F.invdiag, P, dev, F.st)
+        else:
+            _lincomb(x, x, [Zblk[i] for i in range(j_end)], y, None, P, dev, F.st)
         ax = op(x, out=ws.like("kr_ax", b))
         _lib.call("sf_residual_f64", _lib.ptr(r), _lib.ptr(b), _lib.ptr(ax), mult, P, *wk, _lib.ptr(s0[0:1]), F.st)
         F.comm.sum_(s0[0:1])

@@ -83,3 +83,51 @@ def test_schwarz_tgv_steps(cuda, golden_schwarz):
         assert d.p_iterations == row["p_it"] and list(d.v_iterations) == row["v_it"], (d, row)
         assert rel_err(kinetic_energy(sp, state.vel), row["ke"]) < 1e-9
         assert rel_err(enstrophy(sp, state.vel), row["ens"]) < 1e-9
+
+
+def test_schwarz_kernel_vs_host_restatement(cuda):
+    """sf_schwarz_apply_f64 against the numpy restatement of its six launches on
+    the same device-built structures (tests/test_schwarz_setup.py::_emulate)."""
+    from test_schwarz_setup import _emulate
+
+    from paper_2207_07098_b200.basis import make_basis
+    from paper_2207_07098_b200.mesh import gen_box_mesh
+    from paper_2207_07098_b200.precond import HybridSchwarz
+    from paper_2207_07098_b200.space import build_space
+
+    sp = build_space(gen_box_mesh((0.0, 1.0, 0.0, 2.0, 0.0, 1.0), (6, 5, 4)), make_basis(5), device=cuda)
+    mask = torch.ones(sp.shape, dtype=torch.float64, device=cuda)
+    mask.view(-1)[sp.facet_flat.reshape(-1)] = 0.0
+    r = torch.randn(sp.shape, dtype=torch.float64, generator=torch.Generator().manual_seed(3)).to(cuda)
+    for mk in (mask, None):
+        hs = HybridSchwarz(sp, mask=mk, lam_visc=1.0, lam_mass=0.0 if mk is not None else 0.3)
+        got = hs(r).cpu().numpy()
+        want = _emulate(hs, r.cpu().numpy())
+        assert rel_err(got, want) < 1e-13
+        assert torch.equal(hs(r), hs(r))
+        assert hs.n_classes <= 125
+
+
+def test_schwarz_fused_gmres_matches_generic(cuda, monkeypatch):
+    """The fused (graph-captured, flexible) GMRES with hybrid Schwarz against the
+    generic torch loop: identical iteration counts, solutions to rounding."""
+    from paper_2207_07098_b200 import krylov, operators as ops
+    from paper_2207_07098_b200.basis import make_basis
+    from paper_2207_07098_b200.mesh import gen_box_mesh
+    from paper_2207_07098_b200.precond import HybridSchwarz
+    from paper_2207_07098_b200.space import build_space
+
+    sp = build_space(gen_box_mesh((0.0, 1.0, 0.0, 1.0, 0.0, 1.0), (8, 8, 8)), make_basis(7), device=cuda)
+    mask = torch.ones(sp.shape, dtype=torch.float64, device=cuda)
+    mask.view(-1)[sp.facet_flat.reshape(-1)] = 0.0
+    x, y, z = sp.coords
+    f = 3.0 * np.pi ** 2 * torch.sin(np.pi * x) * torch.sin(np.pi * y) * torch.sin(np.pi * z)
+    rhs = mask * sp.gs.add(sp.bm * f)
+    A = ops.make_global_op(sp, 1.0, 0.0, mask)
+    M = HybridSchwarz(sp, mask=mask)
+    fused = krylov.gmres(A, rhs, tol=1e-8, max_iter=200, restart=20, precond=M, dot=sp.gs.dot)
+    again = krylov.gmres(A, rhs, tol=1e-8, max_iter=200, restart=20, precond=M, dot=sp.gs.dot)
+    assert torch.equal(fused.x, again.x)                       # graph replay is deterministic
+    gen = krylov._gmres_generic(A, rhs, 1e-8, 200, 20, M, sp.gs.dot, None)
+    assert fused.iterations == gen.iterations and fused.converged
+    assert rel_err(fused.x.cpu().numpy(), gen.x.cpu().numpy()) < 1e-9
