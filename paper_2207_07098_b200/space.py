@@ -81,52 +81,38 @@ class GatherScatter:
     uint8 multiplicity ``mult8`` for glsc3 weights.
     """
 
-    def __init__(self, gid, perm, offsets, shape, comm=None, starts=None):
+    def __init__(self, gid, perm, offsets, shape, comm=None, starts=None, plan=None, mult8=None, n_gid=None):
         """gid/perm/offsets: the GLOBAL reference-format numbering.  With a
         multi-rank ``comm``, this rank owns elements starts[rank]..starts[rank+1]
-        and its dssum reads the other ranks' copies through a halo exchange."""
+        and its dssum reads the other ranks' copies through a halo exchange.
+        Partitioned build (partition.py): ``gid`` is this rank's slice, perm /
+        offsets are None and ``plan``, ``mult8``, ``n_gid`` come with it."""
         from . import dist as _dist
 
         self.shape = tuple(shape)
         self.device = gid.device
         self.comm = comm if comm is not None else _dist.single()
-        self.n_gid = int(offsets.numel() - 1)
         E = self.shape[0]
         P = E * int(np.prod(self.shape[1:])) if len(self.shape) > 1 else int(gid.numel())
         self.P = P
         if P >= 2**31 - 1:
             raise ConfigError("more than 2^31 local points on one device; partition the mesh")
+        self.plan = None
+        if plan is not None:
+            self.n_gid = int(n_gid)
+            self._init_ranked(gid.contiguous(), plan, mult8.contiguous())
+            return
+        self.n_gid = int(offsets.numel() - 1)
         counts = offsets[1:] - offsets[:-1]
         if counts.numel() and int(counts.max()) > 255:
             raise TopologyError("a global id has more than 255 local copies")
-        self.plan = None
         if self.comm.world > 1:
             nnn = P // E
             r = self.comm.rank
             g0 = starts[r] * nnn
-            self.gid = gid[g0:g0 + P].clone()
-            self.perm = self.offsets = None      # global maps are not kept per rank
-            self.mult8 = counts[self.gid].to(torch.uint8).contiguous()
-            plan = _dist.build_halo_plan(gid, perm, offsets, starts, r, nnn)
-            self.plan = plan
-            self.n_shared = plan.n_shared
-            self.sh_off = plan.sh_off.contiguous()
-            self.sh_perm = plan.sh_perm.contiguous()
-            self.shared_bits = pack_bits((self.mult8 > 1).view(E, nnn))
-            self._sendbuf = torch.empty(int(plan.send_all.numel()), dtype=torch.float64, device=self.device)
-            self._recvbuf = torch.empty(max(plan.n_recv_total, 1), dtype=torch.float64, device=self.device)
-            # NVLink halo (csrc/halo.cu) when the peer-memory path is up; NCCL otherwise
-            import os
-
-            self._ipc = None
-            if self.comm.peer is not None and os.environ.get("SEMFLOW_B200_HALO", "ipc") != "nccl":
-                self._ipc = _dist.HaloIPC(self.comm, plan)
-            self._masked_perm = {}
-            self._mult = None
-            # every host-synchronising derivation done now: an operator application
-            # may first run inside a CUDA-graph capture (krylov._graph_buffers)
-            self._build_classes()
-            self.interior_range()
+            gl = gid[g0:g0 + P].clone()
+            self._init_ranked(gl, _dist.build_halo_plan(gid, perm, offsets, starts, r, nnn),
+                              counts[gl].to(torch.uint8).contiguous())
             return
         self.gid = gid
         self.perm = perm
@@ -155,6 +141,34 @@ class GatherScatter:
         self._mult = None
         if self.device.type == "cuda":
             self._build_classes()
+
+    def _init_ranked(self, gid_loc, plan, mult8):
+        """Multi-rank state: local gid slice, halo plan, multiplicities."""
+        from . import dist as _dist
+
+        E = self.shape[0]
+        nnn = self.P // E
+        self.gid = gid_loc
+        self.perm = self.offsets = None      # global maps are not kept per rank
+        self.mult8 = mult8
+        self.plan = plan
+        self.n_shared = plan.n_shared
+        self.sh_off = plan.sh_off.contiguous()
+        self.sh_perm = plan.sh_perm.contiguous()
+        self.shared_bits = pack_bits((self.mult8 > 1).view(E, nnn))
+        self._sendbuf = torch.empty(int(plan.send_all.numel()), dtype=torch.float64, device=self.device)
+        self._recvbuf = torch.empty(max(plan.n_recv_total, 1), dtype=torch.float64, device=self.device)
+        # NVLink halo (csrc/halo.cu) when the peer-memory path is up; NCCL otherwise
+        self._ipc = None
+        if self.comm.peer is not None and _os.environ.get("SEMFLOW_B200_HALO", "ipc") != "nccl":
+            self._ipc = _dist.HaloIPC(self.comm, plan)
+        self._masked_perm = {}
+        self._mult = None
+        # every host-synchronising derivation done now: an operator application
+        # may first run inside a CUDA-graph capture (krylov._graph_buffers)
+        if self.device.type == "cuda":
+            self._build_classes()
+            self.interior_range()
 
     # ------------------------------------------------------------ properties
     @property
@@ -426,16 +440,17 @@ def _boundary_point_table(n):
             np.array(cor, dtype=np.int64), np.array(pos, dtype=np.int64))
 
 
-def build_gather_scatter(elements, coords, n, tol=None):
-    """Bit-exact reference numbering (space.py:265-314) from topology + coordinates.
-
-    elements: (E, 8) int64 device tensor of vertex ids; coords: (3, E, n, n, n).
-    With ``tol`` (the reference's 1e-8 * max element diameter) the topological
-    groups are cross-checked against the geometric tol-pairs (topology.py)."""
-    dev = coords.device
+def topo_keys(elements, n):
+    """Topological keys (k1, k2) of every boundary point of the given elements and
+    the point's index within the block (element-major): two points coincide in a
+    conforming mesh iff their keys are equal.  Vertices are keyed by their vertex
+    id; edge points by the edge's two vertex ids and the position along the edge
+    counted from the lower id; face points by the face's lowest vertex id, its two
+    neighbours on the face and the in-face position in the frame anchored at the
+    lowest id.  elements: (E, 8) int64 vertex ids (< 2^30)."""
+    dev = elements.device
     E = elements.shape[0]
     nnn = n ** 3
-    P = E * nnn
     m = n - 1
     if E and int(elements.max()) >= 2**30:
         raise ConfigError("vertex ids must be < 2^30")
@@ -469,9 +484,21 @@ def build_gather_scatter(elements, coords, n, tol=None):
     k2 = torch.where(kind_b == 0, torch.zeros_like(va),
                      torch.where(kind_b == 1, e_pos, (f_hi << 16) | (f_P * n + f_Q)))
     del V, four, nA, nB, q1, q2, f_P, f_Q, f_lo, f_hi, e_lo, e_hi, e_pos
-    k1 = k1.reshape(-1)
-    k2 = k2.reshape(-1)
     gpt = (torch.arange(E, device=dev, dtype=torch.int64).view(E, 1) * nnn + lp.view(1, nb)).reshape(-1)
+    return k1.reshape(-1), k2.reshape(-1), gpt
+
+
+def build_gather_scatter(elements, coords, n, tol=None):
+    """Bit-exact reference numbering (space.py:265-314) from topology + coordinates.
+
+    elements: (E, 8) int64 device tensor of vertex ids; coords: (3, E, n, n, n).
+    With ``tol`` (the reference's 1e-8 * max element diameter) the topological
+    groups are cross-checked against the geometric tol-pairs (topology.py)."""
+    dev = coords.device
+    E = elements.shape[0]
+    nnn = n ** 3
+    P = E * nnn
+    k1, k2, gpt = topo_keys(elements, n)
     # lexicographic sort by (k1, k2), ties by point index (stable sorts)
     o = torch.sort(k2, stable=True).indices
     o = o[torch.sort(k1[o], stable=True).indices]
@@ -647,6 +674,31 @@ def _facets(mesh, basis, coords, dev):
     return flat_t, normal, warea
 
 
+def _coords(mesh, basis, elements, c0, c1, dev, st):
+    """Trilinear GLL coordinates of elements c0..c1, curved records applied
+    (space.py:182-192, 204-213): (3, c1 - c0, n, n, n)."""
+    n = basis.n
+    verts = torch.from_numpy(np.ascontiguousarray(mesh.vertices, dtype=np.float64)).to(dev)
+    corners = verts[elements[c0:c1]].contiguous()                          # (Ec, 8, 3)
+    wc = torch.from_numpy(_wc(basis.points)).to(dev)
+    coords = torch.empty((3, c1 - c0, n, n, n), dtype=torch.float64, device=dev)
+    _lib.call("sf_trilinear_coords_f64", _lib.ptr(corners), _lib.ptr(wc), n, c1 - c0, _lib.ptr(coords), st)
+    del corners, verts
+    curved = np.asarray(getattr(mesh, "curved_elem", np.zeros(0, dtype=np.int64)), dtype=np.int64)
+    if curved.size:
+        if mesh.geom_order != basis.order:
+            raise ConfigError(
+                f"mesh curved geometry order {mesh.geom_order} does not match basis order "
+                f"{basis.order}; regenerate the mesh at the solver order")
+        sel = np.nonzero((curved >= c0) & (curved < c1))[0]
+        if sel.size:
+            cc = torch.from_numpy(np.ascontiguousarray(mesh.curved_coords[sel], dtype=np.float64)).to(dev)
+            ce = torch.from_numpy(curved[sel] - c0).to(dev)
+            for l in range(3):
+                coords[l][ce] = cc[..., l]
+    return coords
+
+
 def build_space(mesh, basis, device=None, comm=None):
     """Bind a basis to a mesh on the GPU (reference space.py:195-262).
 
@@ -662,29 +714,17 @@ def build_space(mesh, basis, device=None, comm=None):
     nnn = n ** 3
     st = _lib.stream_ptr(dev)
     elements = torch.from_numpy(np.ascontiguousarray(mesh.elements, dtype=np.int64)).to(dev)
-    verts = torch.from_numpy(np.ascontiguousarray(mesh.vertices, dtype=np.float64)).to(dev)
-    corners = verts[elements].contiguous()                                  # (E, 8, 3)
-    wc = torch.from_numpy(_wc(basis.points)).to(dev)
-    coords = torch.empty((3, E, n, n, n), dtype=torch.float64, device=dev)
-    _lib.call("sf_trilinear_coords_f64", _lib.ptr(corners), _lib.ptr(wc), n, E, _lib.ptr(coords), st)
-    del corners
-    curved = np.asarray(getattr(mesh, "curved_elem", np.zeros(0, dtype=np.int64)), dtype=np.int64)
-    if curved.size:
-        if mesh.geom_order != basis.order:
-            raise ConfigError(
-                f"mesh curved geometry order {mesh.geom_order} does not match basis order "
-                f"{basis.order}; regenerate the mesh at the solver order")
-        cc = torch.from_numpy(np.ascontiguousarray(mesh.curved_coords, dtype=np.float64)).to(dev)
-        ce = torch.from_numpy(curved).to(dev)
-        for l in range(3):
-            coords[l][ce] = cc[..., l]
     from . import dist as _dist
 
     comm = comm if comm is not None else _dist.single()
     starts = _dist.element_ranges(E, comm.world)
     e0, e1 = starts[comm.rank], starts[comm.rank + 1]
     El = e1 - e0
-    lcoords = coords[:, e0:e1].contiguous() if comm.world > 1 else coords
+    # partitioned build: this rank's coordinates and numbering only (partition.py)
+    parted = comm.world > 1 and _os.environ.get("SEMFLOW_B200_GLOBAL_BUILD", "0") != "1"
+    c0, c1 = (e0, e1) if parted else (0, E)
+    coords = _coords(mesh, basis, elements, c0, c1, dev, st)
+    lcoords = coords[:, e0:e1].contiguous() if (comm.world > 1 and not parted) else coords
     rx = torch.empty((3, 3, El, n, n, n), dtype=torch.float64, device=dev)
     jac = torch.empty((El, n, n, n), dtype=torch.float64, device=dev)
     bm = torch.empty_like(jac)
@@ -702,16 +742,37 @@ def build_space(mesh, basis, device=None, comm=None):
                                 element=e + e0,
                                 ref_coords=(basis.points[i], basis.points[j], basis.points[k]))
         raise GeometryError("non-positive Jacobian determinant on another rank")
-    # the gather-scatter numbering is global (every rank builds it; it depends on
-    # the exact coordinates of all elements), everything else is per rank
-    gid, perm, offsets = build_gather_scatter(elements, coords, n, tol=_topo.gs_tolerance(mesh))
+    tol = _topo.gs_tolerance(mesh)
+    gs = None
+    if parted:
+        from . import partition as _part
+
+        gid, plan, mult8, n_gid = _part.partitioned_numbering(elements, coords, n, comm, starts,
+                                                              int(mesh.vertices.shape[0]))
+        # geometric cross-check of this rank's points (topology.py); a mesh whose
+        # topology and geometry disagree falls back to the global build
+        pairs = _topo.coincident_pairs(coords, tol)
+        _topo.check_pairs(pairs, elements[e0:e1], nnn, tol)
+        _, lg = torch.unique(gid, return_inverse=True)
+        agree = _topo.topology_agrees(lg, pairs, coords, tol)
+        del pairs, lg
+        if comm.any(not agree):
+            parted = False
+            coords = _coords(mesh, basis, elements, 0, E, dev, st)
+        else:
+            gs = GatherScatter(gid, None, None, (El, n, n, n), comm=comm, starts=starts, plan=plan,
+                               mult8=mult8, n_gid=n_gid)
+            del gid, plan, mult8
+    if gs is None:
+        # the gather-scatter numbering is global (every rank builds it; it depends on
+        # the exact coordinates of all elements), everything else is per rank
+        gid, perm, offsets = build_gather_scatter(elements, coords, n, tol=tol)
+        if comm.world > 1:
+            coords = coords[:, e0:e1].contiguous()
+            torch.cuda.empty_cache()
+        gs = GatherScatter(gid, perm, offsets, (El, n, n, n), comm=comm, starts=starts)
+        del gid, perm, offsets
     del elements
-    if comm.world > 1:
-        coords = lcoords
-        del lcoords
-        torch.cuda.empty_cache()
-    gs = GatherScatter(gid, perm, offsets, (El, n, n, n), comm=comm, starts=starts)
-    del gid, perm, offsets
     fe = np.asarray(mesh.facet_elem, dtype=np.int64)
     sel = (fe >= e0) & (fe < e1)
     lmesh = _LocalFacets(fe[sel] - e0, np.asarray(mesh.facet_face)[sel])
