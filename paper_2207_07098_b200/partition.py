@@ -113,8 +113,7 @@ def global_ranks(comm, keys, oversample=64):
     sk = keys[o]
     # splitters from evenly spaced samples of every rank
     k = oversample * W
-    pick = torch.linspace(0, max(n - 1, 0), k, device=dev).round().long() if n else \
-        torch.zeros(0, dtype=torch.int64, device=dev)
+    pick = (torch.arange(k, device=dev, dtype=torch.int64) * max(n - 1, 0)) // max(k - 1, 1)
     smp = torch.full((k, 4), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev)
     if n:
         smp[:] = sk[pick]

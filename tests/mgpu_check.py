@@ -2,6 +2,8 @@
 
     torchrun --standalone --nproc-per-node 2 tests/mgpu_check.py [ne] [steps]
 
+0. the partitioned build's gid slice, multiplicities and global id count equal the
+   single-GPU build's (TGV box and the curved mini-rotor mesh);
 1. partitioned dssum (add / avg / masked Poisson operator) on a random field is
    bitwise identical to the single-GPU result, on every rank;
 2. partitioned glsc3 equals the single-GPU value to rounding;
@@ -48,10 +50,16 @@ def main():
     _FULL["space"] = full
     part = build_space(mesh, basis, device=dev, comm=comm)
     e0, e1 = part.e_range
+    nnn = basis.n ** 3
+    # the partitioned build (partition.py, default for N > 1) gives this rank
+    # exactly the single-GPU build's gid slice and multiplicities
+    ok = {}
+    ok["partitioned_gid"] = bool(torch.equal(part.gs.gid, full.gs.gid[e0 * nnn:e1 * nnn]))
+    ok["partitioned_mult"] = bool(torch.equal(part.gs.mult8, full.gs.mult8[e0 * nnn:e1 * nnn]))
+    ok["partitioned_n_gid"] = part.gs.n_gid == full.gs.n_gid
     g = torch.Generator(device="cpu").manual_seed(5)
     u_full = torch.randn(full.shape, generator=g, dtype=torch.float64).to(dev)
     u = u_full[e0:e1].contiguous()
-    ok = {}
     ok["dssum_add"] = bool(torch.equal(part.gs.add(u), full.gs.add(u_full)[e0:e1]))
     ok["dssum_avg"] = bool(torch.equal(part.gs.avg(u), full.gs.avg(u_full)[e0:e1]))
     mask_f = torch.ones(full.shape, dtype=torch.float64, device=dev)
@@ -76,6 +84,7 @@ def main():
     rfull = build_space(rm, make_basis(5), device=dev)
     rpart = build_space(rm, make_basis(5), device=dev, comm=comm)
     q0, q1 = rpart.e_range
+    ok["rotor_partitioned_gid"] = bool(torch.equal(rpart.gs.gid, rfull.gs.gid[q0 * 216:q1 * 216]))
     ru = torch.randn(rfull.shape, generator=g, dtype=torch.float64).to(dev)
     ok["rotor_dssum"] = bool(torch.equal(rpart.gs.add(ru[q0:q1].contiguous()), rfull.gs.add(ru)[q0:q1]))
     del rfull, rpart
