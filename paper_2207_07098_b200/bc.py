@@ -137,8 +137,10 @@ class BoundarySet:
     def __init__(self, space, specs):
         self.space = space
         dev = space.device
-        self.vel_mask = torch.ones((3,) + space.shape, dtype=torch.float64, device=dev)
-        self.prs_mask = torch.ones(space.shape, dtype=torch.float64, device=dev)
+        # 0/1 masks as uint8 (the reference's are float64 0.0/1.0, bc.py:164-201):
+        # the same values in every product (x * 1 = x, x * 0 = +-0), 1 byte per point
+        self.vel_mask = torch.ones((3,) + space.shape, dtype=torch.uint8, device=dev)
+        self.prs_mask = torch.ones(space.shape, dtype=torch.uint8, device=dev)
         self.dirichlet = []   # (tag, facet indices (host), evaluator, flat points (device), host coords)
         self.symmetry = []    # (facet indices, axis, flat points)
         seen = set()
@@ -168,18 +170,18 @@ class BoundarySet:
             elif kind == "symmetry":
                 self.symmetry.append((it, self._symmetry_axis(tag, it), flat))
             elif kind == "outflow":
-                self.prs_mask.view(-1)[flat] = 0.0
+                self.prs_mask.view(-1)[flat] = 0
             else:
                 raise ConfigError(f"boundary kind {kind!r} for tag {tag!r} is not supported on the device path")
         missing = set(space.mesh.tag_names) - seen
         if missing:
             raise ConfigError(f"no boundary condition given for tags {sorted(missing)}")
         for _, axis, flat in self.symmetry:
-            self.vel_mask[axis].view(-1)[flat] = 0.0
+            self.vel_mask[axis].view(-1)[flat] = 0
         for _, _, _, flat, _ in self.dirichlet:
             for l in range(3):
-                self.vel_mask[l].view(-1)[flat] = 0.0
-        self.has_pressure_dirichlet = space.comm.any(bool((self.prs_mask == 0.0).any()))
+                self.vel_mask[l].view(-1)[flat] = 0
+        self.has_pressure_dirichlet = space.comm.any(bool((self.prs_mask == 0).any()))
         self.has_dirichlet = bool(self.dirichlet)
         self._neumann = [it for _, it, _, _, _ in self.dirichlet] + [it for it, _, _ in self.symmetry]
         self._neu_scatter = [_Scatter(space.facet_flat[it].reshape(-1)) for it in self._neumann]

@@ -77,7 +77,8 @@ class GlobalOp:
                 self.inmask = pack_bits(keep)
                 self.outsel = pack_bits(keep) | gs.shared_bits
                 self.sh_perm = gs.masked_perm(keep.reshape(-1))
-            self.mask = m.view(space.shape)
+            # the float mask is not kept: the kernels read the bit-packed words
+            self.mask = mask
         else:
             self.mask = None
         self.launches = 0

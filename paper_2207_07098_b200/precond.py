@@ -22,25 +22,32 @@ def assembled_diagonal(space, lam_visc, lam_mass):
     n = space.n
     d2 = d * d
     dd = torch.diagonal(d).contiguous()
+    # two field buffers + one product temporary (in place; same operation order)
     diag = torch.zeros(space.shape, dtype=torch.float64, device=space.device)
+    tmp = torch.empty_like(diag)
     for m in range(n):        # einsum("mi,emjk->eijk", d2, g0)
-        diag = diag + d2[m].view(1, n, 1, 1) * g[0][:, m:m + 1, :, :]
+        diag.add_(torch.mul(d2[m].view(1, n, 1, 1), g[0][:, m:m + 1, :, :], out=tmp))
     t = torch.zeros_like(diag)
     for m in range(n):        # einsum("mj,eimk->eijk", d2, g3)
-        t = t + d2[m].view(1, 1, n, 1) * g[3][:, :, m:m + 1, :]
-    diag = diag + t
-    t = torch.zeros_like(diag)
+        t.add_(torch.mul(d2[m].view(1, 1, n, 1), g[3][:, :, m:m + 1, :], out=tmp))
+    diag.add_(t)
+    t.zero_()
     for m in range(n):        # einsum("mk,eijm->eijk", d2, g5)
-        t = t + d2[m].view(1, 1, 1, n) * g[5][:, :, :, m:m + 1]
-    diag = diag + t
+        t.add_(torch.mul(d2[m].view(1, 1, 1, n), g[5][:, :, :, m:m + 1], out=tmp))
+    diag.add_(t)
+    del t
     di = dd.view(1, n, 1, 1)
     dj = dd.view(1, 1, n, 1)
     dk = dd.view(1, 1, 1, n)
-    diag = diag + ((2.0 * g[1]) * di) * dj
-    diag = diag + ((2.0 * g[2]) * di) * dk
-    diag = diag + ((2.0 * g[4]) * dj) * dk
-    diag = lam_visc * diag + lam_mass * space.bm
-    return space.gs.add(diag)
+    for gi, a, b in ((g[1], di, dj), (g[2], di, dk), (g[4], dj, dk)):
+        torch.mul(gi, 2.0, out=tmp)
+        tmp.mul_(a).mul_(b)
+        diag.add_(tmp)
+    diag.mul_(lam_visc)
+    torch.mul(space.bm, lam_mass, out=tmp)
+    diag.add_(tmp)
+    del tmp
+    return space.gs.add_(diag)
 
 
 class BlockJacobi:

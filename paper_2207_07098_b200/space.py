@@ -578,6 +578,7 @@ class FunctionSpace:
 
         self.comm = comm if comm is not None else _dist.single()
         self.e_range = e_range if e_range is not None else (0, coords.shape[1])
+        self._coords_h = self._jac_h = None
         self.basis = basis
         self.mesh = mesh
         self.coords = coords
@@ -596,8 +597,24 @@ class FunctionSpace:
         self.dmat = np.ascontiguousarray(basis.dmat, dtype=np.float64)
         self.volume = self.integral(torch.ones(self.shape, dtype=torch.float64, device=self.device))
 
+    # coordinates and Jacobian are set-up fields: release_setup_fields() moves them
+    # to host memory (4 fields of HBM) and they come back to the device on access
+    coords = property(lambda self: self._coords if self._coords is not None else self._coords_h.to(self.device),
+                      lambda self, v: setattr(self, "_coords", v))
+    jac = property(lambda self: self._jac if self._jac is not None else self._jac_h.to(self.device),
+                   lambda self, v: setattr(self, "_jac", v))
+
+    def release_setup_fields(self):
+        """Keep coords and jac in host memory only (a large run's device budget:
+        they are read at set-up -- boundary values, initial fields -- not per step)."""
+        if self._coords is not None:
+            self._coords_h = self._coords.cpu()
+            self._jac_h = self._jac.cpu()
+            self._coords = self._jac = None
+            torch.cuda.empty_cache()
+
     n = property(lambda self: self.basis.n)
-    n_elements = property(lambda self: self.coords.shape[1])
+    n_elements = property(lambda self: self.bm.shape[0])
     shape = property(lambda self: (self.n_elements, self.n, self.n, self.n))
     x = property(lambda self: self.coords[0])
     y = property(lambda self: self.coords[1])
