@@ -1,6 +1,6 @@
 """Device memory of a running step, by owner, in units of one scalar field.
 
-    python tools/mem_breakdown.py <workload tgv|cylinder> <size> [projection on|off] [steps]
+    python tools/mem_breakdown.py <workload tgv|cylinder> <size> [projection on|off] [steps] [jacobi|schwarz]
 
 Builds the problem on cuda:0, runs the steps, then attributes every live tensor
 it can reach (space geometry and maps, FieldWork buffers, stepper state and
@@ -43,11 +43,12 @@ def main():
     size = int(sys.argv[2]) if len(sys.argv) > 2 else 4
     proj = (sys.argv[3] if len(sys.argv) > 3 else "off") == "on"
     steps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+    precond = sys.argv[5] if len(sys.argv) > 5 else "jacobi"
     dev = torch.device("cuda", 0)
     if wl == "cylinder":
         sp, st, state = cylinder_problem(size, device=dev, projection=proj)
     else:
-        sp, st, state = tgv_problem(size, device=dev, projection=proj)
+        sp, st, state = tgv_problem(size, device=dev, projection=proj, precond=precond)
     after_setup = torch.cuda.memory_allocated(dev)
     for _ in range(steps):
         state, _d = st.step(state)
@@ -70,6 +71,15 @@ def main():
             b = nbytes(vv, seen)
             if b:
                 rows[f"stepper.{k}.{kk}"] = b
+    pc = getattr(st, "p_precond", None)
+    if pc is not None and hasattr(pc, "__dict__"):
+        for kk, vv in vars(pc).items():
+            b = nbytes(vv, seen)
+            if b:
+                rows[f"p_precond.{kk}"] = b
+    gb = getattr(getattr(st, "apply_p", None), "_gmres_graphs", None)
+    if gb is not None:
+        rows["gmres graph buffers (V, Z, z)"] = nbytes([gb.V, gb.Z, gb.z], seen)
     for name, pr in getattr(st, "_proj", {}).items():
         rows[f"projection {name}"] = nbytes([pr.xs, pr.axs], seen)
     total = torch.cuda.memory_allocated(dev)
