@@ -337,7 +337,8 @@ typedef struct SfSchwarz {
   const long long* pt_ent;      /* gid * 8 + corner */
   const double* tw;             /* (nnn, 8) trilinear corner weights */
   const uint8_t* vfixed;        /* (nv) constrained vertices */
-  double* rc;                   /* (nv) work: restricted residual */
+  double* rc_part;              /* (nv) work: this rank's restriction (owned gids) */
+  double* rc;                   /* (nv) work: restricted residual (= rc_part on one rank) */
   int ac_width;                 /* coarse matrix, ELL (nv, ac_width), ascending columns */
   const int* ac_col;
   const double* ac_val;
@@ -354,8 +355,10 @@ typedef struct SfSchwarz {
   const int* order;             /* (E) subdomains grouped by class */
   const int* sub;               /* (E, S) gids of each subdomain, padded with G */
   double* sol;                  /* (E, S) work: local solutions */
+  const double* sol_recv;       /* N > 1: the peers' solutions on this rank's gids */
+  long long n_sol;              /* E * S: acc_pos >= n_sol index sol_recv */
   const long long* acc_off;     /* (G + 1) overlap accumulation: gid -> sol slots, */
-  const int* acc_pos;           /*   ascending subdomain */
+  const long long* acc_pos;     /*   ascending global subdomain */
   const int* cvert;             /* (E, 8) element corners, ascending vertex id */
   const uint8_t* ccorn;         /* (E, 8) their corner numbers */
   const uint8_t* constrained;   /* (G) Dirichlet gids */
@@ -366,8 +369,22 @@ typedef struct SfSchwarz {
  * precond.py:239-250): gather, restriction, fixed-iteration Jacobi-CG coarse
  * solve (one persistent launch), local subdomain solves, ordered overlap
  * accumulation + prolongation, scatter.  Stream-ordered, no host sync,
- * deterministic. */
+ * deterministic.  G counts this rank's gids (all gids on one rank). */
 int sf_schwarz_apply_f64(const SfSchwarz* s, const double* r, double* out, void* stream);
+/* The same six stages one by one, for N > 1 where NVLink exchanges go between
+ * them: layer residuals after gather, restriction partials (all-gathered, then
+ * sf_schwarz_rank_sum_f64) after restrict, subdomain solutions after local. */
+int sf_schwarz_gather_f64(const SfSchwarz* s, const double* r, void* stream);
+int sf_schwarz_restrict_f64(const SfSchwarz* s, void* stream);
+int sf_schwarz_rank_sum_f64(const SfSchwarz* s, const double* recv, int rank, int world, void* stream);
+int sf_schwarz_coarse_f64(const SfSchwarz* s, void* stream);
+int sf_schwarz_local_f64(const SfSchwarz* s, void* stream);
+int sf_schwarz_finalize_f64(const SfSchwarz* s, void* stream);
+int sf_schwarz_scatter_f64(const SfSchwarz* s, double* out, void* stream);
+/* out[0..n) = the current bank of a double-banked halo inbox (bank 0 at bank0,
+ * bank stride `stride`, call counter *seq; csrc/halo.cu) */
+int sf_halo_unbank_f64(const double* bank0, const unsigned long long* seq, long long stride, long long n,
+                       double* out, void* stream);
 /* subdomains per local-solve tile; blocks of the coarse CG launch (= SM count) */
 int sf_schwarz_tile(void);
 int sf_schwarz_coarse_blocks(void);

@@ -237,8 +237,9 @@ __global__ void __launch_bounds__(256) sch_local_kernel(const double* __restrict
 
 // z[g] = con ? rg : (sum_k sol[pos[k]]) * wsqrt + sum over the corners of g's
 // first element in ascending vertex id of tw[p*8+c] * xc[vertex]
-__global__ void sch_finalize_kernel(const double* __restrict__ sol, const long long* __restrict__ off,
-                                    const int* __restrict__ pos, const double* __restrict__ wsqrt,
+__global__ void sch_finalize_kernel(const double* __restrict__ sol, const double* __restrict__ sol_recv,
+                                    long long n_sol, const long long* __restrict__ off,
+                                    const long long* __restrict__ pos, const double* __restrict__ wsqrt,
                                     const long long* __restrict__ first, int nnn,
                                     const int* __restrict__ cvert, const uint8_t* __restrict__ ccorn,
                                     const double* __restrict__ tw, const double* __restrict__ xc,
@@ -248,7 +249,10 @@ __global__ void sch_finalize_kernel(const double* __restrict__ sol, const long l
        g += (long long)gridDim.x * blockDim.x) {
     if (con[g]) { z[g] = rg[g]; continue; }
     double acc = 0.0;
-    for (long long k = off[g]; k < off[g + 1]; ++k) acc = __dadd_rn(acc, sol[pos[k]]);
+    for (long long k = off[g]; k < off[g + 1]; ++k) {
+      const long long q = pos[k];            // own subdomains' slots, then the peers' (N > 1)
+      acc = __dadd_rn(acc, q < n_sol ? sol[q] : sol_recv[q - n_sol]);
+    }
     const long long fp = first[g];
     const long long e = fp / nnn;
     const int p = (int)(fp - e * nnn);
@@ -267,6 +271,31 @@ __global__ void sch_scatter_kernel(const double* __restrict__ z, const long long
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P;
        p += (long long)gridDim.x * blockDim.x)
     out[p] = z[gid[p]];
+}
+
+// out[v] = sum over ranks in rank order of the partial restrictions: own partial
+// at position `rank`, the peers' (ascending rank, self skipped) in recv
+__global__ void sch_rank_sum_kernel(const double* __restrict__ own, const double* __restrict__ recv, int rank,
+                                    int world, long long nv, double* __restrict__ out) {
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nv;
+       v += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    int k = 0;
+    for (int q = 0; q < world; ++q) {
+      if (q == rank) acc = __dadd_rn(acc, own[v]);
+      else acc = __dadd_rn(acc, recv[(long long)(k++) * nv + v]);
+    }
+    out[v] = acc;
+  }
+}
+
+// copy the current bank of a double-banked NVLink inbox (csrc/halo.cu) to out
+__global__ void halo_unbank_kernel(const double* __restrict__ bank0, const unsigned long long* __restrict__ seq,
+                                   long long stride, long long n, double* __restrict__ out) {
+  const double* src = bank0 + (long long)(*seq & 1ull) * stride;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = src[i];
 }
 
 static unsigned grid_for(long long n) {
@@ -288,42 +317,108 @@ int sf_schwarz_coarse_blocks(void) {
   return sms;
 }
 
-int sf_schwarz_apply_f64(const SfSchwarz* s, const double* r, double* out, void* stream) {
-  using namespace sf;
-  if (!s || !r || !out || s->S <= 0 || s->G < 0) {
-    set_error("sf_schwarz_apply_f64: bad arguments");
-    return SF_ERR_ARG;
+static int bad(const SfSchwarz* s, const char* what) {
+  if (!s || s->S <= 0 || s->G < 0) {
+    sf::set_error("%s: bad arguments", what);
+    return 1;
   }
-  cudaStream_t st = as_stream(stream);
-  sch_gather_kernel<<<grid_for(s->G), 256, 0, st>>>(r, s->first, s->wsqrt, s->G, s->rg, s->rw);
-  if (int e = check_launch("schwarz gather")) return e;
-  sch_restrict_kernel<<<grid_for(s->nv), 256, 0, st>>>(s->rg, s->pt_ptr, s->pt_ent, s->first, s->tw, s->nnn,
-                                                       s->nv, s->vfixed, s->rc);
-  if (int e = check_launch("schwarz restrict")) return e;
+  return 0;
+}
+
+// stage 1: rg / rw of this rank's nodes (gids with a local copy)
+int sf_schwarz_gather_f64(const SfSchwarz* s, const double* r, void* stream) {
+  using namespace sf;
+  if (bad(s, "sf_schwarz_gather_f64") || !r) return SF_ERR_ARG;
+  sch_gather_kernel<<<grid_for(s->G), 256, 0, as_stream(stream)>>>(r, s->first, s->wsqrt, s->G, s->rg, s->rw);
+  return check_launch("schwarz gather");
+}
+
+// stage 2: restriction of the owned nodes -> rc_part
+int sf_schwarz_restrict_f64(const SfSchwarz* s, void* stream) {
+  using namespace sf;
+  if (bad(s, "sf_schwarz_restrict_f64")) return SF_ERR_ARG;
+  sch_restrict_kernel<<<grid_for(s->nv), 256, 0, as_stream(stream)>>>(s->rg, s->pt_ptr, s->pt_ent, s->first,
+                                                                     s->tw, s->nnn, s->nv, s->vfixed, s->rc_part);
+  return check_launch("schwarz restrict");
+}
+
+// N > 1: rc = rank-order sum of every rank's rc_part (own + received partials)
+int sf_schwarz_rank_sum_f64(const SfSchwarz* s, const double* recv, int rank, int world, void* stream) {
+  using namespace sf;
+  if (bad(s, "sf_schwarz_rank_sum_f64")) return SF_ERR_ARG;
+  sch_rank_sum_kernel<<<grid_for(s->nv), 256, 0, as_stream(stream)>>>(s->rc_part, recv, rank, world, s->nv, s->rc);
+  return check_launch("schwarz rank sum");
+}
+
+// stage 3: coarse Jacobi-CG (one persistent launch) rc -> xc
+int sf_schwarz_coarse_f64(const SfSchwarz* s, void* stream) {
+  using namespace sf;
+  if (bad(s, "sf_schwarz_coarse_f64")) return SF_ERR_ARG;
   CoarseArgs a;
   a.nv = s->nv; a.width = s->ac_width; a.col = s->ac_col; a.val = s->ac_val; a.inv_diag = s->ac_inv_diag;
   a.rc = s->rc; a.x = s->xc; a.r = s->cr; a.z = s->cz; a.p = s->cp; a.ap = s->cap; a.part = s->cpart;
   a.bar = s->cbar; a.iters = s->coarse_iters;
-  sch_coarse_cg_kernel<<<s->coarse_blocks, 256, 0, st>>>(a);
-  if (int e = check_launch("schwarz coarse")) return e;
+  sch_coarse_cg_kernel<<<s->coarse_blocks, 256, 0, as_stream(stream)>>>(a);
+  return check_launch("schwarz coarse");
+}
+
+// stage 4: local subdomain solves sol = inv rw[sub]
+int sf_schwarz_local_f64(const SfSchwarz* s, void* stream) {
+  using namespace sf;
+  if (bad(s, "sf_schwarz_local_f64")) return SF_ERR_ARG;
   constexpr int T = 4;
-  if (s->n_tiles > 0) {
-    const size_t smem = (size_t)T * s->S * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(sch_local_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      attr = true;
-    }
-    sch_local_kernel<T><<<(unsigned)s->n_tiles, 256, smem, st>>>(s->inv, s->S, s->tile_first, s->tile_n,
-                                                                s->tile_cls, s->order, s->sub, s->rw, s->sol);
-    if (int e = check_launch("schwarz local")) return e;
+  if (s->n_tiles <= 0) return SF_OK;
+  const size_t smem = (size_t)T * s->S * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sch_local_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    attr = true;
   }
-  sch_finalize_kernel<<<grid_for(s->G), 256, 0, st>>>(s->sol, s->acc_off, s->acc_pos, s->wsqrt, s->first,
-                                                      s->nnn, s->cvert, s->ccorn, s->tw, s->xc,
-                                                      s->constrained, s->rg, s->G, s->z);
-  if (int e = check_launch("schwarz finalize")) return e;
-  sch_scatter_kernel<<<grid_for(s->P), 256, 0, st>>>(s->z, s->gid, s->P, out);
+  sch_local_kernel<T><<<(unsigned)s->n_tiles, 256, smem, as_stream(stream)>>>(
+      s->inv, s->S, s->tile_first, s->tile_n, s->tile_cls, s->order, s->sub, s->rw, s->sol);
+  return check_launch("schwarz local");
+}
+
+// stage 5: ordered overlap sums (own + received solutions) + prolongation -> z
+int sf_schwarz_finalize_f64(const SfSchwarz* s, void* stream) {
+  using namespace sf;
+  if (bad(s, "sf_schwarz_finalize_f64")) return SF_ERR_ARG;
+  sch_finalize_kernel<<<grid_for(s->G), 256, 0, as_stream(stream)>>>(
+      s->sol, s->sol_recv, s->n_sol, s->acc_off, s->acc_pos, s->wsqrt, s->first, s->nnn, s->cvert, s->ccorn, s->tw,
+      s->xc, s->constrained, s->rg, s->G, s->z);
+  return check_launch("schwarz finalize");
+}
+
+// stage 6: out[p] = z[node of p]
+int sf_schwarz_scatter_f64(const SfSchwarz* s, double* out, void* stream) {
+  using namespace sf;
+  if (bad(s, "sf_schwarz_scatter_f64") || !out) return SF_ERR_ARG;
+  sch_scatter_kernel<<<grid_for(s->P), 256, 0, as_stream(stream)>>>(s->z, s->gid, s->P, out);
   return check_launch("schwarz scatter");
+}
+
+// single rank: the six stages back to back
+int sf_schwarz_apply_f64(const SfSchwarz* s, const double* r, double* out, void* stream) {
+  int e;
+  if ((e = sf_schwarz_gather_f64(s, r, stream))) return e;
+  if ((e = sf_schwarz_restrict_f64(s, stream))) return e;
+  if ((e = sf_schwarz_coarse_f64(s, stream))) return e;
+  if ((e = sf_schwarz_local_f64(s, stream))) return e;
+  if ((e = sf_schwarz_finalize_f64(s, stream))) return e;
+  return sf_schwarz_scatter_f64(s, out, stream);
+}
+
+// copy the current bank of an NVLink halo inbox to out (n doubles)
+int sf_halo_unbank_f64(const double* bank0, const unsigned long long* seq, long long stride, long long n,
+                       double* out, void* stream) {
+  using namespace sf;
+  if (n <= 0) return SF_OK;
+  if (!bank0 || !seq || !out) {
+    set_error("sf_halo_unbank_f64: bad arguments");
+    return SF_ERR_ARG;
+  }
+  halo_unbank_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(bank0, seq, stride, n, out);
+  return check_launch("halo unbank");
 }
 
 }  // extern "C"

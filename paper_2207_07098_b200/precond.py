@@ -81,17 +81,21 @@ def _face_layer(n, face):
     return base[tuple(sl)].ravel()
 
 
-def element_matrices(space, lam_visc, lam_mass, batch=64, elems=None):
+def element_matrices(space, lam_visc, lam_mass, batch=64, elems=None, geom=None, bm=None):
     """Dense element matrices A_e (len(elems), n^3, n^3) on the device: the
     identity basis pushed through the element kernel with the element's metric
     replicated (precond.py:71-91) -- the same arithmetic as the matrix-free
-    operator.  ``elems``: element indices (default all)."""
+    operator.  ``elems``: element indices (default all) into ``geom`` (6, E, n^3)
+    / ``bm`` (E, n^3) (default the space's own)."""
     from . import _lib
     from .operators import _ex
 
-    n, E = space.n, space.n_elements
+    n = space.n
     nn = n ** 3
     dev = space.device
+    geom = space.geom.view(6, -1, nn) if geom is None else geom
+    bm = space.bm.view(-1, nn) if bm is None else bm
+    E = bm.shape[0]
     el = torch.arange(E, device=dev) if elems is None else torch.as_tensor(elems, device=dev).long()
     M = int(el.numel())
     mats = torch.empty((M, nn, nn), dtype=torch.float64, device=dev)
@@ -100,11 +104,11 @@ def element_matrices(space, lam_visc, lam_mass, batch=64, elems=None):
         i1 = min(M, i0 + batch)
         B = i1 - i0
         sel = el[i0:i1]
-        g = space.geom.view(6, E, nn)[:, sel].repeat_interleave(nn, dim=1).contiguous()
-        bm = space.bm.view(E, nn)[sel].repeat_interleave(nn, dim=0).contiguous()
+        g = geom[:, sel].repeat_interleave(nn, dim=1).contiguous()
+        b = bm[sel].repeat_interleave(nn, dim=0).contiguous()
         u = eye.repeat(B, 1).contiguous()
         w = torch.empty_like(u)
-        _lib.call("sf_ax_helm_f64", space.dmat.ctypes.data, n, _lib.ptr(g), _lib.ptr(bm), _lib.ptr(u), _lib.ptr(w),
+        _lib.call("sf_ax_helm_f64", space.dmat.ctypes.data, n, _lib.ptr(g), _lib.ptr(b), _lib.ptr(u), _lib.ptr(w),
                   B * nn, float(lam_visc), float(lam_mass), _ex(), _lib.stream_ptr(dev))
         mats[i0:i1] = w.view(B, nn, nn).transpose(1, 2)
     return mats
@@ -136,6 +140,29 @@ def _classes(h):
     if not bool((h[rep[inv], 1] == h[:, 1]).all()):
         return rows.clone(), rows.clone()
     return inv, rep
+
+
+def _lexsort2(a, b):
+    """Permutation sorting by a, then b (stable)."""
+    o = torch.sort(b, stable=True).indices
+    return o[torch.sort(a[o], stable=True).indices]
+
+
+def _segment_sums(keys, vals):
+    """(unique keys ascending, sum of each key's values in input order)."""
+    o = torch.sort(keys, stable=True).indices
+    ks, vs = keys[o], vals[o]
+    newk = torch.ones_like(ks, dtype=torch.bool)
+    newk[1:] = ks[1:] != ks[:-1]
+    seg = torch.cumsum(newk.to(torch.int64), 0) - 1
+    nseg = int(seg[-1]) + 1 if seg.numel() else 0
+    sstart = torch.nonzero(newk).view(-1)
+    slen = torch.bincount(seg, minlength=nseg)
+    out = torch.zeros(nseg, dtype=vals.dtype, device=vals.device)
+    for j in range(int(slen.max()) if nseg else 0):
+        m_ = slen > j
+        out[m_] = out[m_] + vs[sstart[m_] + j]
+    return ks[sstart], out
 
 
 def _face_neighbours(mesh, dev):
@@ -178,7 +205,7 @@ class _SchwarzStruct(ctypes.Structure):
         ("first", ctypes.c_void_p), ("gid", ctypes.c_void_p), ("wsqrt", ctypes.c_void_p),
         ("rg", ctypes.c_void_p), ("rw", ctypes.c_void_p),
         ("pt_ptr", ctypes.c_void_p), ("pt_ent", ctypes.c_void_p), ("tw", ctypes.c_void_p),
-        ("vfixed", ctypes.c_void_p), ("rc", ctypes.c_void_p),
+        ("vfixed", ctypes.c_void_p), ("rc_part", ctypes.c_void_p), ("rc", ctypes.c_void_p),
         ("ac_width", ctypes.c_int), ("ac_col", ctypes.c_void_p), ("ac_val", ctypes.c_void_p),
         ("ac_inv_diag", ctypes.c_void_p),
         ("xc", ctypes.c_void_p), ("cr", ctypes.c_void_p), ("cz", ctypes.c_void_p), ("cp", ctypes.c_void_p),
@@ -187,15 +214,43 @@ class _SchwarzStruct(ctypes.Structure):
         ("inv", ctypes.c_void_p), ("n_tiles", ctypes.c_int),
         ("tile_first", ctypes.c_void_p), ("tile_n", ctypes.c_void_p), ("tile_cls", ctypes.c_void_p),
         ("order", ctypes.c_void_p), ("sub", ctypes.c_void_p), ("sol", ctypes.c_void_p),
+        ("sol_recv", ctypes.c_void_p), ("n_sol", ctypes.c_longlong),
         ("acc_off", ctypes.c_void_p), ("acc_pos", ctypes.c_void_p),
         ("cvert", ctypes.c_void_p), ("ccorn", ctypes.c_void_p), ("constrained", ctypes.c_void_p),
         ("z", ctypes.c_void_p),
     ]
 
 
+class _Plan:
+    """Send/receive lists of one exchange (the fields dist.HaloIPC reads)."""
+
+    def __init__(self, send_idx, n_recv, dev):
+        self.send_idx = {q: t for q, t in send_idx.items() if t.numel()}
+        self.n_recv = {q: int(k) for q, k in n_recv.items() if k}
+        self.peers = sorted(set(self.send_idx) | set(self.n_recv))
+        self.recv_off, off = {}, 0
+        for q in self.peers:
+            self.recv_off[q] = off
+            off += self.n_recv.get(q, 0)
+        self.n_recv_total = off
+        self.send_off, so = {}, 0
+        for q in self.peers:
+            self.send_off[q] = so
+            so += int(self.send_idx[q].numel()) if q in self.send_idx else 0
+        self.send_all = (torch.cat([self.send_idx[q] for q in self.peers if q in self.send_idx]).to(torch.int32)
+                         if self.send_idx else torch.zeros(0, dtype=torch.int32, device=dev))
+
+
+def _alltoallv(comm, lists, width, dtype, dev):
+    from .partition import alltoallv
+
+    return alltoallv(comm, lists, width, dtype, dev)
+
+
 class HybridSchwarz:
     """Overlapping Schwarz subdomain solves plus a trilinear coarse solve
-    (precond.py:94-250), applied by hand-written kernels (csrc/schwarz.cu).
+    (precond.py:94-250), applied by hand-written kernels (csrc/schwarz.cu), on
+    one rank or across ranks.
 
     Subdomain e = element e's global ids plus the first GLL layer inside each
     face neighbour (precond.py:126-139); its matrix sums the dense element
@@ -208,17 +263,25 @@ class HybridSchwarz:
     Elements are in one metric class when their geometric factors agree to
     ``share_bits`` bits relative to the element's scale (40: ~1e-12; np.linspace
     boxes differ in the last bits only); ``share_bits=None`` shares only
-    bitwise-equal geometry.  A box mesh has <= 27 distinct subdomains whatever
-    its size, so Schwarz runs at 32^3 and 64^3; an unstructured mesh stores one
-    S x S inverse per element, the reference's O(E S^2).
+    bitwise-equal geometry.  A box mesh has <= 5^3 distinct subdomains whatever
+    its size; an unstructured mesh stores one S x S inverse per element, the
+    reference's O(E S^2).
 
-    One application (``apply_into``) is sf_schwarz_apply_f64: six launches, no
-    host synchronisation (CUDA-graph capturable; the fused GMRES captures it).
-    The overlap sums and the coarse restriction/prolongation run in the
-    reference's order; subdomain solves use the explicit inverse instead of LU
-    back-substitution and the 10-iteration coarse Jacobi-CG uses a sparse
-    vertex matrix, so one application agrees with the reference to rounding
-    (~1e-13) and Krylov iteration counts are the reference's.  Single rank.
+    Across ranks (N > 1) every rank treats its own elements' subdomains.  The
+    elements a subdomain reaches on other ranks are all vertex neighbours of the
+    rank's elements: their gid rows, metrics and masks are fetched once.  Each
+    application exchanges over NVLink (dist.HaloIPC): the weighted residual of
+    the other ranks' first layers after the gather, the restriction partials
+    (summed in rank order on every rank; the coarse solve is replicated), and the
+    subdomain solutions on gids held by other ranks, which every holder adds in
+    ascending global subdomain order -- the reference's order.
+
+    One application (``apply_into``) is stream-ordered with no host
+    synchronisation (CUDA-graph capturable; the fused GMRES captures it).
+    Subdomain solves use the explicit inverse instead of LU back-substitution and
+    the 10-iteration coarse Jacobi-CG a sparse vertex matrix, so one application
+    agrees with the reference to rounding (~1e-13) and Krylov iteration counts
+    are the reference's.
     """
 
     TILE = 4
@@ -226,129 +289,213 @@ class HybridSchwarz:
     def __init__(self, space, mask=None, lam_visc=1.0, lam_mass=0.0, coarse_iters=10, chunk=2048,
                  share_bits=40):
         from . import _lib
+        from . import dist as _dist
         from .errors import ConfigError
 
         lib = _lib.load()
         gs = space.gs
-        if space.comm.world > 1:
-            raise ConfigError("the hybrid Schwarz preconditioner is single-rank on the device path")
-        if gs.perm is None:
-            raise ConfigError("HybridSchwarz needs the global gather-scatter maps")
+        comm = space.comm
+        W, rk = comm.world, comm.rank
         self.space = space
         self.coarse_iters = int(coarse_iters)
         dev = space.device
-        n, E = space.n, space.n_elements
+        n, El = space.n, space.n_elements
         nn = n ** 3
-        G = gs.n_gid
-        P = E * nn
-        gid_e = gs.gid.view(E, nn)
-        constrained = torch.zeros(G, dtype=torch.bool, device=dev)
-        if mask is not None:
-            m = torch.as_tensor(mask, dtype=torch.float64, device=dev).reshape(-1)
-            constrained[gs.gid[m == 0.0]] = True
+        P = El * nn
         mesh = space.mesh
+        Eg = int(mesh.n_elements)
+        e0, e1 = space.e_range
+        nv = int(mesh.vertices.shape[0])
         elements = torch.as_tensor(np.ascontiguousarray(mesh.elements), dtype=torch.int64, device=dev)
+        keep = (torch.ones(P, dtype=torch.bool, device=dev) if mask is None else
+                torch.as_tensor(mask, device=dev).reshape(-1) != 0)
+        starts = _dist.element_ranges(Eg, W)
+        BIG = 1 << 62
 
-        # ---- subdomains: own gids + first layer inside each face neighbour
+        # ---- X: own elements + the other ranks' vertex neighbours, ascending global id
+        if W == 1:
+            gx = torch.arange(El, device=dev)
+            i0 = 0
+            gid_X = gs.gid.view(El, nn)
+            geom_X = space.geom.view(6, El, nn)
+            bm_X = space.bm.view(El, nn)
+            keep_X = keep.view(El, nn)
+            owner_X = torch.zeros(El, dtype=torch.int64, device=dev)
+        else:
+            vl = torch.zeros(nv, dtype=torch.bool, device=dev)
+            vl[elements[e0:e1].reshape(-1)] = True
+            touch = vl[elements].any(dim=1)
+            touch[e0:e1] = True
+            gx = torch.nonzero(touch).view(-1)
+            i0 = int(torch.searchsorted(gx, torch.tensor([e0], device=dev)))
+            st_t = torch.tensor(starts, dtype=torch.int64, device=dev)
+            owner_X = torch.searchsorted(st_t, gx, right=True) - 1
+            remote = owner_X != rk
+            H = gx[remote]
+            Ho = owner_X[remote]
+            req = {q: H[Ho == q].view(-1, 1) for q in range(W) if q != rk}
+            got = _alltoallv(comm, req, 1, torch.int64, dev)             # what the peers need from me
+            lo = lambda t: (t.view(-1) - e0)
+            rep_i = {q: gs.gid.view(El, nn)[lo(t)] for q, t in got.items()}
+            rep_f = {q: torch.cat([space.geom.view(6, El, nn)[:, lo(t)].permute(1, 0, 2).reshape(-1, 6 * nn),
+                                   space.bm.view(El, nn)[lo(t)],
+                                   keep.view(El, nn)[lo(t)].to(torch.float64)], dim=1) for q, t in got.items()}
+            ans_i = _alltoallv(comm, rep_i, nn, torch.int64, dev)
+            ans_f = _alltoallv(comm, rep_f, 8 * nn, torch.float64, dev)
+            NX = int(gx.numel())
+            gid_X = torch.empty((NX, nn), dtype=torch.int64, device=dev)
+            fX = torch.empty((NX, 8 * nn), dtype=torch.float64, device=dev)
+            gid_X[i0:i0 + El] = gs.gid.view(El, nn)
+            fX[i0:i0 + El] = torch.cat([space.geom.view(6, El, nn).permute(1, 0, 2).reshape(El, 6 * nn),
+                                       space.bm.view(El, nn), keep.view(El, nn).to(torch.float64)], dim=1)
+            ridx = torch.nonzero(remote).view(-1)
+            for q in ans_i:
+                sel = ridx[Ho == q]
+                gid_X[sel] = ans_i[q]
+                fX[sel] = ans_f[q]
+            geom_X = fX[:, :6 * nn].reshape(NX, 6, nn).permute(1, 0, 2).contiguous()
+            bm_X = fX[:, 6 * nn:7 * nn].contiguous()
+            keep_X = fX[:, 7 * nn:] != 0.0
+            del fX, rep_i, rep_f, ans_i, ans_f
+        NX = int(gx.numel())
+
+        # ---- subdomains (global gids): own gids + first layer inside each face neighbour
         nbr, nface = _face_neighbours(mesh, dev)
+        nbr, nface = nbr[e0:e1], nface[e0:e1]
         layer = torch.as_tensor(np.stack([_face_layer(n, f) for f in range(6)]), device=dev)
-        parts = [gid_e]
+        parts = [gid_X[i0:i0 + El]]
         for f in range(6):
             e2 = nbr[:, f]
-            idx = layer[nface[:, f].clamp(min=0)]                        # (E, n^2)
-            vals = torch.gather(gid_e[e2.clamp(min=0)], 1, idx)
-            parts.append(torch.where((e2 >= 0).view(E, 1), vals, torch.full_like(vals, G)))
-        s = torch.sort(torch.cat(parts, dim=1), dim=1).values
-        dup = torch.zeros_like(s, dtype=torch.bool)
-        dup[:, 1:] = s[:, 1:] == s[:, :-1]
-        s = torch.sort(torch.where(dup, torch.full_like(s, G), s), dim=1).values
-        size = (s < G).sum(dim=1)
+            x2 = torch.searchsorted(gx, e2.clamp(min=0)).clamp(max=NX - 1)
+            idx = layer[nface[:, f].clamp(min=0)]                        # (El, n^2)
+            vals = torch.gather(gid_X[x2], 1, idx)
+            parts.append(torch.where((e2 >= 0).view(El, 1), vals, torch.full_like(vals, BIG)))
+        s_ = torch.sort(torch.cat(parts, dim=1), dim=1).values
+        dup = torch.zeros_like(s_, dtype=torch.bool)
+        dup[:, 1:] = s_[:, 1:] == s_[:, :-1]
+        s_ = torch.sort(torch.where(dup, torch.full_like(s_, BIG), s_), dim=1).values
+        size = (s_ < BIG).sum(dim=1)
         S = int(size.max())
-        sub = s[:, :S].contiguous()
-        del s, dup, parts
+        subg = s_[:, :S].contiguous()
+        del s_, dup, parts
         self.S = S
-        valid = sub < G
-        overlap = torch.bincount(sub[valid], minlength=G)
-        # 1/sqrt of the (small integer) counts from a host table: IEEE sqrt as
-        # numpy computes it (torch's CPU sqrt is not always correctly rounded)
-        tab = 1.0 / np.sqrt(np.arange(1, int(overlap.max()) + 2, dtype=np.float64))
-        self.wsqrt = torch.as_tensor(tab, device=dev)[overlap - 1].contiguous()   # every gid is covered
 
-        # ---- elements touching each gid (ascending), for the candidate lists
-        key = torch.unique(gid_e.reshape(-1) * E + torch.arange(E, device=dev).repeat_interleave(nn))
-        ge_g, ge_e = key // E, key % E
-        ge_off = torch.zeros(G + 1, dtype=torch.int64, device=dev)
-        ge_off[1:] = torch.cumsum(torch.bincount(ge_g, minlength=G), 0)
+        # ---- node space: gids with an own copy first (ascending), then the other
+        #      ranks' layer gids grouped by the rank that provides them
+        loc_nodes = torch.unique(gid_X[i0:i0 + El])
+        Lloc = int(loc_nodes.numel())
+        vsub = subg[subg < BIG]
+        pos = torch.searchsorted(loc_nodes, vsub).clamp(max=Lloc - 1)
+        rem = torch.unique(vsub[loc_nodes[pos] != vsub])
+        Xflat = gid_X.reshape(-1)
+        if rem.numel():
+            # provider: the rank of the first X element holding the gid
+            pr = torch.searchsorted(rem, Xflat).clamp(max=rem.numel() - 1)
+            hit = rem[pr] == Xflat
+            xmin = torch.full((rem.numel(),), NX, dtype=torch.int64, device=dev)
+            xmin.scatter_reduce_(0, pr[hit], torch.arange(NX, device=dev).repeat_interleave(nn)[hit], reduce="amin")
+            prov = owner_X[xmin]
+            o = _lexsort2(prov, rem)
+            rem, prov = rem[o], prov[o]
+        else:
+            prov = torch.zeros(0, dtype=torch.int64, device=dev)
+        L = Lloc + int(rem.numel())
+        self.G, self.L = Lloc, L
+        if rem.numel():
+            rem_sorted, rem_ord = torch.sort(rem)
+
+        def node_of(g, unused):
+            """global gid -> node index (``unused`` where it is not a node)."""
+            p1 = torch.searchsorted(loc_nodes, g).clamp(max=Lloc - 1)
+            out = torch.where(loc_nodes[p1] == g, p1, torch.full_like(g, unused))
+            if rem.numel():
+                p2 = torch.searchsorted(rem_sorted, g).clamp(max=rem.numel() - 1)
+                out = torch.where((out == unused) & (rem_sorted[p2] == g), Lloc + rem_ord[p2], out)
+            return out
+
+        valid = subg < BIG
+        sub = torch.where(valid, node_of(subg.clamp(max=BIG - 1), L), torch.full_like(subg, L))
+        sub = torch.sort(sub, dim=1).values                     # sorted node ids, pad L
+        gidn_X = node_of(Xflat, L + 1).view(NX, nn)
+        del Xflat, subg
+
+        # constrained nodes: a copy (within X, which holds every copy) with mask 0
+        con_n = torch.zeros(L + 2, dtype=torch.int64, device=dev)
+        con_n.index_add_(0, gidn_X.reshape(-1), (~keep_X).reshape(-1).to(torch.int64))
+        constrained = con_n[:L] > 0
+        del con_n
+
+        # ---- X elements touching each node (ascending X index), for the candidates
+        key = torch.unique(gidn_X.reshape(-1) * NX + torch.arange(NX, device=dev).repeat_interleave(nn))
+        ge_g, ge_e = key // NX, key % NX
+        ge_off = torch.zeros(L + 3, dtype=torch.int64, device=dev)
+        ge_off[1:] = torch.cumsum(torch.bincount(ge_g, minlength=L + 2), 0)
         del key, ge_g
 
-        # ---- metric classes of the elements: geometry equal to ``share_bits`` bits
+        # ---- metric classes of the X elements: geometry equal to ``share_bits`` bits
         #      relative to the element's own scale (default 40: ~1e-12) shares one
         #      element matrix -- np.linspace meshes differ elementwise only in the
         #      last bits; share_bits=None hashes the exact bits
         hw = _hash_weights(7 * nn + 2, dev, 1)
-        eh = torch.empty((E, 2), dtype=torch.int64, device=dev)
-        gmax = float(space.geom.abs().max()) or 1.0
-        bmax = float(space.bm.abs().max()) or 1.0
-        for e0 in range(0, E, 4096):
-            e1 = min(E, e0 + 4096)
-            ge = space.geom.view(6, E, nn)[:, e0:e1].permute(1, 0, 2).reshape(e1 - e0, 6 * nn)
-            be = space.bm.view(E, nn)[e0:e1]
+        eh = torch.empty((NX, 2), dtype=torch.int64, device=dev)
+        gmax = float(geom_X.abs().max()) or 1.0
+        bmax = float(bm_X.abs().max()) or 1.0
+        for x0 in range(0, NX, 4096):
+            x1 = min(NX, x0 + 4096)
+            ge = geom_X[:, x0:x1].permute(1, 0, 2).reshape(x1 - x0, 6 * nn)
+            be = bm_X[x0:x1]
             if share_bits is None:
                 q = torch.cat([ge, be], dim=1).contiguous().view(torch.int64)
-                q = torch.cat([q, torch.zeros((e1 - e0, 2), dtype=torch.int64, device=dev)], dim=1)
+                q = torch.cat([q, torch.zeros((x1 - x0, 2), dtype=torch.int64, device=dev)], dim=1)
             else:
                 sc = float(2 ** int(share_bits))
                 sg = ge.abs().amax(dim=1, keepdim=True).clamp_min(1e-300)
                 sb = be.abs().amax(dim=1, keepdim=True).clamp_min(1e-300)
                 q = torch.cat([torch.round(ge / sg * sc), torch.round(be / sb * sc),
                                torch.round(sg / gmax * sc), torch.round(sb / bmax * sc)], dim=1).to(torch.int64)
-            eh[e0:e1] = _row_hash(q, hw)
+            eh[x0:x1] = _row_hash(q, hw)
         ecls, erep = _classes(eh)
         del eh
 
-        # ---- subdomain signatures (candidate classes, landing positions, Dirichlet, size)
+        # ---- subdomain signatures (candidate classes, landing slots, Dirichlet, size)
         bmg = None
         cw = None
-        sig = torch.empty((E, 2), dtype=torch.int64, device=dev)
+        sig = torch.empty((El, 2), dtype=torch.int64, device=dev)
         sub_canon = torch.empty_like(sub)
-        cand_all = []
-        for r0 in range(0, E, chunk):
-            r1 = min(E, r0 + chunk)
-            cand, bi, sub_c = self._candidates(sub[r0:r1], gid_e, ge_off, ge_e, G, E)
+        for r0 in range(0, El, chunk):
+            r1 = min(El, r0 + chunk)
+            cand, bi, sub_c = self._candidates(sub[r0:r1], gidn_X, ge_off, ge_e, L, NX)
             sub_canon[r0:r1] = sub_c
             R, C = cand.shape
             if cw is None or cw.shape[1] < C * nn:
                 cw = _hash_weights(max(C, 64) * nn, dev, 2)
                 sw = [_hash_weights(max(C, 64), dev, 3), _hash_weights(S, dev, 4), _hash_weights(1, dev, 5)]
-            con = (constrained[sub_c.clamp(max=G - 1)] & (sub_c < G)).to(torch.int64)
+            con = (constrained[sub_c.clamp(max=L - 1)] & (sub_c < L)).to(torch.int64)
             cc = torch.where(cand >= 0, ecls[cand.clamp(min=0)] + 1, torch.zeros_like(cand))
             # fixed positions whatever the chunk's candidate count: padding
             # candidates and points outside the subdomain contribute 0
             h = (_row_hash((bi + 1).reshape(R, C * nn), cw[:, :C * nn])
                  + _row_hash(cc, sw[0][:, :C]) + _row_hash(con, sw[1][:, :S])
                  + size[r0:r1].view(R, 1) * sw[2][:, :1].view(1, 2))
-            whole = (size[r0:r1] == G) & (con.sum(dim=1) == 0)
+            whole = (size[r0:r1] == gs.n_gid) & (con.sum(dim=1) == 0)
             if bool(whole.any()):       # the 1e-8 mass shift makes these unique
+                if W > 1:
+                    raise ConfigError("HybridSchwarz: a subdomain covering the whole mesh needs one rank")
                 h[whole] += torch.arange(r0, r1, device=dev)[whole].view(-1, 1) * 0x9E3779B97F4A7C15
             sig[r0:r1] = h
-            cand_all.append(cand)
         scls, srep = _classes(sig)
         U = int(srep.numel())
         self.n_classes = U
         del sig
 
-        # ---- element matrices of the metric classes in use, then the distinct
-        #      subdomain matrices (assembled in ascending candidate order) and
-        #      their inverses
-        Cmax = max(c.shape[1] for c in cand_all)
-        cand_full = torch.full((E, Cmax), -1, dtype=torch.int64, device=dev)
-        o = 0
-        for c in cand_all:
-            cand_full[o:o + c.shape[0], :c.shape[1]] = c
-            o += c.shape[0]
-        del cand_all
-        used = torch.unique(ecls[cand_full[srep][cand_full[srep] >= 0]])
-        emats_u = element_matrices(space, lam_visc, lam_mass, elems=erep[used])
+        # ---- element matrices of the metric classes in use, the distinct subdomain
+        #      matrices (assembled in ascending candidate order) and their inverses
+        used = []
+        for u0 in range(0, U, 256):
+            cand_r, _, _ = self._candidates(sub[srep[u0:u0 + 256]], gidn_X, ge_off, ge_e, L, NX)
+            used.append(torch.unique(ecls[cand_r[cand_r >= 0]]))
+        used = torch.unique(torch.cat(used))
+        emats_u = element_matrices(space, lam_visc, lam_mass, elems=erep[used], geom=geom_X, bm=bm_X)
         slot_of = torch.full((int(erep.numel()),), -1, dtype=torch.int64, device=dev)
         slot_of[used] = torch.arange(used.numel(), device=dev)
         inv = torch.empty((U, S, S), dtype=torch.float64, device=dev)
@@ -356,7 +503,7 @@ class HybridSchwarz:
         for u0 in range(0, U, 64):
             u1 = min(U, u0 + 64)
             reps = srep[u0:u1]
-            cand, bi, sub_r = self._candidates(sub[reps], gid_e, ge_off, ge_e, G, E)
+            cand, bi, sub_r = self._candidates(sub[reps], gidn_X, ge_off, ge_e, L, NX)
             B = reps.numel()
             A = torch.zeros((B, S + 1, S + 1), dtype=torch.float64, device=dev)   # slot S: sink
             bix = torch.where(bi >= 0, bi, torch.full_like(bi, S))
@@ -370,16 +517,15 @@ class HybridSchwarz:
                 bk = bix[:, k]
                 A.index_put_((rows, bk.view(B, nn, 1), bk.view(B, 1, nn)), blk, accumulate=True)
             A = A[:, :S, :S].contiguous()
-            con = constrained[sub_r.clamp(max=G - 1)] & (sub_r < G)
+            con = constrained[sub_r.clamp(max=L - 1)] & (sub_r < L)
             for b in range(B):
-                e = int(reps[b])
-                sz = int(size[e])
+                sz = int(size[int(reps[b])])
                 fx = torch.nonzero(con[b]).view(-1)
                 if fx.numel():
                     A[b, fx, :] = 0.0
                     A[b, :, fx] = 0.0
                     A[b, fx, fx] = 1.0
-                elif sz == G:
+                elif sz == gs.n_gid:
                     if bmg is None:
                         bmg = gs.gather_unique(gs.add(space.bm))
                     A[b, ar[:sz], ar[:sz]] += 1e-8 * bmg[sub_r[b, :sz]]
@@ -393,68 +539,130 @@ class HybridSchwarz:
         # ---- local-solve tiles: subdomains grouped by class, T per tile
         order = torch.sort(scls, stable=True).indices
         cls_sorted = scls[order]
-        newc = torch.ones(E, dtype=torch.bool, device=dev)
+        newc = torch.ones(El, dtype=torch.bool, device=dev)
         newc[1:] = cls_sorted[1:] != cls_sorted[:-1]
         start_of = torch.cumsum(newc.to(torch.int64), 0) - 1
         cstart = torch.nonzero(newc).view(-1)
-        within = torch.arange(E, device=dev) - cstart[start_of]
-        tile_head = (within % self.TILE) == 0
-        tf = torch.nonzero(tile_head).view(-1)
-        cend = torch.cat([cstart[1:], torch.tensor([E], device=dev)])[start_of[tf]]
+        within = torch.arange(El, device=dev) - cstart[start_of]
+        tf = torch.nonzero((within % self.TILE) == 0).view(-1)
+        cend = torch.cat([cstart[1:], torch.tensor([El], device=dev)])[start_of[tf]]
         self.tile_first = tf.to(torch.int32).contiguous()
         self.tile_n = torch.clamp(cend - tf, max=self.TILE).to(torch.int32).contiguous()
         self.tile_cls = cls_sorted[tf].to(torch.int32).contiguous()
         self.order = order.to(torch.int32).contiguous()
         self.sub = sub_canon.to(torch.int32).contiguous()
-        valid = sub_canon < G
+        valid = sub_canon < L
         del sub, sub_canon
-
-        # ---- overlap accumulation: gid -> (subdomain, slot), ascending subdomain
-        if E * S >= 2 ** 31:
+        if El * S >= 2 ** 31:
             raise ConfigError("HybridSchwarz: E * S exceeds int32 slot indexing; partition the mesh")
+
+        # ---- overlap accumulation: node -> (global subdomain, slot), ascending
+        #      subdomain; on several ranks the other ranks' solutions on this rank's
+        #      gids arrive through an exchange (plan "sol")
         vi = torch.nonzero(valid.view(-1)).view(-1)
-        gsub = self.sub.view(-1)[vi].long()
-        o = torch.sort(gsub * E + vi // S).indices
-        self.acc_pos = vi[o].to(torch.int32).contiguous()
-        self.acc_off = torch.zeros(G + 1, dtype=torch.int64, device=dev)
-        self.acc_off[1:] = torch.cumsum(torch.bincount(gsub, minlength=G), 0)
-        del vi, gsub, o, valid
+        nsub = self.sub.view(-1)[vi].long()
+        gsub = vi // S + e0                                     # global subdomain id
+        ent_node, ent_sub, ent_pos = [nsub], [gsub], [vi]
+        n_sol = El * S
+        self.plan_sol = None
+        gid_of_node = torch.cat([loc_nodes, rem])
+        if W > 1:
+            has = torch.zeros((W, L + 2), dtype=torch.bool, device=dev)
+            for q in range(W):
+                has[q, gidn_X[owner_X == q].reshape(-1)] = True
+            send_meta, send_flat = {}, {}
+            for q in range(W):
+                if q == rk:
+                    continue
+                m_ = has[q][nsub]
+                if not bool(m_.any()):
+                    continue
+                gq, sq, fq = gid_of_node[nsub[m_]], gsub[m_], vi[m_]
+                o = _lexsort2(gq, sq)
+                send_meta[q] = torch.stack([gq[o], sq[o]], dim=1)
+                send_flat[q] = fq[o]
+            recv_meta = _alltoallv(comm, send_meta, 2, torch.int64, dev)
+            self.plan_sol = _Plan(send_flat, {q: t.shape[0] for q, t in recv_meta.items()}, dev)
+            for q, t in recv_meta.items():
+                nd = node_of(t[:, 0], L)
+                if bool((nd >= Lloc).any()):
+                    raise ConfigError("HybridSchwarz: a received solution names a gid this rank does not hold")
+                ent_node.append(nd)
+                ent_sub.append(t[:, 1])
+                ent_pos.append(n_sol + self.plan_sol.recv_off[q] + torch.arange(t.shape[0], device=dev))
+            del has
+        en, es, ep = torch.cat(ent_node), torch.cat(ent_sub), torch.cat(ent_pos)
+        keep_e = en < Lloc
+        en, es, ep = en[keep_e], es[keep_e], ep[keep_e]
+        o = _lexsort2(en, es)
+        self.acc_pos = ep[o].contiguous()
+        cnt = torch.bincount(en, minlength=Lloc)
+        self.acc_off = torch.zeros(Lloc + 1, dtype=torch.int64, device=dev)
+        self.acc_off[1:] = torch.cumsum(cnt, 0)
+        # 1/sqrt of the (small integer) overlap counts from a host table: IEEE sqrt
+        # as numpy computes it (torch's CPU sqrt is not always correctly rounded)
+        tab = 1.0 / np.sqrt(np.arange(1, int(cnt.max()) + 2, dtype=np.float64))
+        self.wsqrt = torch.as_tensor(tab, device=dev)[cnt - 1].contiguous()      # every node is covered
+        del vi, nsub, gsub, ent_node, ent_sub, ent_pos, en, es, ep, valid
+
+        # ---- layer residuals from the other ranks (plan "layer"): rw of the
+        #      remote-only nodes, provider by provider
+        self.plan_layer = None
+        if W > 1:
+            req = {q: rem[prov == q].view(-1, 1) for q in range(W) if q != rk}
+            asked = _alltoallv(comm, req, 1, torch.int64, dev)
+            send = {}
+            for q, t in asked.items():
+                nd = node_of(t.view(-1), L)
+                if bool((nd >= Lloc).any()):
+                    raise ConfigError("HybridSchwarz: a peer asked for a gid this rank does not hold")
+                send[q] = nd
+            self.plan_layer = _Plan(send, {q: int((prov == q).sum()) for q in range(W) if q != rk}, dev)
 
         # ---- coarse space: one dof per vertex, trilinear embedding (:180-236)
-        pts = torch.as_tensor(np.asarray(space.basis.points), dtype=torch.float64, device=dev)
+        pts = torch.as_tensor(np.array(space.basis.points, dtype=np.float64), device=dev)
         phi = torch.stack([(1.0 - pts) / 2.0, (1.0 + pts) / 2.0])
         tw = torch.empty((nn, 8), dtype=torch.float64, device=dev)
         for c in range(8):
             tw[:, c] = (phi[c & 1].view(n, 1, 1) * phi[(c >> 1) & 1].view(1, n, 1)
                         * phi[(c >> 2) & 1].view(1, 1, n)).reshape(-1)
         self.tw = tw.contiguous()
-        nv = int(mesh.vertices.shape[0])
-        self.first = gs.perm[gs.offsets[:-1]].contiguous()
+        loc_el = elements[e0:e1]
+        # first own copy of every own node; owned = the global first copy is here
+        lnode = gidn_X[i0:i0 + El].reshape(-1)
+        self.first = torch.full((Lloc,), P, dtype=torch.int64, device=dev)
+        self.first.scatter_reduce_(0, lnode, torch.arange(P, device=dev), reduce="amin")
+        gflat = (gx.view(NX, 1) * nn + torch.arange(nn, device=dev).view(1, nn)).reshape(-1)
+        gfirst = torch.full((L + 2,), BIG, dtype=torch.int64, device=dev)
+        gfirst.scatter_reduce_(0, gidn_X.reshape(-1), gflat, reduce="amin")
+        owned = gfirst[:Lloc] == self.first + e0 * nn
+        del gflat, gfirst
         fe, fp = self.first // nn, self.first % nn
-        cv, cc = torch.sort(elements, dim=1)
+        cv, cc = torch.sort(loc_el, dim=1)
         self.cvert = cv.to(torch.int32).contiguous()
         self.ccorn = cc.to(torch.uint8).contiguous()
-        # restriction rows: (vertex, gid ascending) over the nonzero weights of each
-        # gid's first element (explicit zeros of the reference's CSR add nothing);
-        # a chunked stable counting sort by vertex keeps the transients small
-        nzw = tw != 0.0                                                          # (nn, 8)
+        # restriction rows: (vertex, node ascending) over the nonzero weights of each
+        # owned node's first element (explicit zeros of the reference's CSR add
+        # nothing); a chunked stable counting sort by vertex
+        nzw = tw != 0.0
+        own_nodes = torch.nonzero(owned).view(-1)
         cnt = torch.zeros(nv, dtype=torch.int64, device=dev)
         step = 1 << 24
-        for g0 in range(0, G, step):
-            g1 = min(G, g0 + step)
-            m_ = nzw[fp[g0:g1]]
-            cnt += torch.bincount(elements[fe[g0:g1]][m_], minlength=nv)
+        for g0 in range(0, own_nodes.numel(), step):
+            gsel = own_nodes[g0:g0 + step]
+            m_ = nzw[fp[gsel]]
+            cnt += torch.bincount(loc_el[fe[gsel]][m_], minlength=nv)
         self.pt_ptr = torch.zeros(nv + 1, dtype=torch.int64, device=dev)
         self.pt_ptr[1:] = torch.cumsum(cnt, 0)
         self.pt_ent = torch.empty(int(self.pt_ptr[-1]), dtype=torch.int64, device=dev)
         fill = self.pt_ptr[:-1].clone()
-        for g0 in range(0, G, step):
-            g1 = min(G, g0 + step)
-            m_ = nzw[fp[g0:g1]]                                                  # (B, 8)
-            gi, ci = torch.nonzero(m_, as_tuple=True)                            # g-ascending
-            vv = elements[fe[g0:g1][gi], ci]
+        for g0 in range(0, own_nodes.numel(), step):
+            gsel = own_nodes[g0:g0 + step]
+            m_ = nzw[fp[gsel]]                                                   # (B, 8)
+            gi, ci = torch.nonzero(m_, as_tuple=True)                            # node-ascending
+            vv = loc_el[fe[gsel][gi], ci]
             o = torch.sort(vv, stable=True).indices
-            vv, ent = vv[o], ((gi + g0) * 8 + ci)[o]
+            vv, ent = vv[o], (gsel[gi] * 8 + ci)[o]
             newv = torch.ones_like(vv, dtype=torch.bool)
             newv[1:] = vv[1:] != vv[:-1]
             run = torch.arange(vv.numel(), device=dev)
@@ -462,37 +670,38 @@ class HybridSchwarz:
             self.pt_ent[fill[vv] + (run - head)] = ent
             fill += torch.bincount(vv, minlength=nv)
         del cnt, fill
-        # vertex blocks t^T A_e t per metric class, assembled in element order
-        ucls = torch.unique(ecls)
-        em = element_matrices(space, lam_visc, lam_mass, elems=erep[ucls])
+        # vertex blocks t^T A_e t of this rank's elements, summed per (i, j) in
+        # element order; across ranks the partial sums add in rank order
+        lcls = ecls[i0:i0 + El]
+        ucls = torch.unique(lcls)
+        em = element_matrices(space, lam_visc, lam_mass, elems=erep[ucls], geom=geom_X, bm=bm_X)
         blocks_c = tw.T.unsqueeze(0) @ em @ tw.unsqueeze(0)                     # (nc, 8, 8)
         del em
         cslot = torch.full((int(erep.numel()),), -1, dtype=torch.int64, device=dev)
         cslot[ucls] = torch.arange(ucls.numel(), device=dev)
-        bl = blocks_c[cslot[ecls]]                                              # (E, 8, 8)
-        ri = elements.view(E, 8, 1).expand(E, 8, 8).reshape(-1)
-        ci = elements.view(E, 1, 8).expand(E, 8, 8).reshape(-1)
-        kv = ri * nv + ci
-        o = torch.sort(kv, stable=True).indices                                  # element order kept
-        ks, vs = kv[o], bl.reshape(-1)[o]
-        newk = torch.ones_like(ks, dtype=torch.bool)
-        newk[1:] = ks[1:] != ks[:-1]
-        seg = torch.cumsum(newk.to(torch.int64), 0) - 1
-        nseg = int(seg[-1]) + 1
-        sstart = torch.nonzero(newk).view(-1)
-        slen = torch.bincount(seg, minlength=nseg)
-        val = torch.zeros(nseg, dtype=torch.float64, device=dev)
-        for j in range(int(slen.max())):
-            m_ = slen > j
-            val[m_] = val[m_] + vs[sstart[m_] + j]
-        krow, kcol = ks[sstart] // nv, ks[sstart] % nv
-        # constrained vertices: a corner whose gid is Dirichlet (:202-216)
+        bl = blocks_c[cslot[lcls]]                                              # (El, 8, 8)
+        ri = loc_el.view(El, 8, 1).expand(El, 8, 8).reshape(-1)
+        ci = loc_el.view(El, 1, 8).expand(El, 8, 8).reshape(-1)
+        kv, vs = _segment_sums(ri * nv + ci, bl.reshape(-1))
         corners_loc = torch.tensor([((c & 1) * (n - 1) * n + ((c >> 1) & 1) * (n - 1)) * n + ((c >> 2) & 1) * (n - 1)
                                     for c in range(8)], device=dev)
         vfixed = torch.zeros(nv, dtype=torch.bool, device=dev)
-        vfixed[elements[constrained[gid_e[:, corners_loc]]]] = True
+        vfixed[loc_el[constrained[gidn_X[i0:i0 + El][:, corners_loc]]]] = True
+        if W > 1:
+            from .partition import all_gather_cat
+
+            cnts = all_gather_cat(comm, torch.tensor([kv.numel()], dtype=torch.int64, device=dev)).cpu()
+            mx = int(cnts.max())
+            pk = torch.full((mx,), -1, dtype=torch.int64, device=dev)
+            pv = torch.zeros(mx, dtype=torch.float64, device=dev)
+            pk[:kv.numel()], pv[:vs.numel()] = kv, vs
+            ak, av = all_gather_cat(comm, pk), all_gather_cat(comm, pv)
+            okk = ak >= 0
+            kv, vs = _segment_sums(ak[okk], av[okk])                    # rank order = element order
+            vfixed = all_gather_cat(comm, vfixed.to(torch.int32)).view(W, nv).amax(dim=0) > 0
+        krow, kcol = kv // nv, kv % nv
         fr, fcn = vfixed[krow], vfixed[kcol]
-        val = torch.where(fr | fcn, torch.zeros_like(val), val)
+        val = torch.where(fr | fcn, torch.zeros_like(vs), vs)
         val = torch.where(fr & (krow == kcol), torch.ones_like(val), val)
         diag = torch.zeros(nv, dtype=torch.float64, device=dev)
         dm = krow == kcol
@@ -503,32 +712,46 @@ class HybridSchwarz:
         width = int(rcnt.max())
         rstart = torch.zeros(nv + 1, dtype=torch.int64, device=dev)
         rstart[1:] = torch.cumsum(rcnt, 0)
-        slot = torch.arange(nseg, device=dev) - rstart[krow]
+        slot = torch.arange(kv.numel(), device=dev) - rstart[krow]
         self.ac_col = torch.arange(nv, device=dev, dtype=torch.int32).view(nv, 1).repeat(1, width).contiguous()
         self.ac_val = torch.zeros((nv, width), dtype=torch.float64, device=dev)
         self.ac_col[krow, slot] = kcol.to(torch.int32)
         self.ac_val[krow, slot] = val
         self.vfixed = vfixed.to(torch.uint8).contiguous()
-        self.constrained = constrained.to(torch.uint8).contiguous()
-        self.G, self.nv = G, nv
+        self.constrained = constrained[:Lloc].to(torch.uint8).contiguous()
+        self.nv = nv
+        self.gid = lnode.contiguous()                            # node of every own point
+        self.gid_of_node = gid_of_node
 
-        # ---- work buffers and the C struct
+        # ---- work buffers, the exchanges (N > 1) and the C struct
         f64 = lambda k: torch.zeros(k, dtype=torch.float64, device=dev)
-        self.rg, self.rw, self.rc = f64(G), f64(G + 1), f64(nv)
+        self.rg, self.rw = f64(Lloc), f64(L + 1)                # rw[L] = 0: the padding slot
+        self.rc_part = f64(nv)
+        self.rc = self.rc_part if W == 1 else f64(nv)
         self.xc, self.cr, self.cz, self.cp, self.cap = (f64(nv) for _ in range(5))
         nblk = int(lib.sf_schwarz_coarse_blocks())
         self.cpart = f64(2 * nblk)
         self.cbar = torch.zeros(2, dtype=torch.int32, device=dev)
-        self.sol = f64(E * S)
-        self.z = f64(G)
-        self.gid = gs.gid
+        self.sol = f64(n_sol)
+        self.z = f64(Lloc)
+        self.sol_recv = f64(max(self.plan_sol.n_recv_total, 1)) if self.plan_sol is not None else None
+        self._ipc = {}
+        if W > 1:
+            allv = torch.arange(nv, dtype=torch.int32, device=dev)
+            self.plan_rc = _Plan({q: allv for q in range(W) if q != rk}, {q: nv for q in range(W) if q != rk}, dev)
+            self.rc_recv = f64(max(self.plan_rc.n_recv_total, 1))
+            if dev.type == "cuda":
+                if comm.peer is None:
+                    raise ConfigError("HybridSchwarz across ranks needs the NVLink peer path")
+                for name, plan in (("layer", self.plan_layer), ("rc", self.plan_rc), ("sol", self.plan_sol)):
+                    self._ipc[name] = _dist.HaloIPC(comm, plan)
         st = _SchwarzStruct()
-        pt = lambda t: ctypes.c_void_p(t.data_ptr())
-        st.G, st.P, st.nv, st.nnn, st.S = G, P, nv, nn, S
+        pt = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None
+        st.G, st.P, st.nv, st.nnn, st.S = Lloc, P, nv, nn, S
         st.first, st.gid, st.wsqrt, st.rg, st.rw = (pt(t) for t in (self.first, self.gid, self.wsqrt, self.rg,
                                                                       self.rw))
-        st.pt_ptr, st.pt_ent, st.tw, st.vfixed, st.rc = (pt(t) for t in (self.pt_ptr, self.pt_ent, self.tw,
-                                                                           self.vfixed, self.rc))
+        st.pt_ptr, st.pt_ent, st.tw, st.vfixed = (pt(t) for t in (self.pt_ptr, self.pt_ent, self.tw, self.vfixed))
+        st.rc_part, st.rc = pt(self.rc_part), pt(self.rc)
         st.ac_width = width
         st.ac_col, st.ac_val, st.ac_inv_diag = pt(self.ac_col), pt(self.ac_val), pt(self.coarse_inv_diag)
         st.xc, st.cr, st.cz, st.cp, st.cap = (pt(t) for t in (self.xc, self.cr, self.cz, self.cp, self.cap))
@@ -537,10 +760,22 @@ class HybridSchwarz:
         st.inv, st.n_tiles = pt(self.inv), int(self.tile_first.numel())
         st.tile_first, st.tile_n, st.tile_cls = pt(self.tile_first), pt(self.tile_n), pt(self.tile_cls)
         st.order, st.sub, st.sol = pt(self.order), pt(self.sub), pt(self.sol)
+        st.sol_recv, st.n_sol = pt(self.sol_recv), n_sol
         st.acc_off, st.acc_pos = pt(self.acc_off), pt(self.acc_pos)
         st.cvert, st.ccorn, st.constrained, st.z = pt(self.cvert), pt(self.ccorn), pt(self.constrained), pt(self.z)
         self._st = st
         self.launches = 0
+
+    def _exchange_into(self, name, src, dst):
+        """NVLink exchange `name` of src's listed entries; the received values are
+        copied (the current inbox bank) to dst."""
+        from . import _lib
+
+        ipc = self._ipc[name]
+        recv = ipc.exchange(src)
+        if recv is not None and ipc.plan.n_recv_total:
+            _lib.call("sf_halo_unbank_f64", recv.ptr, recv.seq_ptr, recv.bank, ipc.plan.n_recv_total,
+                      _lib.ptr(dst), _lib.stream_ptr(self.space.device))
 
     @staticmethod
     def _candidates(sub, gid_e, ge_off, ge_e, G, E):
@@ -593,9 +828,25 @@ class HybridSchwarz:
         """out <- M^-1 r (HybridSchwarz.__call__, precond.py:239-250); r, out: fields."""
         from . import _lib
 
-        _lib.call("sf_schwarz_apply_f64", ctypes.addressof(self._st), _lib.ptr(r.contiguous()), _lib.ptr(out),
-                  _lib.stream_ptr(self.space.device))
-        self.launches += 6
+        st = ctypes.addressof(self._st)
+        stream = _lib.stream_ptr(self.space.device)
+        r = r.contiguous()
+        if not self._ipc:
+            _lib.call("sf_schwarz_apply_f64", st, _lib.ptr(r), _lib.ptr(out), stream)
+            self.launches += 6
+            return out
+        comm = self.space.comm
+        _lib.call("sf_schwarz_gather_f64", st, _lib.ptr(r), stream)
+        self._exchange_into("layer", self.rw, self.rw[self.G:])
+        _lib.call("sf_schwarz_restrict_f64", st, stream)
+        self._exchange_into("rc", self.rc_part, self.rc_recv)
+        _lib.call("sf_schwarz_rank_sum_f64", st, _lib.ptr(self.rc_recv), comm.rank, comm.world, stream)
+        _lib.call("sf_schwarz_coarse_f64", st, stream)
+        _lib.call("sf_schwarz_local_f64", st, stream)
+        self._exchange_into("sol", self.sol, self.sol_recv)
+        _lib.call("sf_schwarz_finalize_f64", st, stream)
+        _lib.call("sf_schwarz_scatter_f64", st, _lib.ptr(out), stream)
+        self.launches += 16
         return out
 
     def __call__(self, r):

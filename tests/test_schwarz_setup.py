@@ -38,6 +38,7 @@ class _GS:
 
 class _Comm:
     world = 1
+    rank = 0
 
 
 class _Space:
@@ -55,18 +56,21 @@ class _Space:
         self.geom = torch.from_numpy(np.ascontiguousarray(osp.geom))
         self.bm = torch.from_numpy(np.ascontiguousarray(osp.bm))
         self.dmat = np.ascontiguousarray(osp.basis.dmat)
+        self.e_range = (0, osp.shape[0])
 
 
 def _oracle_element_matrices(oracle, osp):
-    def em(space, lam_visc, lam_mass, batch=64, elems=None):
+    def em(space, lam_visc, lam_mass, batch=64, elems=None, geom=None, bm=None):
         n, E = space.n, space.n_elements
         nn = n ** 3
+        gg = osp.geom.reshape(6, -1, nn) if geom is None else geom.cpu().numpy()
+        bb = osp.bm.reshape(-1, nn) if bm is None else bm.cpu().numpy()
         el = np.arange(E) if elems is None else np.asarray(torch.as_tensor(elems).cpu())
         out = np.empty((el.size, nn, nn))
         ident = np.eye(nn).reshape(nn, n, n, n)
         for i, e in enumerate(el):
-            g = np.ascontiguousarray(np.broadcast_to(osp.geom[:, e:e + 1], (6, nn, n, n, n)))
-            b = np.ascontiguousarray(np.broadcast_to(osp.bm[e:e + 1], (nn, n, n, n)))
+            g = np.ascontiguousarray(np.broadcast_to(gg[:, e:e + 1].reshape(6, 1, n, n, n), (6, nn, n, n, n)))
+            b = np.ascontiguousarray(np.broadcast_to(bb[e:e + 1].reshape(1, n, n, n), (nn, n, n, n)))
             out[i] = oracle.ax_helmholtz_local(osp.basis.dmat, g, b, ident, lam_visc, lam_mass).reshape(nn, nn).T
         return torch.from_numpy(out)
     return em
@@ -79,7 +83,7 @@ def _emulate(hs, r):
     first, wsqrt, tw = t(hs.first), t(hs.wsqrt), t(hs.tw)
     rflat = r.reshape(-1)
     rg = rflat[first]
-    rw = np.concatenate([wsqrt * rg, [0.0]])
+    rw = np.concatenate([wsqrt * rg, np.zeros(hs.L - hs.G + 1)])
     # restriction
     ptr, ent, vfixed = t(hs.pt_ptr), t(hs.pt_ent), t(hs.vfixed)
     rc = np.zeros(hs.nv)
@@ -187,3 +191,174 @@ def test_box_mesh_deduplicates(oracle, monkeypatch):
     r = np.random.default_rng(1).standard_normal(osp.shape)
     z = _emulate(hs, r)
     assert np.isfinite(z).all()
+
+
+# ---------------------------------------------------------------- several ranks
+
+def _rank_worker(rank, world, port, payload, q):
+    import sys as _sys
+
+    _sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    _sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import semflow_oracle as oracle
+
+        from paper_2207_07098_b200 import precond
+        from paper_2207_07098_b200.dist import Comm, element_ranges
+
+        mesh, order, mask_np, lm = payload
+        osp = oracle.build_space(mesh, oracle.make_basis(order))
+        precond.element_matrices = _oracle_element_matrices(oracle, osp)
+        E = osp.shape[0]
+        nn = osp.n ** 3
+        st = element_ranges(E, world)
+        e0, e1 = st[rank], st[rank + 1]
+        sp = _Space(osp, mesh)
+        sp.comm = Comm()
+        sp.e_range = (e0, e1)
+        sp.n_elements = e1 - e0
+        sp.shape = (e1 - e0,) + tuple(osp.shape[1:])
+        sp.geom = torch.from_numpy(np.ascontiguousarray(osp.geom[:, e0:e1]))
+        sp.bm = torch.from_numpy(np.ascontiguousarray(osp.bm[e0:e1]))
+        sp.gs.gid = torch.from_numpy(osp.gs.gid[e0 * nn:e1 * nn].copy())
+        mk = None if mask_np is None else torch.from_numpy(np.ascontiguousarray(mask_np[e0:e1]))
+        hs = precond.HybridSchwarz(sp, mask=mk, lam_visc=1.0, lam_mass=lm)
+        t = lambda x: x.cpu().numpy()
+        out = {k: t(getattr(hs, k)) for k in ("first", "wsqrt", "tw", "pt_ptr", "pt_ent", "vfixed", "ac_col",
+                                             "ac_val", "coarse_inv_diag", "sub", "inv", "order", "tile_first",
+                                             "tile_n", "tile_cls", "acc_off", "acc_pos", "cvert", "ccorn",
+                                             "constrained", "gid")}
+        out.update(G=hs.G, L=hs.L, S=hs.S, nv=hs.nv, iters=hs.coarse_iters, e0=e0, e1=e1,
+                   layer={p: t(v) for p, v in hs.plan_layer.send_idx.items()},
+                   layer_recv=dict(hs.plan_layer.n_recv),
+                   sol={p: t(v) for p, v in hs.plan_sol.send_idx.items()},
+                   sol_recv=dict(hs.plan_sol.n_recv), n_classes=hs.n_classes)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def _emulate_ranks(res, r_glob, nn):
+    """numpy restatement of the N-rank application (gather, layer exchange,
+    restriction partials summed in rank order, replicated coarse CG, local solves,
+    solution exchange, ordered accumulation, scatter)."""
+    W = len(res)
+    res = {k: res[k] for k in sorted(res)}
+    rg, rw, rcp = {}, {}, {}
+    for k, h in res.items():
+        rl = r_glob.reshape(-1)[h["e0"] * nn:h["e1"] * nn]
+        rg[k] = rl[h["first"]]
+        rw[k] = np.zeros(h["L"] + 1)
+        rw[k][:h["G"]] = h["wsqrt"] * rg[k]
+    for k, h in res.items():          # layer residuals, providers in rank order
+        off = h["G"]
+        for p in sorted(h["layer_recv"]):
+            vals = rw[p][res[p]["layer"][k]]
+            rw[k][off:off + vals.size] = vals
+            off += vals.size
+    for k, h in res.items():
+        rc = np.zeros(h["nv"])
+        for v in range(h["nv"]):
+            if h["vfixed"][v]:
+                continue
+            acc = 0.0
+            for e in range(h["pt_ptr"][v], h["pt_ptr"][v + 1]):
+                g, c = h["pt_ent"][e] >> 3, h["pt_ent"][e] & 7
+                acc = acc + h["tw"][h["first"][g] % nn, c] * rg[k][g]
+            rc[v] = acc
+        rcp[k] = rc
+    rc = np.zeros_like(rcp[0])
+    for k in range(W):
+        rc = rc + rcp[k]
+    h0 = res[0]
+    col, val, invd = h0["ac_col"].astype(np.int64), h0["ac_val"], h0["coarse_inv_diag"]
+    x = np.zeros_like(rc)
+    rr = rc.copy()
+    z = invd * rr
+    p_ = z.copy()
+    rz = float(rr @ z)
+    if rz > 0.0:
+        for _ in range(h0["iters"]):
+            ap = (val * p_[col]).sum(axis=1)
+            pap = float(p_ @ ap)
+            if pap <= 0.0:
+                break
+            alpha = rz / pap
+            x += alpha * p_
+            rr -= alpha * ap
+            z = invd * rr
+            rzn = float(rr @ z)
+            if rzn <= 0.0:
+                break
+            p_ = z + (rzn / rz) * p_
+            rz = rzn
+    sol = {}
+    for k, h in res.items():
+        s_ = np.zeros(h["sub"].shape)
+        for t in range(h["tile_first"].size):
+            for j in range(h["tile_n"][t]):
+                e = h["order"][h["tile_first"][t] + j]
+                s_[e] = h["inv"][h["tile_cls"][t]] @ rw[k][h["sub"][e].astype(np.int64)]
+        sol[k] = s_.reshape(-1)
+    outs = []
+    for k, h in res.items():
+        recv = [sol[p][res[p]["sol"][k]] for p in sorted(h["sol_recv"])]
+        src = np.concatenate([sol[k]] + recv)
+        zg = np.empty(h["G"])
+        for g in range(h["G"]):
+            if h["constrained"][g]:
+                zg[g] = rg[k][g]
+                continue
+            acc = 0.0
+            for e in range(h["acc_off"][g], h["acc_off"][g + 1]):
+                acc = acc + src[h["acc_pos"][e]]
+            el, pp = divmod(int(h["first"][g]), nn)
+            pc = 0.0
+            for c in range(8):
+                pc = pc + h["tw"][pp, h["ccorn"][el, c]] * x[h["cvert"][el, c]]
+            zg[g] = acc * h["wsqrt"][g] + pc
+        outs.append(zg[h["gid"]])
+    return np.concatenate(outs)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("masked", [True, False])
+def test_schwarz_ranks_match_reference(oracle, pbox, world, masked):
+    """Each rank builds its own subdomains (remote vertex neighbours fetched over
+    gloo); the emulated N-rank application reproduces the reference's
+    single-process application (golden)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    mesh, osp = pbox
+    gold = np.load(os.path.join(GOLDEN, "schwarz.npz"))
+    mask = np.ones(osp.shape)
+    mask.reshape(-1)[osp.facet_flat.ravel()] = 0.0
+    name, mk, lm = ("masked", mask, 0.0) if masked else ("free", None, 0.5)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_worker, args=(r, world, port, (mesh, 5, mk, lm), q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, out = q.get(timeout=600)
+        res[r] = out
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    got = _emulate_ranks(res, gold["r"], osp.n ** 3)
+    assert rel_err(got.reshape(gold[f"apply_{name}"].shape), gold[f"apply_{name}"]) < 1e-10
+    # every rank holds the same coarse operator
+    for r in range(1, world):
+        assert np.array_equal(res[r]["ac_val"], res[0]["ac_val"])
