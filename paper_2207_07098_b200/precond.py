@@ -165,6 +165,46 @@ def _segment_sums(keys, vals):
     return ks[sstart], out
 
 
+def _metric_classes(geom, bm, share_bits, chunk=4096):
+    """(class id per element, representative element per class) for geom (6, E,
+    nn) / bm (E, nn): equal within share_bits bits of the element's scale (or
+    bitwise for None)."""
+    dev = bm.device
+    E, nn = bm.shape
+    wr = (torch.rand(7 * nn, generator=torch.Generator().manual_seed(_HASH_SEED), dtype=torch.float64)
+          + 0.5).to(dev)
+    feats = torch.empty((E, 9), dtype=torch.float64, device=dev)
+    for x0 in range(0, E, chunk):
+        x1 = min(E, x0 + chunk)
+        v = torch.cat([geom[:, x0:x1].permute(1, 0, 2).reshape(x1 - x0, 6 * nn), bm[x0:x1]], dim=1)
+        feats[x0:x1, :7] = v.view(x1 - x0, 7, nn).sum(dim=2)
+        feats[x0:x1, 7] = (v * wr).sum(dim=1)
+        feats[x0:x1, 8] = v.abs().amax(dim=1)
+    # one scale for all summaries: a plane of round-off (the off-diagonal G of an
+    # affine box) quantises to 0 instead of to its own noise
+    rng = float(feats.abs().max()) or 1.0
+    q = torch.round(feats / rng * float(2 ** 28)).to(torch.int64)
+    cls, rep = _classes(_row_hash(q, _hash_weights(9, dev, 7)))
+    # verify every element against its class representative; split the misfits
+    bad = torch.zeros(E, dtype=torch.bool, device=dev)
+    for x0 in range(0, E, chunk):
+        x1 = min(E, x0 + chunk)
+        r_ = rep[cls[x0:x1]]
+        a = torch.cat([geom[:, x0:x1].permute(1, 0, 2).reshape(x1 - x0, 6 * nn), bm[x0:x1]], dim=1)
+        b = torch.cat([geom[:, r_].permute(1, 0, 2).reshape(x1 - x0, 6 * nn), bm[r_]], dim=1)
+        if share_bits is None:
+            bad[x0:x1] = (a.view(torch.int64) != b.view(torch.int64)).any(dim=1)
+        else:
+            tol = a.abs().amax(dim=1) * float(2.0 ** -int(share_bits))
+            bad[x0:x1] = (a - b).abs().amax(dim=1) > tol
+    if bool(bad.any()):
+        nb = int(bad.sum())
+        cls = cls.clone()
+        cls[bad] = int(rep.numel()) + torch.arange(nb, device=dev)
+        rep = torch.cat([rep, torch.nonzero(bad).view(-1)])
+    return cls, rep
+
+
 def _face_neighbours(mesh, dev):
     """(E, 6) neighbour element across each face (-1 on exterior faces) and the
     neighbour's face number: faces keyed by their vertex SET, exactly two owners
@@ -432,30 +472,15 @@ class HybridSchwarz:
         ge_off[1:] = torch.cumsum(torch.bincount(ge_g, minlength=L + 2), 0)
         del key, ge_g
 
-        # ---- metric classes of the X elements: geometry equal to ``share_bits`` bits
-        #      relative to the element's own scale (default 40: ~1e-12) shares one
-        #      element matrix -- np.linspace meshes differ elementwise only in the
-        #      last bits; share_bits=None hashes the exact bits
-        hw = _hash_weights(7 * nn + 2, dev, 1)
-        eh = torch.empty((NX, 2), dtype=torch.int64, device=dev)
-        gmax = float(geom_X.abs().max()) or 1.0
-        bmax = float(bm_X.abs().max()) or 1.0
-        for x0 in range(0, NX, 4096):
-            x1 = min(NX, x0 + 4096)
-            ge = geom_X[:, x0:x1].permute(1, 0, 2).reshape(x1 - x0, 6 * nn)
-            be = bm_X[x0:x1]
-            if share_bits is None:
-                q = torch.cat([ge, be], dim=1).contiguous().view(torch.int64)
-                q = torch.cat([q, torch.zeros((x1 - x0, 2), dtype=torch.int64, device=dev)], dim=1)
-            else:
-                sc = float(2 ** int(share_bits))
-                sg = ge.abs().amax(dim=1, keepdim=True).clamp_min(1e-300)
-                sb = be.abs().amax(dim=1, keepdim=True).clamp_min(1e-300)
-                q = torch.cat([torch.round(ge / sg * sc), torch.round(be / sb * sc),
-                               torch.round(sg / gmax * sc), torch.round(sb / bmax * sc)], dim=1).to(torch.int64)
-            eh[x0:x1] = _row_hash(q, hw)
-        ecls, erep = _classes(eh)
-        del eh
+        # ---- metric classes of the X elements: elements whose geometric factors
+        #      agree to ``share_bits`` bits relative to the element's own scale
+        #      (default 40: ~1e-12) share one element matrix -- np.linspace meshes
+        #      differ elementwise only in the last bits; share_bits=None requires
+        #      bitwise equality.  Candidates come from a hash of robust summaries
+        #      (per-plane sums quantised to 2^-28 of their range: a last-bit
+        #      difference does not move them), then every element is checked
+        #      against its candidate representative and split off if it differs.
+        ecls, erep = _metric_classes(geom_X, bm_X, share_bits)
 
         # ---- subdomain signatures (candidate classes, landing slots, Dirichlet, size)
         bmg = None
