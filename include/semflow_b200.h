@@ -347,14 +347,10 @@ typedef struct SfSchwarz {
   double* cpart;                /* (2 * coarse_blocks) partial sums */
   unsigned* cbar;               /* (2) grid-barrier words, zero between launches */
   int coarse_iters, coarse_blocks;
-  const double* inv;            /* (U, S, S) inverses of the distinct subdomain matrices */
-  int n_tiles;                  /* tiles of <= sf_schwarz_tile() same-class subdomains */
-  const int* tile_first;
-  const int* tile_n;
-  const int* tile_cls;
-  const int* order;             /* (E) subdomains grouped by class */
-  const int* sub;               /* (E, S) gids of each subdomain, padded with G */
-  double* sol;                  /* (E, S) work: local solutions */
+  const int* sub;               /* (E, S) nodes of each subdomain slot, rows grouped by class;
+                                   padding slots name rw's zero slot */
+  double* rwg;                  /* (E, S) work: rw[sub], the solve GEMM operand */
+  double* sol;                  /* (E, S) work: local solutions (class-ordered rows) */
   const double* sol_recv;       /* N > 1: the peers' solutions on this rank's gids */
   long long n_sol;              /* E * S: acc_pos >= n_sol index sol_recv */
   const long long* acc_off;     /* (G + 1) overlap accumulation: gid -> sol slots, */
@@ -366,27 +362,29 @@ typedef struct SfSchwarz {
 } SfSchwarz;
 
 /* out = M^-1 r for the hybrid Schwarz preconditioner (HybridSchwarz.__call__,
- * precond.py:239-250): gather, restriction, fixed-iteration Jacobi-CG coarse
- * solve (one persistent launch), local subdomain solves, ordered overlap
- * accumulation + prolongation, scatter.  Stream-ordered, no host sync,
- * deterministic.  G counts this rank's gids (all gids on one rank). */
-int sf_schwarz_apply_f64(const SfSchwarz* s, const double* r, double* out, void* stream);
-/* The same six stages one by one, for N > 1 where NVLink exchanges go between
- * them: layer residuals after gather, restriction partials (all-gathered, then
- * sf_schwarz_rank_sum_f64) after restrict, subdomain solutions after local. */
+ * precond.py:239-250), in stream-ordered stages (no host sync, deterministic):
+ *   gather      rg, rw of this rank's nodes (G counts them; all gids on one rank)
+ *   restrict    this rank's coarse restriction (owned gids) -> rc_part
+ *   rank_sum    N > 1: rc = rank-order sum of the all-gathered partials
+ *   coarse      fixed-iteration Jacobi-CG on the vertex problem (one launch)
+ *   gather_rw   rwg = rw[sub], then per class sol_c = rwg_c inv_c^T (FP64 GEMM
+ *               issued by the caller)
+ *   finalize    ordered overlap sums (own + received solutions) + prolongation
+ *   scatter     out[p] = z[node of p]
+ * N > 1: the layer residuals, restriction partials and subdomain solutions
+ * travel over NVLink between the stages (halo put/wait + sf_halo_unbank_f64). */
 int sf_schwarz_gather_f64(const SfSchwarz* s, const double* r, void* stream);
 int sf_schwarz_restrict_f64(const SfSchwarz* s, void* stream);
 int sf_schwarz_rank_sum_f64(const SfSchwarz* s, const double* recv, int rank, int world, void* stream);
 int sf_schwarz_coarse_f64(const SfSchwarz* s, void* stream);
-int sf_schwarz_local_f64(const SfSchwarz* s, void* stream);
+int sf_schwarz_gather_rw_f64(const SfSchwarz* s, void* stream);
 int sf_schwarz_finalize_f64(const SfSchwarz* s, void* stream);
 int sf_schwarz_scatter_f64(const SfSchwarz* s, double* out, void* stream);
 /* out[0..n) = the current bank of a double-banked halo inbox (bank 0 at bank0,
  * bank stride `stride`, call counter *seq; csrc/halo.cu) */
 int sf_halo_unbank_f64(const double* bank0, const unsigned long long* seq, long long stride, long long n,
                        double* out, void* stream);
-/* subdomains per local-solve tile; blocks of the coarse CG launch (= SM count) */
-int sf_schwarz_tile(void);
+/* blocks of the coarse CG launch (= SM count) */
 int sf_schwarz_coarse_blocks(void);
 
 #ifdef __cplusplus

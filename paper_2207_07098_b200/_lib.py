@@ -70,16 +70,14 @@ _SIGS = {
     "sf_halo_wait": [_vp, _i, _vp, _vp, _vp],
     "sf_trilinear_coords_f64": [_vp, _vp, _i, _ll, _vp, _vp],
     "sf_metrics_f64": [_vp, _vp, _i, _vp, _ll, _vp, _vp, _vp, _vp, _vp],
-    "sf_schwarz_apply_f64": [_vp, _vp, _vp, _vp],
     "sf_schwarz_gather_f64": [_vp, _vp, _vp],
     "sf_schwarz_restrict_f64": [_vp, _vp],
     "sf_schwarz_rank_sum_f64": [_vp, _vp, _i, _i, _vp],
     "sf_schwarz_coarse_f64": [_vp, _vp],
-    "sf_schwarz_local_f64": [_vp, _vp],
+    "sf_schwarz_gather_rw_f64": [_vp, _vp],
     "sf_schwarz_finalize_f64": [_vp, _vp],
     "sf_schwarz_scatter_f64": [_vp, _vp, _vp],
     "sf_halo_unbank_f64": [_vp, _vp, _ll, _ll, _vp, _vp],
-    "sf_schwarz_tile": [],
     "sf_schwarz_coarse_blocks": [],
 }
 _RESTYPES = {"sf_version": ctypes.c_char_p, "sf_last_error": ctypes.c_char_p}
@@ -137,9 +135,9 @@ NVTX_TAGS = {
     "sf_bdf_ext_f64": "K8 bdf_ext",
     "sf_halo_put_f64": "C1 halo", "sf_halo_wait": "C1 halo",
     "sf_peer_allreduce_f64": "C2 allreduce", "sf_rank_sum_f64": "C2 allreduce",
-    "sf_schwarz_apply_f64": "K9 schwarz", "sf_schwarz_gather_f64": "K9 schwarz",
+    "sf_schwarz_gather_f64": "K9 schwarz", "sf_schwarz_gather_rw_f64": "K9 schwarz",
     "sf_schwarz_restrict_f64": "K9 schwarz", "sf_schwarz_rank_sum_f64": "C2 allreduce",
-    "sf_schwarz_coarse_f64": "K9 schwarz", "sf_schwarz_local_f64": "K9 schwarz",
+    "sf_schwarz_coarse_f64": "K9 schwarz",
     "sf_schwarz_finalize_f64": "K9 schwarz", "sf_schwarz_scatter_f64": "K9 schwarz",
     "sf_halo_unbank_f64": "C1 halo",
 }

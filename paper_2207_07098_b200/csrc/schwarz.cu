@@ -1,5 +1,5 @@
 // Hybrid overlapping Schwarz preconditioner, application (reference
-// precond.py:94-250, HybridSchwarz.__call__ at :239-250).  Five stream-ordered
+// precond.py:94-250, HybridSchwarz.__call__ at :239-250).  Stream-ordered
 // launches, no host synchronisation, CUDA-graph capturable:
 //
 //   gather    rg[g] = r[first copy of g]; rw[g] = wsqrt[g] * rg[g]      (:241-242)
@@ -7,9 +7,9 @@
 //   coarse    fixed-iteration Jacobi-CG on the vertex problem (:205-230), one
 //             persistent launch with software grid barriers
 //   local     sol_e = A_e^{-1} rw[sub_e] for every subdomain (:243-244): the
-//             explicit inverses of the DISTINCT subdomain matrices (bitwise-equal
-//             matrices are stored once), subdomains of one class in tiles of T
-//             so each inverse row is read once per tile
+//             explicit inverses of the DISTINCT subdomain matrices; the operand
+//             Rw = rw[sub] is gathered here (rows grouped by class) and each
+//             class's products are one FP64 GEMM (cuBLAS, issued by the host)
 //   finalize  z[g] = (sum over subdomains holding g, ascending) sol * wsqrt[g]
 //             + sum_v (ascending) P[g, v] xc[v]; z = rg on constrained g  (:244-249)
 //   scatter   out[p] = z[gid[p]]                                          (:250)
@@ -37,24 +37,29 @@ __global__ void sch_gather_kernel(const double* __restrict__ r, const long long*
   }
 }
 
-// rc[v] = sum over entries k of vertex v (gid-ascending) of tw[p_g*8 + c] * rg[g];
-// entry = g * 8 + c.
+// rc[v] = sum over the entries k of vertex v (gid-ascending) of tw[p_g*8 + c] * rg[g],
+// entry = g * 8 + c.  A warp per vertex: lane l folds entries l, l+32, ... in
+// order, then a fixed xor tree (a vertex has ~(2n-1)^3 entries; one thread per
+// vertex was latency-bound).
 __global__ void sch_restrict_kernel(const double* __restrict__ rg, const long long* __restrict__ ptr,
                                     const long long* __restrict__ ent, const long long* __restrict__ first,
                                     const double* __restrict__ tw, int nnn, long long nv,
                                     const uint8_t* __restrict__ vfixed, double* __restrict__ rc) {
-  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nv;
-       v += (long long)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long v = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; v < nv; v += warps) {
     double acc = 0.0;
     if (!vfixed[v]) {
-      for (long long k = ptr[v]; k < ptr[v + 1]; ++k) {
+      for (long long k = ptr[v] + lane; k < ptr[v + 1]; k += 32) {
         const long long e = ent[k];
         const long long g = e >> 3;
         const int p = (int)(first[g] % nnn);
         acc = __dadd_rn(acc, __dmul_rn(tw[p * 8 + (int)(e & 7)], rg[g]));
       }
     }
-    rc[v] = acc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    if (lane == 0) rc[v] = acc;
   }
 }
 
@@ -192,47 +197,13 @@ __global__ void __launch_bounds__(256) sch_coarse_cg_kernel(CoarseArgs a) {
 
 // ----------------------------------------------------------------- local solves
 
-// A tile = up to T subdomains of the same class (same inverse).  order[] lists
-// the subdomains class by class; tile t covers order[tfirst[t] .. +tn[t]).
-template <int T>
-__global__ void __launch_bounds__(256) sch_local_kernel(const double* __restrict__ inv, int S,
-                                                        const int* __restrict__ tfirst,
-                                                        const int* __restrict__ tn,
-                                                        const int* __restrict__ tcls,
-                                                        const int* __restrict__ order,
-                                                        const int* __restrict__ sub,
-                                                        const double* __restrict__ rw,
-                                                        double* __restrict__ sol) {
-  extern __shared__ double rs[];            // T * S
-  const int tile = blockIdx.x;
-  const int n = tn[tile];
-  const int f = tfirst[tile];
-  const double* A = inv + (size_t)tcls[tile] * S * S;
-  for (int idx = threadIdx.x; idx < T * S; idx += blockDim.x) {
-    const int t = idx / S, i = idx - t * S;
-    rs[idx] = t < n ? rw[sub[(size_t)order[f + t] * S + i]] : 0.0;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i = warp; i < S; i += nw) {
-    double acc[T];
-#pragma unroll
-    for (int t = 0; t < T; ++t) acc[t] = 0.0;
-    const double* row = A + (size_t)i * S;
-    for (int j = lane; j < S; j += 32) {
-      const double aij = row[j];
-#pragma unroll
-      for (int t = 0; t < T; ++t) acc[t] = fma(aij, rs[t * S + j], acc[t]);
-    }
-#pragma unroll
-    for (int t = 0; t < T; ++t)
-      for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
-    if (lane == 0) {
-#pragma unroll
-      for (int t = 0; t < T; ++t)
-        if (t < n) sol[(size_t)order[f + t] * S + i] = acc[t];
-    }
-  }
+// Rw[p][j] = rw[sub[p][j]]: the weighted residual of every subdomain slot, rows in
+// class order (the operand of the per-class solve GEMM sol_c = Rw_c inv_c^T)
+__global__ void sch_gather_rw_kernel(const double* __restrict__ rw, const int* __restrict__ sub, long long n,
+                                     double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = rw[sub[i]];
 }
 
 // z[g] = con ? rg : (sum_k sol[pos[k]]) * wsqrt + sum over the corners of g's
@@ -309,8 +280,6 @@ static unsigned grid_for(long long n) {
 
 extern "C" {
 
-int sf_schwarz_tile(void) { return 4; }
-
 int sf_schwarz_coarse_blocks(void) {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -337,7 +306,7 @@ int sf_schwarz_gather_f64(const SfSchwarz* s, const double* r, void* stream) {
 int sf_schwarz_restrict_f64(const SfSchwarz* s, void* stream) {
   using namespace sf;
   if (bad(s, "sf_schwarz_restrict_f64")) return SF_ERR_ARG;
-  sch_restrict_kernel<<<grid_for(s->nv), 256, 0, as_stream(stream)>>>(s->rg, s->pt_ptr, s->pt_ent, s->first,
+  sch_restrict_kernel<<<grid_for(s->nv * 32), 256, 0, as_stream(stream)>>>(s->rg, s->pt_ptr, s->pt_ent, s->first,
                                                                      s->tw, s->nnn, s->nv, s->vfixed, s->rc_part);
   return check_launch("schwarz restrict");
 }
@@ -362,21 +331,14 @@ int sf_schwarz_coarse_f64(const SfSchwarz* s, void* stream) {
   return check_launch("schwarz coarse");
 }
 
-// stage 4: local subdomain solves sol = inv rw[sub]
-int sf_schwarz_local_f64(const SfSchwarz* s, void* stream) {
+// stage 4a: the solve operand Rw = rw[sub] (rows in class order); the per-class
+// products sol_c = Rw_c inv_c^T are FP64 GEMMs issued by the host (cuBLAS)
+int sf_schwarz_gather_rw_f64(const SfSchwarz* s, void* stream) {
   using namespace sf;
-  if (bad(s, "sf_schwarz_local_f64")) return SF_ERR_ARG;
-  constexpr int T = 4;
-  if (s->n_tiles <= 0) return SF_OK;
-  const size_t smem = (size_t)T * s->S * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sch_local_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    attr = true;
-  }
-  sch_local_kernel<T><<<(unsigned)s->n_tiles, 256, smem, as_stream(stream)>>>(
-      s->inv, s->S, s->tile_first, s->tile_n, s->tile_cls, s->order, s->sub, s->rw, s->sol);
-  return check_launch("schwarz local");
+  if (bad(s, "sf_schwarz_gather_rw_f64")) return SF_ERR_ARG;
+  const long long n = s->n_sol;
+  sch_gather_rw_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(s->rw, s->sub, n, s->rwg);
+  return check_launch("schwarz gather rw");
 }
 
 // stage 5: ordered overlap sums (own + received solutions) + prolongation -> z
@@ -395,17 +357,6 @@ int sf_schwarz_scatter_f64(const SfSchwarz* s, double* out, void* stream) {
   if (bad(s, "sf_schwarz_scatter_f64") || !out) return SF_ERR_ARG;
   sch_scatter_kernel<<<grid_for(s->P), 256, 0, as_stream(stream)>>>(s->z, s->gid, s->P, out);
   return check_launch("schwarz scatter");
-}
-
-// single rank: the six stages back to back
-int sf_schwarz_apply_f64(const SfSchwarz* s, const double* r, double* out, void* stream) {
-  int e;
-  if ((e = sf_schwarz_gather_f64(s, r, stream))) return e;
-  if ((e = sf_schwarz_restrict_f64(s, stream))) return e;
-  if ((e = sf_schwarz_coarse_f64(s, stream))) return e;
-  if ((e = sf_schwarz_local_f64(s, stream))) return e;
-  if ((e = sf_schwarz_finalize_f64(s, stream))) return e;
-  return sf_schwarz_scatter_f64(s, out, stream);
 }
 
 // copy the current bank of an NVLink halo inbox to out (n doubles)

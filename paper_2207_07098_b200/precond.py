@@ -251,9 +251,7 @@ class _SchwarzStruct(ctypes.Structure):
         ("xc", ctypes.c_void_p), ("cr", ctypes.c_void_p), ("cz", ctypes.c_void_p), ("cp", ctypes.c_void_p),
         ("cap", ctypes.c_void_p), ("cpart", ctypes.c_void_p), ("cbar", ctypes.c_void_p),
         ("coarse_iters", ctypes.c_int), ("coarse_blocks", ctypes.c_int),
-        ("inv", ctypes.c_void_p), ("n_tiles", ctypes.c_int),
-        ("tile_first", ctypes.c_void_p), ("tile_n", ctypes.c_void_p), ("tile_cls", ctypes.c_void_p),
-        ("order", ctypes.c_void_p), ("sub", ctypes.c_void_p), ("sol", ctypes.c_void_p),
+        ("sub", ctypes.c_void_p), ("rwg", ctypes.c_void_p), ("sol", ctypes.c_void_p),
         ("sol_recv", ctypes.c_void_p), ("n_sol", ctypes.c_longlong),
         ("acc_off", ctypes.c_void_p), ("acc_pos", ctypes.c_void_p),
         ("cvert", ctypes.c_void_p), ("ccorn", ctypes.c_void_p), ("constrained", ctypes.c_void_p),
@@ -317,7 +315,10 @@ class HybridSchwarz:
     ascending global subdomain order -- the reference's order.
 
     One application (``apply_into``) is stream-ordered with no host
-    synchronisation (CUDA-graph capturable; the fused GMRES captures it).
+    synchronisation (CUDA-graph capturable; the fused GMRES captures it): the
+    gather / restriction / coarse CG / overlap sums / scatter kernels are ours,
+    and each subdomain class's solves are one FP64 GEMM (cuBLAS, the FP64 tensor
+    cores) on the gathered residual slots.
     Subdomain solves use the explicit inverse instead of LU back-substitution and
     the 10-iteration coarse Jacobi-CG a sparse vertex matrix, so one application
     agrees with the reference to rounding (~1e-13) and Krylov iteration counts
@@ -559,35 +560,38 @@ class HybridSchwarz:
             inv[u0:u1] = torch.linalg.inv(A)
             del A
         del emats_u
-        self.inv = inv
 
-        # ---- local-solve tiles: subdomains grouped by class, T per tile
+        # ---- local solves: subdomain rows grouped by class; class c's solutions
+        #      are one FP64 GEMM  sol[p0:p1] = rw[sub[p0:p1]] @ inv_c^T
         order = torch.sort(scls, stable=True).indices
         cls_sorted = scls[order]
         newc = torch.ones(El, dtype=torch.bool, device=dev)
         newc[1:] = cls_sorted[1:] != cls_sorted[:-1]
-        start_of = torch.cumsum(newc.to(torch.int64), 0) - 1
-        cstart = torch.nonzero(newc).view(-1)
-        within = torch.arange(El, device=dev) - cstart[start_of]
-        tf = torch.nonzero((within % self.TILE) == 0).view(-1)
-        cend = torch.cat([cstart[1:], torch.tensor([El], device=dev)])[start_of[tf]]
-        self.tile_first = tf.to(torch.int32).contiguous()
-        self.tile_n = torch.clamp(cend - tf, max=self.TILE).to(torch.int32).contiguous()
-        self.tile_cls = cls_sorted[tf].to(torch.int32).contiguous()
-        self.order = order.to(torch.int32).contiguous()
-        self.sub = sub_canon.to(torch.int32).contiguous()
+        cstart = torch.nonzero(newc).view(-1).tolist() + [El]
+        self.blocks = [(int(cls_sorted[a]), a, b) for a, b in zip(cstart[:-1], cstart[1:])]
+        self.invT = inv.transpose(1, 2).contiguous()
+        del inv
+        self.order = order
+        self.row_cls = cls_sorted
+        inv_order = torch.empty_like(order)
+        inv_order[order] = torch.arange(El, device=dev)
+        self.sub = sub_canon[order].to(torch.int32).contiguous()
         valid = sub_canon < L
         del sub, sub_canon
         if El * S >= 2 ** 31:
             raise ConfigError("HybridSchwarz: E * S exceeds int32 slot indexing; partition the mesh")
 
+        def flat_pos(vi_):
+            """canonical (subdomain, slot) flat index -> row of the class-ordered sol"""
+            return inv_order[vi_ // S] * S + vi_ % S
+
         # ---- overlap accumulation: node -> (global subdomain, slot), ascending
         #      subdomain; on several ranks the other ranks' solutions on this rank's
         #      gids arrive through an exchange (plan "sol")
         vi = torch.nonzero(valid.view(-1)).view(-1)
-        nsub = self.sub.view(-1)[vi].long()
+        nsub = self.sub.view(-1)[flat_pos(vi)].long()
         gsub = vi // S + e0                                     # global subdomain id
-        ent_node, ent_sub, ent_pos = [nsub], [gsub], [vi]
+        ent_node, ent_sub, ent_pos = [nsub], [gsub], [flat_pos(vi)]
         n_sol = El * S
         self.plan_sol = None
         gid_of_node = torch.cat([loc_nodes, rem])
@@ -602,7 +606,7 @@ class HybridSchwarz:
                 m_ = has[q][nsub]
                 if not bool(m_.any()):
                     continue
-                gq, sq, fq = gid_of_node[nsub[m_]], gsub[m_], vi[m_]
+                gq, sq, fq = gid_of_node[nsub[m_]], gsub[m_], flat_pos(vi[m_])
                 o = _lexsort2(gq, sq)
                 send_meta[q] = torch.stack([gq[o], sq[o]], dim=1)
                 send_flat[q] = fq[o]
@@ -758,6 +762,7 @@ class HybridSchwarz:
         self.cpart = f64(2 * nblk)
         self.cbar = torch.zeros(2, dtype=torch.int32, device=dev)
         self.sol = f64(n_sol)
+        self.rwg = f64(n_sol)
         self.z = f64(Lloc)
         self.sol_recv = f64(max(self.plan_sol.n_recv_total, 1)) if self.plan_sol is not None else None
         self._ipc = {}
@@ -782,9 +787,7 @@ class HybridSchwarz:
         st.xc, st.cr, st.cz, st.cp, st.cap = (pt(t) for t in (self.xc, self.cr, self.cz, self.cp, self.cap))
         st.cpart, st.cbar = pt(self.cpart), pt(self.cbar)
         st.coarse_iters, st.coarse_blocks = self.coarse_iters, nblk
-        st.inv, st.n_tiles = pt(self.inv), int(self.tile_first.numel())
-        st.tile_first, st.tile_n, st.tile_cls = pt(self.tile_first), pt(self.tile_n), pt(self.tile_cls)
-        st.order, st.sub, st.sol = pt(self.order), pt(self.sub), pt(self.sol)
+        st.sub, st.rwg, st.sol = pt(self.sub), pt(self.rwg), pt(self.sol)
         st.sol_recv, st.n_sol = pt(self.sol_recv), n_sol
         st.acc_off, st.acc_pos = pt(self.acc_off), pt(self.acc_pos)
         st.cvert, st.ccorn, st.constrained, st.z = pt(self.cvert), pt(self.ccorn), pt(self.constrained), pt(self.z)
@@ -799,7 +802,7 @@ class HybridSchwarz:
         ipc = self._ipc[name]
         recv = ipc.exchange(src)
         if recv is not None and ipc.plan.n_recv_total:
-            _lib.call("sf_halo_unbank_f64", recv.ptr, recv.seq_ptr, recv.bank, ipc.plan.n_recv_total,
+            _lib.call("sf_halo_unbank_f64", recv.data_ptr(), recv.seq_ptr, recv.bank, ipc.plan.n_recv_total,
                       _lib.ptr(dst), _lib.stream_ptr(self.space.device))
 
     @staticmethod
@@ -850,28 +853,32 @@ class HybridSchwarz:
         return cand, bi_c.view(R, C, nn), sub_c
 
     def apply_into(self, r, out):
-        """out <- M^-1 r (HybridSchwarz.__call__, precond.py:239-250); r, out: fields."""
+        """out <- M^-1 r (HybridSchwarz.__call__, precond.py:239-250); r, out: fields.
+        Stream-ordered, no host synchronisation (capturable in a CUDA graph)."""
         from . import _lib
 
         st = ctypes.addressof(self._st)
         stream = _lib.stream_ptr(self.space.device)
-        r = r.contiguous()
-        if not self._ipc:
-            _lib.call("sf_schwarz_apply_f64", st, _lib.ptr(r), _lib.ptr(out), stream)
-            self.launches += 6
-            return out
         comm = self.space.comm
-        _lib.call("sf_schwarz_gather_f64", st, _lib.ptr(r), stream)
-        self._exchange_into("layer", self.rw, self.rw[self.G:])
+        multi = bool(self._ipc)
+        _lib.call("sf_schwarz_gather_f64", st, _lib.ptr(r.contiguous()), stream)
+        if multi:
+            self._exchange_into("layer", self.rw, self.rw[self.G:])
         _lib.call("sf_schwarz_restrict_f64", st, stream)
-        self._exchange_into("rc", self.rc_part, self.rc_recv)
-        _lib.call("sf_schwarz_rank_sum_f64", st, _lib.ptr(self.rc_recv), comm.rank, comm.world, stream)
+        if multi:
+            self._exchange_into("rc", self.rc_part, self.rc_recv)
+            _lib.call("sf_schwarz_rank_sum_f64", st, _lib.ptr(self.rc_recv), comm.rank, comm.world, stream)
         _lib.call("sf_schwarz_coarse_f64", st, stream)
-        _lib.call("sf_schwarz_local_f64", st, stream)
-        self._exchange_into("sol", self.sol, self.sol_recv)
+        _lib.call("sf_schwarz_gather_rw_f64", st, stream)
+        S = self.S
+        rwg, sol = self.rwg.view(-1, S), self.sol.view(-1, S)
+        for c, a, b in self.blocks:                 # one FP64 GEMM per subdomain class
+            torch.matmul(rwg[a:b], self.invT[c], out=sol[a:b])
+        if multi:
+            self._exchange_into("sol", self.sol, self.sol_recv)
         _lib.call("sf_schwarz_finalize_f64", st, stream)
         _lib.call("sf_schwarz_scatter_f64", st, _lib.ptr(out), stream)
-        self.launches += 16
+        self.launches += 6 + len(self.blocks) + (8 if multi else 0)
         return out
 
     def __call__(self, r):

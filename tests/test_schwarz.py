@@ -86,7 +86,7 @@ def test_schwarz_tgv_steps(cuda, golden_schwarz):
 
 
 def test_schwarz_kernel_vs_host_restatement(cuda):
-    """sf_schwarz_apply_f64 against the numpy restatement of its six launches on
+    """HybridSchwarz.apply_into against the numpy restatement of its stages on
     the same device-built structures (tests/test_schwarz_setup.py::_emulate)."""
     from test_schwarz_setup import _emulate
 

@@ -77,7 +77,7 @@ def _oracle_element_matrices(oracle, osp):
 
 
 def _emulate(hs, r):
-    """numpy restatement of sf_schwarz_apply_f64 (csrc/schwarz.cu) on hs's buffers."""
+    """numpy restatement of HybridSchwarz.apply_into (csrc/schwarz.cu stages + class GEMMs)."""
     t = lambda x: x.cpu().numpy()
     G, S, nn = hs.G, hs.S, hs.space.n ** 3
     first, wsqrt, tw = t(hs.first), t(hs.wsqrt), t(hs.tw)
@@ -119,13 +119,10 @@ def _emulate(hs, r):
             p = z + (rzn / rz) * p
             rz = rzn
     # local solves
-    sub, inv, order = t(hs.sub).astype(np.int64), t(hs.inv), t(hs.order)
-    tf, tn, tc = t(hs.tile_first), t(hs.tile_n), t(hs.tile_cls)
+    sub, invT, rcls = t(hs.sub).astype(np.int64), t(hs.invT), t(hs.row_cls)
     sol = np.zeros(sub.shape)
-    for k in range(tf.size):
-        for j in range(tn[k]):
-            e = order[tf[k] + j]
-            sol[e] = inv[tc[k]] @ rw[sub[e]]
+    for p_ in range(sub.shape[0]):            # rows in class order: sol = rw[sub] @ inv^T
+        sol[p_] = rw[sub[p_]] @ invT[rcls[p_]]
     # finalize + scatter
     off, pos = t(hs.acc_off), t(hs.acc_pos)
     cvert, ccorn, con = t(hs.cvert), t(hs.ccorn), t(hs.constrained)
@@ -230,8 +227,8 @@ def _rank_worker(rank, world, port, payload, q):
         hs = precond.HybridSchwarz(sp, mask=mk, lam_visc=1.0, lam_mass=lm)
         t = lambda x: x.cpu().numpy()
         out = {k: t(getattr(hs, k)) for k in ("first", "wsqrt", "tw", "pt_ptr", "pt_ent", "vfixed", "ac_col",
-                                             "ac_val", "coarse_inv_diag", "sub", "inv", "order", "tile_first",
-                                             "tile_n", "tile_cls", "acc_off", "acc_pos", "cvert", "ccorn",
+                                             "ac_val", "coarse_inv_diag", "sub", "invT", "row_cls", "acc_off",
+                                             "acc_pos", "cvert", "ccorn",
                                              "constrained", "gid")}
         out.update(G=hs.G, L=hs.L, S=hs.S, nv=hs.nv, iters=hs.coarse_iters, e0=e0, e1=e1,
                    layer={p: t(v) for p, v in hs.plan_layer.send_idx.items()},
@@ -300,10 +297,8 @@ def _emulate_ranks(res, r_glob, nn):
     sol = {}
     for k, h in res.items():
         s_ = np.zeros(h["sub"].shape)
-        for t in range(h["tile_first"].size):
-            for j in range(h["tile_n"][t]):
-                e = h["order"][h["tile_first"][t] + j]
-                s_[e] = h["inv"][h["tile_cls"][t]] @ rw[k][h["sub"][e].astype(np.int64)]
+        for p_ in range(s_.shape[0]):
+            s_[p_] = rw[k][h["sub"][p_].astype(np.int64)] @ h["invT"][h["row_cls"][p_]]
         sol[k] = s_.reshape(-1)
     outs = []
     for k, h in res.items():
