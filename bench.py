@@ -515,7 +515,7 @@ def bench_tgv(args, world, rank, dev):
     else:
         ne = args.ne or (64 if args.warmup + args.steps <= 8 else 48)
         sp, st, state = tgv_problem(ne, device=dev, comm=comm, precond=args.precond,
-                                    projection=args.projection == "on",
+                                    projection=args.projection == "on", dealias=args.dealias,
                                     **({"dt": args.dt} if args.dt > 0 else {}))
         P = ne ** 3 * sp.n ** 3            # global points: strong scaling, fixed total work
     for k in range(args.warmup):
@@ -609,6 +609,7 @@ def bench_tgv(args, world, rank, dev):
     else:
         wl_name = (f"TGV Re=1600 {ne}^3 elements lx=8 (config {'3' if ne == 64 else '1' if ne == 8 else '1/3 analogue'}),"
                    f" symmetry box, {'Schwarz' if args.precond == 'schwarz' else 'Jacobi'}-GMRES(20) p 1e-5,"
+                   f"{' dealiased convection (3/2 rule),' if args.dealias else ''}"
                    f" Jacobi-PCG v 1e-8, projection {args.projection}")
         metric = "GDOF/s per time step (TGV, lx=8)"
     return {
@@ -667,6 +668,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--workload", default="tgv", choices=("tgv", "poisson", "channel", "cylinder"))
     ap.add_argument("--ne", type=int, default=0)
+    ap.add_argument("--dealias", action="store_true",
+                    help="TGV: over-integrated convection (operators.Dealias, 3/2 rule)")
     ap.add_argument("--restart", type=int, default=20,
                     help="cylinder: pressure GMRES restart (20 as the reference; 10 frees 10 fields)")
     ap.add_argument("--projection", default="on", choices=("on", "off"),

@@ -318,6 +318,16 @@ int sf_trilinear_coords_f64(const double* corners, const double* wc, int n, long
 int sf_metrics_f64(const double* d_host, const double* w_host, int n, const double* coords,
                    long long E, double* rx, double* jac, double* bm, double* geom, void* stream);
 
+/* Over-integrated convection in one launch (Dealias.advect via advect_vec,
+ * operators.py:119-158): out (3, E, n^3) = sign * project_back(wjac_f *
+ * sum_l to_fine(c_l) to_fine(grad_l v_f)) / bm, every fine-grid field in shared
+ * memory.  d_host (n x n) GLL derivative and j_host (m x n) GLL -> GL
+ * interpolation are HOST arrays; (n, m) in {(8, 12), (6, 9), (4, 6)}; wjac_f
+ * (E, m^3); exact = 1: the reference's contraction order without FMA. */
+int sf_dealias_advect_f64(const double* d_host, const double* j_host, int n, int m, const double* c,
+                          const double* v, const double* rx, const double* wjac_f, const double* bm, long long E,
+                          double sign, double* out, int exact, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Hybrid overlapping Schwarz preconditioner (precond.py:94-250)
  * ------------------------------------------------------------------------- */

@@ -70,6 +70,7 @@ _SIGS = {
     "sf_halo_wait": [_vp, _i, _vp, _vp, _vp],
     "sf_trilinear_coords_f64": [_vp, _vp, _i, _ll, _vp, _vp],
     "sf_metrics_f64": [_vp, _vp, _i, _vp, _ll, _vp, _vp, _vp, _vp, _vp],
+    "sf_dealias_advect_f64": [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _ll, _d, _vp, _i, _vp],
     "sf_schwarz_gather_f64": [_vp, _vp, _vp],
     "sf_schwarz_restrict_f64": [_vp, _vp],
     "sf_schwarz_rank_sum_f64": [_vp, _vp, _i, _i, _vp],
@@ -127,7 +128,7 @@ NVTX_TAGS = {
     "sf_dssum_f64": "K2 dssum", "sf_dssum_cls_f64": "K2 dssum", "sf_dssum_blk_f64": "K2 dssum",
     "sf_gs_gather_f64": "K2 dssum", "sf_gs_scatter_f64": "K2 dssum", "sf_gather_f64": "K2 dssum",
     "sf_grad_ref_f64": "K3 deriv", "sf_deriv_f64": "K3 deriv", "sf_cfl_f64": "K3 deriv",
-    "sf_cdtp_f64": "K4 cdtp", "sf_apply_axis_f64": "K4 cdtp", "sf_apply_axis3_f64": "K4 cdtp",
+    "sf_cdtp_f64": "K4 cdtp", "sf_dealias_advect_f64": "K4 cdtp", "sf_apply_axis_f64": "K4 cdtp", "sf_apply_axis3_f64": "K4 cdtp",
     "sf_glsc3_f64": "K5 glsc3", "sf_glsc3_peer_f64": "K5 glsc3",
     "sf_cg_init_f64": "K6 pcg", "sf_cg_update_f64": "K6 pcg", "sf_cg_direction_f64": "K6 pcg",
     "sf_mgs_step_f64": "K7 gmres", "sf_mgs_step_peer_f64": "K7 gmres", "sf_gmres_gate_f64": "K7 gmres",

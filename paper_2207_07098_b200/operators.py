@@ -179,8 +179,7 @@ def advect_vec(space, c, v, dealias=None, sign=1.0):
     """(c . grad) v_l for l = 0, 1, 2 (operators.py:108-126): collocation, or
     over-integrated on the Gauss-Legendre grid with a :class:`Dealias`."""
     if dealias is not None:
-        out = dealias.advect_vec(c, v)
-        return out if sign == 1.0 else out * sign
+        return dealias.advect_vec(c, v, sign=sign)
     return _deriv(space, OP_ADVECT, v, c=c, sign=sign)
 
 
@@ -243,9 +242,20 @@ class Dealias:
     def advect(self, c, u):
         return self._advect_fine([self._to_fine(c[l]) for l in range(3)], u)
 
-    def advect_vec(self, c, v):
+    def advect_vec(self, c, v, sign=1.0, out=None):
+        """sign * (c . grad) v_l for l = 0, 1, 2, over-integrated.  lx = 4, 6, 8: one
+        fused launch per call (csrc/dealias.cu: every fine-grid field lives in
+        shared memory); other orders: the contraction chain."""
+        sp = self.space
+        if (sp.n, self.m) in ((8, 12), (6, 9), (4, 6)):
+            out = torch.empty((3,) + sp.shape, dtype=torch.float64, device=sp.device) if out is None else out
+            _lib.call("sf_dealias_advect_f64", sp.dmat.ctypes.data, self.interp.ctypes.data, sp.n, self.m,
+                      _lib.ptr(c.contiguous()), _lib.ptr(v.contiguous()), _lib.ptr(sp.rx), _lib.ptr(self.wjac_f),
+                      _lib.ptr(sp.bm), sp.n_elements, float(sign), _lib.ptr(out), _ex(), _lib.stream_ptr(sp.device))
+            return out
         cf = [self._to_fine(c[l]) for l in range(3)]     # the advecting field, once
-        return torch.stack([self._advect_fine(cf, v[l]) for l in range(3)])
+        res = torch.stack([self._advect_fine(cf, v[l]) for l in range(3)])
+        return res if sign == 1.0 else res * sign
 
 
 def weak_grad_dot(space, w, out=None):

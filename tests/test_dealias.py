@@ -78,3 +78,25 @@ def test_dealiased_tgv_steps(cuda):
         assert d.p_iterations == row["p_it"] and list(d.v_iterations) == row["v_it"]
         assert rel_err(kinetic_energy(sp, state.vel), row["ke"]) < 1e-9
         assert rel_err(enstrophy(sp, state.vel), row["ens"]) < 1e-9
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order", [3, 5, 7])
+def test_fused_dealias_equals_chain(cuda, monkeypatch, order):
+    """sf_dealias_advect_f64 (one launch, fine grid in shared memory) against the
+    contraction chain it replaces: bitwise in exact mode, with the sign applied."""
+    from paper_2207_07098_b200 import _device, operators as ops
+    from paper_2207_07098_b200.basis import make_basis
+    from paper_2207_07098_b200.mesh import gen_box_mesh
+    from paper_2207_07098_b200.space import build_space
+
+    monkeypatch.setattr(_device, "EXACT", True)
+    sp = build_space(gen_box_mesh((0.0, 1.3, 0.0, 1.0, 0.0, 0.7), (3, 2, 2)), make_basis(order), device=cuda)
+    dl = ops.Dealias(sp)
+    g = torch.Generator().manual_seed(order)
+    c = torch.randn((3,) + sp.shape, generator=g, dtype=torch.float64).to(cuda)
+    v = torch.randn((3,) + sp.shape, generator=g, dtype=torch.float64).to(cuda)
+    fused = dl.advect_vec(c, v, sign=-1.0)
+    cf = [dl._to_fine(c[l]) for l in range(3)]
+    chain = -torch.stack([dl._advect_fine(cf, v[l]) for l in range(3)])
+    assert torch.equal(fused, chain)
