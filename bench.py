@@ -509,7 +509,7 @@ def bench_tgv(args, world, rank, dev):
 
         ne = args.ne or 2                    # scale divisor of the config-5 counts
         sp, st, state = cylinder_problem(ne, device=dev, comm=comm, projection=args.projection == "on",
-                                         restart=args.restart)
+                                         restart=args.restart, recycle=True)
         sp.release_setup_fields()          # coords / jac: set-up only (4 fields of HBM)
         P = sp.mesh.n_elements * sp.n ** 3
     else:
