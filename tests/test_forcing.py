@@ -87,3 +87,26 @@ def test_tripped_channel_steps(cuda, tmp_path):
     for _ in range(len(rows) - 1):
         resumed, _ = st2.step(resumed)
     assert torch.equal(resumed.vel, state.vel)
+
+
+@pytest.mark.gpu
+def test_force_field_equals_pointwise(cuda):
+    """force_field evaluates g(z) and the envelope on the distinct coordinate
+    values and gathers: bit-identical to the per-point expression."""
+    import torch
+
+    from paper_2207_07098_b200.basis import make_basis
+    from paper_2207_07098_b200.forcing import TrippingForcing
+    from paper_2207_07098_b200.mesh import gen_box_mesh
+    from paper_2207_07098_b200.space import build_space
+
+    sp = build_space(gen_box_mesh((0.0, 4.0, 0.0, 2.0, 0.0, 3.0), (4, 3, 5)), make_basis(5), device=cuda)
+    trip = TrippingForcing(x0=1.0, y0=0.2, length_x=0.7, length_y=0.3, z_min=0.5, z_max=2.5, amp_steady=0.1,
+                           amp_unsteady=0.3, t_scale=0.14, n_modes=40, seed=3)
+    ref = TrippingForcing(x0=1.0, y0=0.2, length_x=0.7, length_y=0.3, z_min=0.5, z_max=2.5, amp_steady=0.1,
+                          amp_unsteady=0.3, t_scale=0.14, n_modes=40, seed=3)
+    for t in (0.01, 0.2, 0.45):
+        f = trip.force_field(sp, t)
+        x, y, z = sp.coords
+        want = ref.evaluate(x, y, z, t)
+        assert torch.equal(f[1], want) and float(f[0].abs().max()) == 0.0 and float(f[2].abs().max()) == 0.0
