@@ -360,6 +360,15 @@ class _GraphBuffers:
     """Fixed buffers and the per-step CUDA graphs of the look-ahead GMRES for one
     (operator, preconditioner, restart, size) -- kept on the operator."""
 
+    @property
+    def z(self):
+        """Scratch preconditioned vector, allocated on first use (the Jacobi
+        pre-scaled Ax never writes it)."""
+        z = getattr(self, "_z", None)
+        if z is None:
+            z = self._z = torch.empty(self._shape, dtype=torch.float64, device=self._dev)
+        return z
+
     def __init__(self, b, restart, S, key, flexible=False):
         self.key = key
         self.V = torch.empty((restart + 1,) + tuple(b.shape), dtype=torch.float64, device=b.device)
@@ -368,7 +377,8 @@ class _GraphBuffers:
             if flexible else None
         self.blk = torch.zeros((restart, S), dtype=torch.float64, device=b.device)
         self.host = torch.zeros((restart, S), dtype=torch.float64, pin_memory=True)
-        self.z = torch.empty_like(b)
+        self._shape = tuple(b.shape)
+        self._dev = b.device
         self.graphs = {}
         self.counts = {}          # library launches recorded in each captured step
         self.bytes = {}           # and their algorithmic bytes (traffic.py)
@@ -432,7 +442,10 @@ def _gmres_pipelined(F, op, b, tol, max_iter, restart):
     converged = False
     gb = _graph_buffers(F, op, b, restart, S)
     if gb is not None:
-        blk, host, z, Vbuf, Z = gb.blk, gb.host, gb.z, gb.V, gb.Z
+        # the scratch z only where apply_precond writes it (not with the
+        # Jacobi-prescaled Ax, nor with no preconditioner, nor with Schwarz's Z)
+        need_z = F.pc is None and F.invdiag is not None and not (F.sp.n == 8 and _PRE_FUSED)
+        blk, host, z, Vbuf, Z = gb.blk, gb.host, (gb.z if need_z else None), gb.V, gb.Z
     else:
         blk = torch.zeros((restart, S), dtype=torch.float64, device=dev)
         host = torch.zeros((restart, S), dtype=torch.float64, pin_memory=True)
