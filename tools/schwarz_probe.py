@@ -44,9 +44,38 @@ def main():
     ev[1].record()
     torch.cuda.synchronize()
     us = ev[0].elapsed_time(ev[1]) / reps * 1e3
+    # per-stage device time of one application (CUDA events around each stage)
+    from paper_2207_07098_b200 import _lib
+    import ctypes
+
+    st = ctypes.addressof(M._st)
+    stream = _lib.stream_ptr(dev)
+    stages = {}
+
+    def tick(name, fn):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        stages[name] = round(a.elapsed_time(b) * 1e3, 1)
+
+    tick("gather", lambda: _lib.call("sf_schwarz_gather_f64", st, _lib.ptr(r), stream))
+    tick("restrict", lambda: _lib.call("sf_schwarz_restrict_f64", st, stream))
+    tick("coarse", lambda: _lib.call("sf_schwarz_coarse_f64", st, stream))
+    tick("gather_rw", lambda: _lib.call("sf_schwarz_gather_rw_f64", st, stream))
+
+    def gemms():
+        rwg, sol = M.rwg.view(-1, M.S), M.sol.view(-1, M.S)
+        for c, a_, b_ in M.blocks:
+            torch.matmul(rwg[a_:b_], M.invT[c], out=sol[a_:b_])
+    tick("class_gemms", gemms)
+    tick("finalize", lambda: _lib.call("sf_schwarz_finalize_f64", st, stream))
+    tick("scatter", lambda: _lib.call("sf_schwarz_scatter_f64", st, _lib.ptr(z), stream))
     E, S, U = sp.n_elements, M.S, M.n_classes
     print(json.dumps({"ne": ne, "points": sp.n_points, "setup_s": round(t_setup, 2), "classes": U, "S": S,
-                      "apply_us": round(us, 1), "local_solve_gflop": round(2.0 * E * S * S / 1e9, 2),
+                      "apply_us": round(us, 1), "stages_us": stages,
+                      "local_solve_gflop": round(2.0 * E * S * S / 1e9, 2),
                       "mem_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 2)}), flush=True)
 
 

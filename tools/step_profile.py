@@ -24,7 +24,7 @@ def main():
 
     comm = dist.init_from_env()          # torchrun: one rank per GPU, rank 0 reports
     dev = torch.device("cuda", torch.cuda.current_device())
-    sp, st, state = tgv_problem(ne, device=dev, comm=comm)
+    sp, st, state = tgv_problem(ne, device=dev, comm=comm, precond=os.environ.get("PRECOND", "jacobi"))
     for k in range(warm):
         if k == warm - 1 and os.environ.get("RESERVE", "1") == "1":
             st.reserve_projection(steps + 1)     # as bench.py does before its last warm-up step
