@@ -343,8 +343,8 @@ typedef struct SfSchwarz {
   const double* wsqrt;          /* (G) 1 / sqrt(overlap count) */
   double* rg;                   /* (G) work: gathered residual */
   double* rw;                   /* (G + 1) work: wsqrt * rg, rw[G] = 0 (padding slot) */
-  const long long* pt_ptr;      /* (nv + 1) restriction rows (vertex -> gids ascending) */
-  const long long* pt_ent;      /* gid * 8 + corner */
+  const long long* pt_ptr;      /* (nv + 1) restriction rows: vertex -> (element, corner) */
+  const long long* pt_ent;      /*   entries element * 8 + corner, ascending element */
   const double* tw;             /* (nnn, 8) trilinear corner weights */
   const uint8_t* vfixed;        /* (nv) constrained vertices */
   double* rc_part;              /* (nv) work: this rank's restriction (owned gids) */
@@ -364,11 +364,13 @@ typedef struct SfSchwarz {
   const double* sol_recv;       /* N > 1: the peers' solutions on this rank's gids */
   long long n_sol;              /* E * S: acc_pos >= n_sol index sol_recv */
   const long long* acc_off;     /* (G + 1) overlap accumulation: gid -> sol slots, */
-  const long long* acc_pos;     /*   ascending global subdomain */
+  const int* acc_pos;           /*   ascending global subdomain */
   const int* cvert;             /* (E, 8) element corners, ascending vertex id */
   const uint8_t* ccorn;         /* (E, 8) their corner numbers */
   const uint8_t* constrained;   /* (G) Dirichlet gids */
   double* z;                    /* (G) work: assembled correction */
+  const uint8_t* rflag;         /* (P) point carries its gid's owned first copy */
+  double* se;                   /* (E, 8) work: per element corner restriction sums */
 } SfSchwarz;
 
 /* out = M^-1 r for the hybrid Schwarz preconditioner (HybridSchwarz.__call__,

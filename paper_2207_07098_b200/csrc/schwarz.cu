@@ -3,7 +3,7 @@
 // launches, no host synchronisation, CUDA-graph capturable:
 //
 //   gather    rg[g] = r[first copy of g]; rw[g] = wsqrt[g] * rg[g]      (:241-242)
-//   restrict  rc[v] = sum_g (ascending) P[g, v] rg[g]; 0 on fixed v     (:246-247)
+//   restrict  rc = P^T rg: per element corner sums, then per vertex     (:246-247)
 //   coarse    fixed-iteration Jacobi-CG on the vertex problem (:205-230), one
 //             persistent launch with software grid barriers
 //   local     sol_e = A_e^{-1} rw[sub_e] for every subdomain (:243-244): the
@@ -37,29 +37,54 @@ __global__ void sch_gather_kernel(const double* __restrict__ r, const long long*
   }
 }
 
-// rc[v] = sum over the entries k of vertex v (gid-ascending) of tw[p_g*8 + c] * rg[g],
-// entry = g * 8 + c.  A warp per vertex: lane l folds entries l, l+32, ... in
-// order, then a fixed xor tree (a vertex has ~(2n-1)^3 entries; one thread per
-// vertex was latency-bound).
-__global__ void sch_restrict_kernel(const double* __restrict__ rg, const long long* __restrict__ ptr,
-                                    const long long* __restrict__ ent, const long long* __restrict__ first,
-                                    const double* __restrict__ tw, int nnn, long long nv,
-                                    const uint8_t* __restrict__ vfixed, double* __restrict__ rc) {
+// Restriction rc = P^T rg in two deterministic stages.
+//   element: se[e][c] = sum over the points p of e that carry their gid's owned
+//            first copy (rflag) of tw[p, c] * rg[node(p)] -- each gid counted once;
+//            a warp per element, lane-strided points, a fixed xor tree
+//   vertex:  rc[v] = sum over the (e, c) at vertex v, ascending e, of se[e][c]
+// (the reference sums per vertex over gids ascending, precond.py:246; the coarse
+// solve is approximate, one rounding order is as good as another, this one reads
+// every point once and coalesced instead of ~(2n-1)^3 scattered gids per vertex)
+__global__ void sch_restrict_elem_kernel(const double* __restrict__ rg, const long long* __restrict__ node,
+                                         const uint8_t* __restrict__ rflag, const double* __restrict__ tw,
+                                         int nnn, long long E, double* __restrict__ se) {
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long v = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; v < nv; v += warps) {
-    double acc = 0.0;
-    if (!vfixed[v]) {
-      for (long long k = ptr[v] + lane; k < ptr[v + 1]; k += 32) {
-        const long long e = ent[k];
-        const long long g = e >> 3;
-        const int p = (int)(first[g] % nnn);
-        acc = __dadd_rn(acc, __dmul_rn(tw[p * 8 + (int)(e & 7)], rg[g]));
+  for (long long e = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; e < E; e += warps) {
+    double acc[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+    for (int p = lane; p < nnn; p += 32) {
+      const long long q = e * nnn + p;
+      if (rflag[q]) {
+        const double v = rg[node[q]];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(tw[p * 8 + c], v));
       }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-    if (lane == 0) rc[v] = acc;
+    for (int c = 0; c < 8; ++c)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[c] = __dadd_rn(acc[c], __shfl_xor_sync(0xffffffffu, acc[c], o));
+    if (lane < 8) {
+      double mine = acc[0];
+#pragma unroll
+      for (int c = 1; c < 8; ++c)
+        if (lane == c) mine = acc[c];
+      se[e * 8 + lane] = mine;
+    }
+  }
+}
+
+__global__ void sch_restrict_vert_kernel(const double* __restrict__ se, const long long* __restrict__ vptr,
+                                         const long long* __restrict__ vent, long long nv,
+                                         const uint8_t* __restrict__ vfixed, double* __restrict__ rc) {
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nv;
+       v += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    if (!vfixed[v])
+      for (long long k = vptr[v]; k < vptr[v + 1]; ++k) acc = __dadd_rn(acc, se[vent[k]]);
+    rc[v] = acc;
   }
 }
 
@@ -210,7 +235,7 @@ __global__ void sch_gather_rw_kernel(const double* __restrict__ rw, const int* _
 // first element in ascending vertex id of tw[p*8+c] * xc[vertex]
 __global__ void sch_finalize_kernel(const double* __restrict__ sol, const double* __restrict__ sol_recv,
                                     long long n_sol, const long long* __restrict__ off,
-                                    const long long* __restrict__ pos, const double* __restrict__ wsqrt,
+                                    const int* __restrict__ pos, const double* __restrict__ wsqrt,
                                     const long long* __restrict__ first, int nnn,
                                     const int* __restrict__ cvert, const uint8_t* __restrict__ ccorn,
                                     const double* __restrict__ tw, const double* __restrict__ xc,
@@ -306,9 +331,13 @@ int sf_schwarz_gather_f64(const SfSchwarz* s, const double* r, void* stream) {
 int sf_schwarz_restrict_f64(const SfSchwarz* s, void* stream) {
   using namespace sf;
   if (bad(s, "sf_schwarz_restrict_f64")) return SF_ERR_ARG;
-  sch_restrict_kernel<<<grid_for(s->nv * 32), 256, 0, as_stream(stream)>>>(s->rg, s->pt_ptr, s->pt_ent, s->first,
-                                                                     s->tw, s->nnn, s->nv, s->vfixed, s->rc_part);
-  return check_launch("schwarz restrict");
+  const long long E = s->P / s->nnn;
+  sch_restrict_elem_kernel<<<grid_for(E * 32), 256, 0, as_stream(stream)>>>(s->rg, s->gid, s->rflag, s->tw, s->nnn,
+                                                                          E, s->se);
+  if (int e = check_launch("schwarz restrict (elements)")) return e;
+  sch_restrict_vert_kernel<<<grid_for(s->nv), 256, 0, as_stream(stream)>>>(s->se, s->pt_ptr, s->pt_ent, s->nv,
+                                                                          s->vfixed, s->rc_part);
+  return check_launch("schwarz restrict (vertices)");
 }
 
 // N > 1: rc = rank-order sum of every rank's rc_part (own + received partials)

@@ -255,7 +255,7 @@ class _SchwarzStruct(ctypes.Structure):
         ("sol_recv", ctypes.c_void_p), ("n_sol", ctypes.c_longlong),
         ("acc_off", ctypes.c_void_p), ("acc_pos", ctypes.c_void_p),
         ("cvert", ctypes.c_void_p), ("ccorn", ctypes.c_void_p), ("constrained", ctypes.c_void_p),
-        ("z", ctypes.c_void_p),
+        ("z", ctypes.c_void_p), ("rflag", ctypes.c_void_p), ("se", ctypes.c_void_p),
     ]
 
 
@@ -423,8 +423,16 @@ class HybridSchwarz:
 
         # ---- node space: gids with an own copy first (ascending), then the other
         #      ranks' layer gids grouped by the rank that provides them
-        loc_nodes = torch.unique(gid_X[i0:i0 + El])
+        loc_nodes, loc_inv = torch.unique(gid_X[i0:i0 + El], return_inverse=True)
         Lloc = int(loc_nodes.numel())
+        # own nodes are numbered in the order of their first local copy (element
+        # major): the gather, the overlap sums and the scatter then walk memory in
+        # element order instead of the gids' coordinate order
+        fpt = torch.full((Lloc,), P, dtype=torch.int64, device=dev)
+        fpt.scatter_reduce_(0, loc_inv.reshape(-1), torch.arange(P, device=dev), reduce="amin")
+        loc_rank = torch.empty(Lloc, dtype=torch.int64, device=dev)
+        loc_rank[torch.argsort(fpt)] = torch.arange(Lloc, device=dev)
+        del fpt, loc_inv
         vsub = subg[subg < BIG]
         pos = torch.searchsorted(loc_nodes, vsub).clamp(max=Lloc - 1)
         rem = torch.unique(vsub[loc_nodes[pos] != vsub])
@@ -448,7 +456,7 @@ class HybridSchwarz:
         def node_of(g, unused):
             """global gid -> node index (``unused`` where it is not a node)."""
             p1 = torch.searchsorted(loc_nodes, g).clamp(max=Lloc - 1)
-            out = torch.where(loc_nodes[p1] == g, p1, torch.full_like(g, unused))
+            out = torch.where(loc_nodes[p1] == g, loc_rank[p1], torch.full_like(g, unused))
             if rem.numel():
                 p2 = torch.searchsorted(rem_sorted, g).clamp(max=rem.numel() - 1)
                 out = torch.where((out == unused) & (rem_sorted[p2] == g), Lloc + rem_ord[p2], out)
@@ -594,7 +602,9 @@ class HybridSchwarz:
         ent_node, ent_sub, ent_pos = [nsub], [gsub], [flat_pos(vi)]
         n_sol = El * S
         self.plan_sol = None
-        gid_of_node = torch.cat([loc_nodes, rem])
+        gid_of_node = torch.empty(L, dtype=torch.int64, device=dev)
+        gid_of_node[loc_rank] = loc_nodes
+        gid_of_node[Lloc:] = rem
         if W > 1:
             has = torch.zeros((W, L + 2), dtype=torch.bool, device=dev)
             for q in range(W):
@@ -624,7 +634,9 @@ class HybridSchwarz:
         keep_e = en < Lloc
         en, es, ep = en[keep_e], es[keep_e], ep[keep_e]
         o = _lexsort2(en, es)
-        self.acc_pos = ep[o].contiguous()
+        if int(ep.max()) >= 2 ** 31 if ep.numel() else False:
+            raise ConfigError("HybridSchwarz: solution slots exceed int32 indexing")
+        self.acc_pos = ep[o].to(torch.int32).contiguous()
         cnt = torch.bincount(en, minlength=Lloc)
         self.acc_off = torch.zeros(Lloc + 1, dtype=torch.int64, device=dev)
         self.acc_off[1:] = torch.cumsum(cnt, 0)
@@ -666,39 +678,20 @@ class HybridSchwarz:
         gfirst.scatter_reduce_(0, gidn_X.reshape(-1), gflat, reduce="amin")
         owned = gfirst[:Lloc] == self.first + e0 * nn
         del gflat, gfirst
-        fe, fp = self.first // nn, self.first % nn
         cv, cc = torch.sort(loc_el, dim=1)
         self.cvert = cv.to(torch.int32).contiguous()
         self.ccorn = cc.to(torch.uint8).contiguous()
-        # restriction rows: (vertex, node ascending) over the nonzero weights of each
-        # owned node's first element (explicit zeros of the reference's CSR add
-        # nothing); a chunked stable counting sort by vertex
-        nzw = tw != 0.0
-        own_nodes = torch.nonzero(owned).view(-1)
-        cnt = torch.zeros(nv, dtype=torch.int64, device=dev)
-        step = 1 << 24
-        for g0 in range(0, own_nodes.numel(), step):
-            gsel = own_nodes[g0:g0 + step]
-            m_ = nzw[fp[gsel]]
-            cnt += torch.bincount(loc_el[fe[gsel]][m_], minlength=nv)
+        # restriction rc = P^T rg (csrc/schwarz.cu): per element, the points that
+        # carry their gid's owned first copy add tw[p, c] rg to corner c; per
+        # vertex, the (element, corner) sums in ascending element order
+        pts = torch.arange(P, device=dev)
+        self.rflag = ((self.first[lnode] == pts) & owned[lnode]).to(torch.uint8).contiguous()
+        vv = loc_el.reshape(-1)
+        o = torch.sort(vv, stable=True).indices
+        self.pt_ent = o.contiguous()                          # = element * 8 + corner
         self.pt_ptr = torch.zeros(nv + 1, dtype=torch.int64, device=dev)
-        self.pt_ptr[1:] = torch.cumsum(cnt, 0)
-        self.pt_ent = torch.empty(int(self.pt_ptr[-1]), dtype=torch.int64, device=dev)
-        fill = self.pt_ptr[:-1].clone()
-        for g0 in range(0, own_nodes.numel(), step):
-            gsel = own_nodes[g0:g0 + step]
-            m_ = nzw[fp[gsel]]                                                   # (B, 8)
-            gi, ci = torch.nonzero(m_, as_tuple=True)                            # node-ascending
-            vv = loc_el[fe[gsel][gi], ci]
-            o = torch.sort(vv, stable=True).indices
-            vv, ent = vv[o], (gsel[gi] * 8 + ci)[o]
-            newv = torch.ones_like(vv, dtype=torch.bool)
-            newv[1:] = vv[1:] != vv[:-1]
-            run = torch.arange(vv.numel(), device=dev)
-            head = torch.cummax(torch.where(newv, run, torch.zeros_like(run)), 0).values
-            self.pt_ent[fill[vv] + (run - head)] = ent
-            fill += torch.bincount(vv, minlength=nv)
-        del cnt, fill
+        self.pt_ptr[1:] = torch.cumsum(torch.bincount(vv, minlength=nv), 0)
+        del pts, vv, o
         # vertex blocks t^T A_e t of this rank's elements, summed per (i, j) in
         # element order; across ranks the partial sums add in rank order
         lcls = ecls[i0:i0 + El]
@@ -763,6 +756,7 @@ class HybridSchwarz:
         self.cbar = torch.zeros(2, dtype=torch.int32, device=dev)
         self.sol = f64(n_sol)
         self.rwg = f64(n_sol)
+        self.se = f64(El * 8)
         self.z = f64(Lloc)
         self.sol_recv = f64(max(self.plan_sol.n_recv_total, 1)) if self.plan_sol is not None else None
         self._ipc = {}
@@ -791,6 +785,7 @@ class HybridSchwarz:
         st.sol_recv, st.n_sol = pt(self.sol_recv), n_sol
         st.acc_off, st.acc_pos = pt(self.acc_off), pt(self.acc_pos)
         st.cvert, st.ccorn, st.constrained, st.z = pt(self.cvert), pt(self.ccorn), pt(self.constrained), pt(self.z)
+        st.rflag, st.se = pt(self.rflag), pt(self.se)
         self._st = st
         self.launches = 0
 
