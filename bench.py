@@ -502,7 +502,7 @@ def bench_tgv(args, world, rank, dev):
 
         counts = (48, 32, 48) if not args.ne else (args.ne, max(1, 2 * args.ne // 3), args.ne)
         ne = counts
-        sp, st, state = channel_problem(counts, device=dev, comm=comm)
+        sp, st, state = channel_problem(counts, device=dev, comm=comm, precond=args.precond)
         P = counts[0] * counts[1] * counts[2] * sp.n ** 3
     elif args.workload == "cylinder":
         from paper_2207_07098_b200.timestep import cylinder_problem
@@ -598,7 +598,8 @@ def bench_tgv(args, world, rank, dev):
     mgs_gbs = mgs_bytes / t_mgs / 1e9
     if args.workload == "channel":
         wl_name = (f"channel {ne[0]}x{ne[1]}x{ne[2]} elements lx=8 (config 4{'' if ne == (48, 32, 48) else ' analogue'}),"
-                   " Poiseuille inflow/outflow/no-slip/symmetry, nu=1/2800 dt=2e-3, Jacobi-GMRES(20) p 1e-5,"
+                   " Poiseuille inflow/outflow/no-slip/symmetry, nu=1/2800 dt=2e-3,"
+                   f" {'Schwarz' if args.precond == 'schwarz' else 'Jacobi'}-GMRES(20) p 1e-5,"
                    f" Jacobi-PCG v 1e-8, projection {args.projection}")
         metric = "GDOF/s per time step (channel, lx=8)"
     elif args.workload == "cylinder":

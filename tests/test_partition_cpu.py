@@ -3,7 +3,7 @@ build, on CPU over gloo: every rank builds only its element range's numbering
 and halo plan, and must get exactly what the global build gives it
 (dist.build_halo_plan over the reference-order global maps) -- gid slice,
 multiplicities, shared maps, send lists and receive counts -- on a perturbed
-box and on the curved cylinder mini-rotor mesh, at 2, 3 and 4 ranks.
+box (2, 3, 4 and 8 ranks) and on the curved cylinder mini-rotor mesh (2, 3, 4).
 """
 
 import os
@@ -78,8 +78,8 @@ def _rotor():
     return mesh_from_golden(load_npz("spaces.npz"), "rotor"), 5
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
-@pytest.mark.parametrize("case", ["box", "rotor"])
+@pytest.mark.parametrize("world,case", [(2, "box"), (3, "box"), (4, "box"), (8, "box"),
+                                        (2, "rotor"), (3, "rotor"), (4, "rotor")])
 def test_partitioned_numbering_equals_global(oracle, world, case):
     mesh, order = _box(oracle) if case == "box" else _rotor()
     osp = oracle.build_space(mesh, oracle.make_basis(order))
