@@ -7,7 +7,6 @@ sm_100a Ax_helm launch (mask applied on load, output select fused) followed by
 one in-place dssum over the shared gids.
 """
 
-import math
 import os
 
 import numpy as np

@@ -26,7 +26,6 @@ Everything is torch (CUDA on the GPU box, CPU + gloo in the tests), O(P / N)
 memory per rank plus the interface, and bitwise equal to the global build.
 """
 
-import numpy as np
 import torch
 
 from . import dist as _dist
