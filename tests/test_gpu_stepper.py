@@ -222,6 +222,43 @@ def test_mini_rotor_steps(cuda):
         assert rel_err(kinetic_energy(sp, state.vel), row["ke"]) < 1e-7
 
 
+def test_mini_rotor_schwarz_steps(cuda):
+    """pkg/cases/mini_rotor.json as shipped: the reference's DEFAULT hybrid Schwarz
+    pressure preconditioner on the curved, unstructured mini-rotor mesh (every
+    subdomain distinct: one inverse per element), projection on; per-step counts,
+    CFL, kinetic energy and enstrophy against the reference
+    (tests/golden/make_rotor_schwarz_golden.py)."""
+    import json
+    import os
+
+    from paper_2207_07098_b200.basis import make_basis
+    from paper_2207_07098_b200.bc import BoundarySet
+    from paper_2207_07098_b200.mesh import gen_cylinder_box_mesh
+    from paper_2207_07098_b200.space import build_space
+    from paper_2207_07098_b200.timestep import SolverOptions, Stepper, enstrophy, kinetic_energy
+
+    specs = {"inflow": {"kind": "inflow", "u_cl": 1.0, "h": 2.0}, "outflow": {"kind": "outflow"},
+             "bottom": {"kind": "noslip"}, "top": {"kind": "symmetry"}, "span": {"kind": "symmetry"},
+             "cylinder": {"kind": "rotor", "u_cl": 1.0, "alpha": 3.0, "delta": 0.25}}
+    with open(os.path.join(os.path.dirname(__file__), "golden", "rotor_schwarz_steps.json")) as fh:
+        rows = json.load(fh)["rows"]
+    m = gen_cylinder_box_mesh(1.0, (-4.0, 6.0), (-4.0, 4.0), 2.0, n_azimuthal=8, n_radial=2, n_axial=2,
+                              n_upstream=4, n_downstream=5, n_front=3, n_back=3, geom_order=5)
+    sp = build_space(m, make_basis(5), device=cuda)
+    st = Stepper(sp, BoundarySet(sp, specs), nu=1.0 / 100.0, dt=2e-3, scheme_order=3,
+                 pressure=SolverOptions(tol=1e-5, max_iter=200, restart=20, precond="schwarz"),
+                 velocity=SolverOptions(tol=1e-8, max_iter=100, precond="jacobi"))
+    v0 = torch.zeros((3,) + sp.shape, dtype=torch.float64, device=cuda)
+    v0[0] = 1.0
+    state = st.initial_state(v0)
+    for row in rows:
+        state, d = st.step(state)
+        assert d.p_iterations == row["p_it"] and list(d.v_iterations) == row["v_it"], (d, row)
+        assert rel_err(d.cfl, row["cfl"]) < 1e-8
+        assert rel_err(kinetic_energy(sp, state.vel), row["ke"]) < 1e-9
+        assert rel_err(enstrophy(sp, state.vel), row["ens"]) < 1e-9
+
+
 def test_primed_taylor_green(cuda):
     """primed_state (timestep.py:174-200) with taylor_green walls: full-order steps
     from an exact history; counts, KE and the error against the analytic vortex."""
