@@ -371,6 +371,7 @@ typedef struct SfSchwarz {
   double* z;                    /* (G) work: assembled correction */
   const uint8_t* rflag;         /* (P) point carries its gid's owned first copy */
   double* se;                   /* (E, 8) work: per element corner restriction sums */
+  long long L;                  /* nodes incl. the peers' layer nodes; rw has L + 1 */
 } SfSchwarz;
 
 /* out = M^-1 r for the hybrid Schwarz preconditioner (HybridSchwarz.__call__,

@@ -11,7 +11,9 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsemflow_b200.so")
+# SEMFLOW_B200_CHECKED=1: the build with device bounds checks (build.py --checked)
+LIB_PATH = os.path.join(_HERE, "libsemflow_b200_checked.so"
+                        if os.environ.get("SEMFLOW_B200_CHECKED", "0") not in ("", "0") else "libsemflow_b200.so")
 
 _lib = None
 

@@ -14,6 +14,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsemflow_b200.so")
+# the checked build: device bounds checks (SF_CHECK in csrc/common.cuh) compiled in
+OUT_CHECKED = os.path.join(HERE, "libsemflow_b200_checked.so")
 ROOT = os.path.dirname(HERE)
 
 NVCC_FLAGS = [
@@ -30,26 +32,29 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
-def _stale():
-    if not os.path.exists(OUT):
+def _stale(out=OUT):
+    if not os.path.exists(out):
         return True
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh"))
     deps.append(os.path.join(ROOT, "include", "semflow_b200.h"))
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
-        return OUT
+def build(force=False, verbose=False, checked=False):
+    out = OUT_CHECKED if checked else OUT
+    if not force and not _stale(out):
+        return out
     from concurrent.futures import ThreadPoolExecutor
 
     nvcc = os.environ.get("NVCC", "nvcc")
-    os.makedirs(OBJDIR, exist_ok=True)
+    objdir = OBJDIR + ("_checked" if checked else "")
+    os.makedirs(objdir, exist_ok=True)
+    flags = NVCC_FLAGS + (["-DSF_CHECKS"] if checked else [])
     jobs = []
     for src in sources():
-        obj = os.path.join(OBJDIR, os.path.basename(src)[:-3] + ".o")
-        jobs.append((obj, [nvcc, *NVCC_FLAGS, "-c", src, "-o", obj]))
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        jobs.append((obj, [nvcc, *flags, "-c", src, "-o", obj]))
 
     def run(job):
         if verbose:
@@ -60,10 +65,10 @@ def build(force=False, verbose=False):
     with ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
         objs = list(ex.map(run, jobs))
     subprocess.run([nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
-                    "-o", OUT + ".tmp", *objs], check=True)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+                    "-o", out + ".tmp", *objs], check=True)
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

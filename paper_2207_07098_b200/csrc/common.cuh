@@ -10,6 +10,26 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Device-side bounds checks of the checked build (libsemflow_b200_checked.so,
+// nvcc -DSF_CHECKS; SEMFLOW_B200_CHECKED=1 loads it): an index out of range traps
+// the kernel with the failing condition printed -- this pool closes
+// compute-sanitizer, so the GPU tests run against this build instead.
+#ifdef SF_CHECKS
+#include <cstdio>
+#define SF_CHECK(cond)                                                                           \
+  do {                                                                                           \
+    if (!(cond)) {                                                                               \
+      printf("SF_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond,     \
+             (int)blockIdx.x, (int)threadIdx.x);                                                  \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define SF_CHECK(cond) \
+  do {              \
+  } while (0)
+#endif
+
 namespace sf {
 
 template <bool EX>

@@ -96,6 +96,7 @@ __device__ __forceinline__ void dss_finish(double* __restrict__ v, const double*
     int p = idx[o];
     if (MODE == 2 && p < 0) {
       p &= 0x7fffffff;
+      SF_CHECK(p < n_local);
       v[p] = dss_input(u, pre, p);
     } else if (p < n_local) {
       v[p] = acc;
@@ -106,6 +107,7 @@ __device__ __forceinline__ void dss_finish(double* __restrict__ v, const double*
 __device__ __forceinline__ double dss_load(const double* __restrict__ v, const double* __restrict__ recv,
                                            int p, int n_local) {
   p &= 0x7fffffff;
+  SF_CHECK(p < n_local || recv != nullptr);   // a remote copy needs the halo inbox
   return p < n_local ? v[p] : __ldg(recv + (p - n_local));
 }
 

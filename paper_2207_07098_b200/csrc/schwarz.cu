@@ -31,6 +31,7 @@ __global__ void sch_gather_kernel(const double* __restrict__ r, const long long*
                                   double* __restrict__ rw) {
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < G;
        g += (long long)gridDim.x * blockDim.x) {
+    SF_CHECK(first[g] >= 0);
     const double v = r[first[g]];
     rg[g] = v;
     rw[g] = __dmul_rn(wsqrt[g], v);
@@ -225,10 +226,12 @@ __global__ void __launch_bounds__(256) sch_coarse_cg_kernel(CoarseArgs a) {
 // Rw[p][j] = rw[sub[p][j]]: the weighted residual of every subdomain slot, rows in
 // class order (the operand of the per-class solve GEMM sol_c = Rw_c inv_c^T)
 __global__ void sch_gather_rw_kernel(const double* __restrict__ rw, const int* __restrict__ sub, long long n,
-                                     double* __restrict__ out) {
+                                     long long L, double* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
+       i += (long long)gridDim.x * blockDim.x) {
+    SF_CHECK(sub[i] >= 0 && sub[i] <= L);     // rw[L] is the zero padding slot
     out[i] = rw[sub[i]];
+  }
 }
 
 // z[g] = con ? rg : (sum_k sol[pos[k]]) * wsqrt + sum over the corners of g's
@@ -247,6 +250,7 @@ __global__ void sch_finalize_kernel(const double* __restrict__ sol, const double
     double acc = 0.0;
     for (long long k = off[g]; k < off[g + 1]; ++k) {
       const long long q = pos[k];            // own subdomains' slots, then the peers' (N > 1)
+      SF_CHECK(q >= 0 && (q < n_sol || sol_recv != nullptr));
       acc = __dadd_rn(acc, q < n_sol ? sol[q] : sol_recv[q - n_sol]);
     }
     const long long fp = first[g];
@@ -263,10 +267,12 @@ __global__ void sch_finalize_kernel(const double* __restrict__ sol, const double
 }
 
 __global__ void sch_scatter_kernel(const double* __restrict__ z, const long long* __restrict__ gid,
-                                   long long P, double* __restrict__ out) {
+                                   long long P, long long G, double* __restrict__ out) {
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P;
-       p += (long long)gridDim.x * blockDim.x)
+       p += (long long)gridDim.x * blockDim.x) {
+    SF_CHECK(gid[p] >= 0 && gid[p] < G);
     out[p] = z[gid[p]];
+  }
 }
 
 // out[v] = sum over ranks in rank order of the partial restrictions: own partial
@@ -366,7 +372,7 @@ int sf_schwarz_gather_rw_f64(const SfSchwarz* s, void* stream) {
   using namespace sf;
   if (bad(s, "sf_schwarz_gather_rw_f64")) return SF_ERR_ARG;
   const long long n = s->n_sol;
-  sch_gather_rw_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(s->rw, s->sub, n, s->rwg);
+  sch_gather_rw_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(s->rw, s->sub, n, s->L, s->rwg);
   return check_launch("schwarz gather rw");
 }
 
@@ -384,7 +390,7 @@ int sf_schwarz_finalize_f64(const SfSchwarz* s, void* stream) {
 int sf_schwarz_scatter_f64(const SfSchwarz* s, double* out, void* stream) {
   using namespace sf;
   if (bad(s, "sf_schwarz_scatter_f64") || !out) return SF_ERR_ARG;
-  sch_scatter_kernel<<<grid_for(s->P), 256, 0, as_stream(stream)>>>(s->z, s->gid, s->P, out);
+  sch_scatter_kernel<<<grid_for(s->P), 256, 0, as_stream(stream)>>>(s->z, s->gid, s->P, s->G, out);
   return check_launch("schwarz scatter");
 }
 

@@ -256,6 +256,7 @@ class _SchwarzStruct(ctypes.Structure):
         ("acc_off", ctypes.c_void_p), ("acc_pos", ctypes.c_void_p),
         ("cvert", ctypes.c_void_p), ("ccorn", ctypes.c_void_p), ("constrained", ctypes.c_void_p),
         ("z", ctypes.c_void_p), ("rflag", ctypes.c_void_p), ("se", ctypes.c_void_p),
+        ("L", ctypes.c_longlong),
     ]
 
 
@@ -786,6 +787,7 @@ class HybridSchwarz:
         st.acc_off, st.acc_pos = pt(self.acc_off), pt(self.acc_pos)
         st.cvert, st.ccorn, st.constrained, st.z = pt(self.cvert), pt(self.ccorn), pt(self.constrained), pt(self.z)
         st.rflag, st.se = pt(self.rflag), pt(self.se)
+        st.L = L
         self._st = st
         self.launches = 0
 
