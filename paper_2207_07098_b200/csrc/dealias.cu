@@ -22,9 +22,15 @@ namespace sf {
 template <int N, int M>
 struct DealiasMats {
   double D[N * N];   // GLL derivative
-  double J[M * N];   // GLL -> GL interpolation
-  double Jt[N * M];  // its transpose (projection)
+  double J[M * N];   // GLL -> GL interpolation, row p = J[p * N + i]
+  double Jt[N * M];  // its transpose (projection), row a = Jt[a * M + p]
 };
+
+// In a contraction the output index p of the matrix row varies fastest across
+// the threads of a warp for the t axis (and every few threads for s): the
+// matrix is read column-major there, mat_cm[i * R + p], so a warp's lanes hit
+// consecutive addresses instead of one row stride apart (6-way bank conflicts
+// at R = 12, N = 8).
 
 // smem layout (doubles): cf 3 m^3 | fine m^3 | tf m^3 | t1 max(m n n, n m m) |
 // t2 max(m m n, n n m) | u n^3 | g 3 n^3
@@ -50,42 +56,43 @@ __device__ __forceinline__ void contract_r(const double* __restrict__ mat, const
   }
 }
 template <int R, int I0, int I1, int I2, bool EX>
-__device__ __forceinline__ void contract_s(const double* __restrict__ mat, const double* __restrict__ in,
+__device__ __forceinline__ void contract_s(const double* __restrict__ mat_cm, const double* __restrict__ in,
                                            double* __restrict__ out) {
-  // out[i, p, k] = sum_j mat[p, j] in[i, j, k]
+  // out[i, p, k] = sum_j mat[p, j] in[i, j, k]   (mat column-major: mat_cm[j * R + p])
   for (int x = threadIdx.x; x < I0 * R * I2; x += blockDim.x) {
     const int i = x / (R * I2), rem = x - i * (R * I2), p = rem / I2, k = rem - p * I2;
     double s = 0.0;
 #pragma unroll
-    for (int j = 0; j < I1; ++j) s = mac<EX>(s, mat[p * I1 + j], in[(i * I1 + j) * I2 + k]);
+    for (int j = 0; j < I1; ++j) s = mac<EX>(s, mat_cm[j * R + p], in[(i * I1 + j) * I2 + k]);
     out[x] = s;
   }
 }
 template <int R, int I0, int I1, int I2, bool EX>
-__device__ __forceinline__ void contract_t(const double* __restrict__ mat, const double* __restrict__ in,
+__device__ __forceinline__ void contract_t(const double* __restrict__ mat_cm, const double* __restrict__ in,
                                            double* __restrict__ out) {
-  // out[i, j, p] = sum_k mat[p, k] in[i, j, k]
+  // out[i, j, p] = sum_k mat[p, k] in[i, j, k]   (mat column-major: mat_cm[k * R + p])
   for (int x = threadIdx.x; x < I0 * I1 * R; x += blockDim.x) {
     const int ij = x / R, p = x - ij * R;
     double s = 0.0;
 #pragma unroll
-    for (int k = 0; k < I2; ++k) s = mac<EX>(s, mat[p * I2 + k], in[ij * I2 + k]);
+    for (int k = 0; k < I2; ++k) s = mac<EX>(s, mat_cm[k * R + p], in[ij * I2 + k]);
     out[x] = s;
   }
 }
 
 template <int N, int M, bool EX>
-__device__ __forceinline__ void to_fine(const double* J, const double* in, double* t1, double* t2, double* out) {
+__device__ __forceinline__ void to_fine(const double* J, const double* Jcm, const double* in, double* t1,
+                                        double* t2, double* out) {
   contract_r<M, N, N, N, EX>(J, in, t1);
   __syncthreads();
-  contract_s<M, M, N, N, EX>(J, t1, t2);
+  contract_s<M, M, N, N, EX>(Jcm, t1, t2);
   __syncthreads();
-  contract_t<M, M, M, N, EX>(J, t2, out);
+  contract_t<M, M, M, N, EX>(Jcm, t2, out);
   __syncthreads();
 }
 
 template <int N, int M, bool EX>
-__global__ void __launch_bounds__(256) dealias_advect_kernel(DealiasMats<N, M> mats, const double* __restrict__ c,
+__global__ void __launch_bounds__(512) dealias_advect_kernel(DealiasMats<N, M> mats, const double* __restrict__ c,
                                                              const double* __restrict__ v,
                                                              const double* __restrict__ rx,
                                                              const double* __restrict__ wjf,
@@ -115,7 +122,7 @@ __global__ void __launch_bounds__(256) dealias_advect_kernel(DealiasMats<N, M> m
   for (int l = 0; l < 3; ++l) {
     for (int x = threadIdx.x; x < NNN; x += blockDim.x) u[x] = __ldg(c + l * PT + base + x);
     __syncthreads();
-    to_fine<N, M, EX>(mt.J, u, t1, t2, cf + l * MMM);
+    to_fine<N, M, EX>(mt.J, mt.Jt, u, t1, t2, cf + l * MMM);
   }
   for (int f = 0; f < 3; ++f) {
     for (int x = threadIdx.x; x < NNN; x += blockDim.x) u[x] = __ldg(v + f * PT + base + x);
@@ -141,7 +148,7 @@ __global__ void __launch_bounds__(256) dealias_advect_kernel(DealiasMats<N, M> m
     __syncthreads();
     // fine = cf0 * gf0; fine += cf1 * gf1; fine += cf2 * gf2 (operators.py:150-152)
     for (int l = 0; l < 3; ++l) {
-      to_fine<N, M, EX>(mt.J, g + l * NNN, t1, t2, tf);
+      to_fine<N, M, EX>(mt.J, mt.Jt, g + l * NNN, t1, t2, tf);
       for (int x = threadIdx.x; x < MMM; x += blockDim.x) {
         const double pr = mul<EX>(cf[l * MMM + x], tf[x]);
         fine[x] = (l == 0) ? pr : add<EX>(fine[x], pr);
@@ -153,13 +160,13 @@ __global__ void __launch_bounds__(256) dealias_advect_kernel(DealiasMats<N, M> m
     __syncthreads();
     contract_r<N, M, M, M, EX>(mt.Jt, fine, t1);
     __syncthreads();
-    contract_s<N, N, M, M, EX>(mt.Jt, t1, t2);
+    contract_s<N, N, M, M, EX>(mt.J, t1, t2);      // Jt column-major is J row-major
     __syncthreads();
     for (int x = threadIdx.x; x < NNN; x += blockDim.x) {
       const int ij = x / N, p = x - ij * N;
       double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < M; ++k) s = mac<EX>(s, mt.Jt[p * M + k], t2[ij * M + k]);
+      for (int k = 0; k < M; ++k) s = mac<EX>(s, mt.J[k * N + p], t2[ij * M + k]);
       out[f * PT + base + x] = sign * (s / __ldg(bm + base + x));   // sign is +-1: exact
     }
     __syncthreads();
@@ -186,9 +193,9 @@ static int launch_dealias(const double* D, const double* J, const double* c, con
   }
   if (E <= 0) return SF_OK;
   if (exact)
-    dealias_advect_kernel<N, M, true><<<(unsigned)E, 256, smem, st>>>(m, c, v, rx, wjf, bm, E, sign, out);
+    dealias_advect_kernel<N, M, true><<<(unsigned)E, 512, smem, st>>>(m, c, v, rx, wjf, bm, E, sign, out);
   else
-    dealias_advect_kernel<N, M, false><<<(unsigned)E, 256, smem, st>>>(m, c, v, rx, wjf, bm, E, sign, out);
+    dealias_advect_kernel<N, M, false><<<(unsigned)E, 512, smem, st>>>(m, c, v, rx, wjf, bm, E, sign, out);
   return check_launch("dealias_advect");
 }
 
