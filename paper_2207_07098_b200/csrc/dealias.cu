@@ -11,10 +11,19 @@
 // interpolations, the fine-grid product, the weighting and the projection, all in
 // shared memory.  HBM sees c, v, rx, wjac_f, bm once and out once.
 //
-// Every contraction is one thread's sequential sum over the contracted index in
-// ascending order, starting from 0.0 -- the numba lane's loop (kernels/_numba.py
-// apply_r/s/t) -- and the products / sums between stages are those of the
-// reference expression, so EX=true is bit-identical to the reference chain.
+// Every contraction output is one thread's sequential sum over the contracted
+// index in ascending order, starting from 0.0 -- the numba lane's loop
+// (kernels/_numba.py apply_r/s/t) -- and the products / sums between stages are
+// those of the reference expression, so EX=true is bit-identical to the chain.
+//
+// Register blocking: a thread loads one input line (the n or m values along the
+// contracted axis) into registers and produces every output of that line; the
+// matrices sit in the kernel's parameter (constant) bank and are indexed with
+// compile-time constants, so each FMA reads one register and one constant -- no
+// shared-memory traffic for the matrices and one shared load per 8-12 FMAs
+// (the one-output-per-thread form was shared-memory bound at ~12 % of the FP64
+// pipe).  Inputs of the t-axis contractions are stored with an odd line stride
+// (n+1, m+1) so the lanes of a warp read distinct banks.
 #include "common.cuh"
 
 namespace sf {
@@ -22,99 +31,110 @@ namespace sf {
 template <int N, int M>
 struct DealiasMats {
   double D[N * N];   // GLL derivative
-  double J[M * N];   // GLL -> GL interpolation, row p = J[p * N + i]
-  double Jt[N * M];  // its transpose (projection), row a = Jt[a * M + p]
+  double J[M * N];   // GLL -> GL interpolation, J[p * N + i]
 };
 
-// In a contraction the output index p of the matrix row varies fastest across
-// the threads of a warp for the t axis (and every few threads for s): the
-// matrix is read column-major there, mat_cm[i * R + p], so a warp's lanes hit
-// consecutive addresses instead of one row stride apart (6-way bank conflicts
-// at R = 12, N = 8).
-
-// smem layout (doubles): cf 3 m^3 | fine m^3 | tf m^3 | t1 max(m n n, n m m) |
-// t2 max(m m n, n n m) | u n^3 | g 3 n^3
+// Every shared buffer keeps its contiguous lines at an odd pitch (n+1 or m+1
+// doubles) so the lanes of a warp, which walk lines, hit distinct banks.
+// smem layout (doubles): cf 3 m m (m+1) | fine | tf | t1 max(m n (n+1), n m (m+1)) |
+// t2 max(m m (n+1), n n (m+1)) | u n^3 | g 3 n^3
 template <int N, int M>
 __host__ __device__ constexpr int dealias_smem_doubles() {
-  constexpr int MN = (M * N * N > N * M * M) ? M * N * N : N * M * M;
-  constexpr int MM = (M * M * N > N * N * M) ? M * M * N : N * N * M;
-  return 5 * M * M * M + MN + MM + 4 * N * N * N;
+  constexpr int FP = M * M * (M + 1);
+  constexpr int T1 = (M * N * (N + 1) > N * M * (M + 1)) ? M * N * (N + 1) : N * M * (M + 1);
+  constexpr int T2 = (M * M * (N + 1) > N * N * (M + 1)) ? M * M * (N + 1) : N * N * (M + 1);
+  return 5 * FP + T1 + T2 + 4 * N * N * N;
 }
 
-// out (A, B, C) with A = rows of mat applied on axis `axis` of in (I0, I1, I2):
-// three specialisations written out so every loop bound is a constant
-template <int R, int I0, int I1, int I2, bool EX>
-__device__ __forceinline__ void contract_r(const double* __restrict__ mat, const double* __restrict__ in,
-                                           double* __restrict__ out) {
-  // out[p, j, k] = sum_i mat[p, i] in[i, j, k]
-  for (int x = threadIdx.x; x < R * I1 * I2; x += blockDim.x) {
-    const int p = x / (I1 * I2), jk = x - p * (I1 * I2);
+// One register-blocked contraction line: a[0..I) (the values along the
+// contracted axis) -> outputs o in [O0, O0 + OC) of rows of the row-major matrix
+// mat (R x I) or, with TR, of its transpose (mat I x R read as mat[i * R + o]);
+// every matrix index is a compile-time constant (parameter bank).
+template <int I, int O0, int OC, int R, bool TR, bool EX>
+__device__ __forceinline__ void line(const double* mat, const double (&a)[I], double* out, int ostride) {
+#pragma unroll
+  for (int o = O0; o < O0 + OC; ++o) {
     double s = 0.0;
 #pragma unroll
-    for (int i = 0; i < I0; ++i) s = mac<EX>(s, mat[p * I0 + i], in[i * I1 * I2 + jk]);
-    out[x] = s;
+    for (int i = 0; i < I; ++i) s = mac<EX>(s, TR ? mat[i * R + o] : mat[o * I + i], a[i]);
+    out[o * ostride] = s;
   }
 }
-template <int R, int I0, int I1, int I2, bool EX>
-__device__ __forceinline__ void contract_s(const double* __restrict__ mat_cm, const double* __restrict__ in,
-                                           double* __restrict__ out) {
-  // out[i, p, k] = sum_j mat[p, j] in[i, j, k]   (mat column-major: mat_cm[j * R + p])
-  for (int x = threadIdx.x; x < I0 * R * I2; x += blockDim.x) {
-    const int i = x / (R * I2), rem = x - i * (R * I2), p = rem / I2, k = rem - p * I2;
-    double s = 0.0;
+
+// A contraction phase: LINES input lines x 2 output halves.  The half is the slow
+// index of the thread id (warp-uniform except at one boundary warp), so both
+// halves run with compile-time matrix indices.
+template <int I, int R, bool TR, bool EX, int LINES, class Load, class Out>
+__device__ __forceinline__ void phase(const double* mat, Load load, Out outp) {
+  constexpr int H = R / 2;
+  for (int x = threadIdx.x; x < 2 * LINES; x += blockDim.x) {
+    const int half = x / LINES, ln = x - half * LINES;
+    double a[I];
 #pragma unroll
-    for (int j = 0; j < I1; ++j) s = mac<EX>(s, mat_cm[j * R + p], in[(i * I1 + j) * I2 + k]);
-    out[x] = s;
+    for (int i = 0; i < I; ++i) a[i] = load(ln, i);
+    int stride;
+    double* o = outp(ln, stride);
+    if (half == 0)
+      line<I, 0, H, R, TR, EX>(mat, a, o, stride);
+    else
+      line<I, H, R - H, R, TR, EX>(mat, a, o, stride);
   }
 }
-template <int R, int I0, int I1, int I2, bool EX>
-__device__ __forceinline__ void contract_t(const double* __restrict__ mat_cm, const double* __restrict__ in,
-                                           double* __restrict__ out) {
-  // out[i, j, p] = sum_k mat[p, k] in[i, j, k]   (mat column-major: mat_cm[k * R + p])
-  for (int x = threadIdx.x; x < I0 * I1 * R; x += blockDim.x) {
-    const int ij = x / R, p = x - ij * R;
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < I2; ++k) s = mac<EX>(s, mat_cm[k * R + p], in[ij * I2 + k]);
-    out[x] = s;
-  }
+
+// GLL (N^3) -> GL (M^3): apply_t(J, apply_s(J, apply_r(J, in))); out lines pitch M+1
+template <int N, int M, bool EX>
+__device__ __forceinline__ void to_fine(const DealiasMats<N, M>& m, const double* __restrict__ in,
+                                        double* __restrict__ t1, double* __restrict__ t2,
+                                        double* __restrict__ out) {
+  // r: t1[p][j][k] = sum_i J[p][i] in[i][j][k]; line (j, k); t1 lines pitch N+1
+  phase<N, M, false, EX, N * N>(
+      m.J, [&](int ln, int i) { return in[i * N * N + ln]; },
+      [&](int ln, int& st) {
+        st = N * (N + 1);
+        const int j = ln / N, k = ln - j * N;
+        return t1 + j * (N + 1) + k;
+      });
+  __syncthreads();
+  // s: t2[p][q][k] = sum_j J[q][j] t1[p][j][k]; line (p, k); t2 lines pitch N+1
+  phase<N, M, false, EX, M * N>(
+      m.J, [&](int ln, int j) { const int p = ln / N, k = ln - p * N; return t1[(p * N + j) * (N + 1) + k]; },
+      [&](int ln, int& st) {
+        st = N + 1;
+        const int p = ln / N, k = ln - p * N;
+        return t2 + p * M * (N + 1) + k;
+      });
+  __syncthreads();
+  // t: out[p][q][r] = sum_k J[r][k] t2[p][q][k]; line (p, q)
+  phase<N, M, false, EX, M * M>(
+      m.J, [&](int ln, int k) { return t2[ln * (N + 1) + k]; },
+      [&](int ln, int& st) {
+        st = 1;
+        return out + ln * (M + 1);
+      });
+  __syncthreads();
 }
 
 template <int N, int M, bool EX>
-__device__ __forceinline__ void to_fine(const double* J, const double* Jcm, const double* in, double* t1,
-                                        double* t2, double* out) {
-  contract_r<M, N, N, N, EX>(J, in, t1);
-  __syncthreads();
-  contract_s<M, M, N, N, EX>(Jcm, t1, t2);
-  __syncthreads();
-  contract_t<M, M, M, N, EX>(Jcm, t2, out);
-  __syncthreads();
-}
-
-template <int N, int M, bool EX>
-__global__ void __launch_bounds__(512) dealias_advect_kernel(DealiasMats<N, M> mats, const double* __restrict__ c,
+__global__ void __launch_bounds__(256, 2) dealias_advect_kernel(const __grid_constant__ DealiasMats<N, M> mats,
+                                                             const double* __restrict__ c,
                                                              const double* __restrict__ v,
                                                              const double* __restrict__ rx,
                                                              const double* __restrict__ wjf,
-                                                             const double* __restrict__ bm, long long E, double sign,
-                                                             double* __restrict__ out) {
+                                                             const double* __restrict__ bm, long long E,
+                                                             double sign, double* __restrict__ out) {
   constexpr int NNN = N * N * N, MMM = M * M * M;
-  constexpr int MN = (M * N * N > N * M * M) ? M * N * N : N * M * M;
-  constexpr int MM = (M * M * N > N * N * M) ? M * M * N : N * N * M;
+  constexpr int FP = M * M * (M + 1);   // a fine field, lines at pitch M+1
+  constexpr int T1 = (M * N * (N + 1) > N * M * (M + 1)) ? M * N * (N + 1) : N * M * (M + 1);
+  constexpr int T2 = (M * M * (N + 1) > N * N * (M + 1)) ? M * M * (N + 1) : N * N * (M + 1);
   extern __shared__ double sm[];
-  double* cf = sm;                 // 3 MMM
-  double* fine = cf + 3 * MMM;     // MMM
-  double* tf = fine + MMM;         // MMM
-  double* t1 = tf + MMM;           // MN
-  double* t2 = t1 + MN;            // MM
-  double* u = t2 + MM;             // NNN
+  double* cf = sm;                 // 3 FP
+  double* fine = cf + 3 * FP;      // FP
+  double* tf = fine + FP;          // FP
+  double* t1 = tf + FP;            // T1
+  double* t2 = t1 + T1;            // T2
+  double* u = t2 + T2;             // NNN
   double* g = u + NNN;             // 3 NNN
-  __shared__ DealiasMats<N, M> mt;
-  for (int x = threadIdx.x; x < N * N; x += blockDim.x) mt.D[x] = mats.D[x];
-  for (int x = threadIdx.x; x < M * N; x += blockDim.x) {
-    mt.J[x] = mats.J[x];
-    mt.Jt[x] = mats.Jt[x];
-  }
+  const DealiasMats<N, M>& m = mats;
   const long long e = blockIdx.x;
   const long long PT = E * NNN;
   const long long base = e * NNN;
@@ -122,7 +142,7 @@ __global__ void __launch_bounds__(512) dealias_advect_kernel(DealiasMats<N, M> m
   for (int l = 0; l < 3; ++l) {
     for (int x = threadIdx.x; x < NNN; x += blockDim.x) u[x] = __ldg(c + l * PT + base + x);
     __syncthreads();
-    to_fine<N, M, EX>(mt.J, mt.Jt, u, t1, t2, cf + l * MMM);
+    to_fine<N, M, EX>(m, u, t1, t2, cf + l * FP);
   }
   for (int f = 0; f < 3; ++f) {
     for (int x = threadIdx.x; x < NNN; x += blockDim.x) u[x] = __ldg(v + f * PT + base + x);
@@ -133,9 +153,9 @@ __global__ void __launch_bounds__(512) dealias_advect_kernel(DealiasMats<N, M> m
       double ar = 0.0, as = 0.0, at = 0.0;
 #pragma unroll
       for (int q = 0; q < N; ++q) {
-        ar = mac<EX>(ar, mt.D[i * N + q], u[(q * N + j) * N + k]);
-        as = mac<EX>(as, mt.D[j * N + q], u[(i * N + q) * N + k]);
-        at = mac<EX>(at, mt.D[k * N + q], u[(i * N + j) * N + q]);
+        ar = mac<EX>(ar, m.D[i * N + q], u[(q * N + j) * N + k]);
+        as = mac<EX>(as, m.D[j * N + q], u[(i * N + q) * N + k]);
+        at = mac<EX>(at, m.D[k * N + q], u[(i * N + j) * N + q]);
       }
 #pragma unroll
       for (int l = 0; l < 3; ++l) {
@@ -148,27 +168,48 @@ __global__ void __launch_bounds__(512) dealias_advect_kernel(DealiasMats<N, M> m
     __syncthreads();
     // fine = cf0 * gf0; fine += cf1 * gf1; fine += cf2 * gf2 (operators.py:150-152)
     for (int l = 0; l < 3; ++l) {
-      to_fine<N, M, EX>(mt.J, mt.Jt, g + l * NNN, t1, t2, tf);
+      to_fine<N, M, EX>(m, g + l * NNN, t1, t2, tf);
       for (int x = threadIdx.x; x < MMM; x += blockDim.x) {
-        const double pr = mul<EX>(cf[l * MMM + x], tf[x]);
-        fine[x] = (l == 0) ? pr : add<EX>(fine[x], pr);
+        const int y = (x / M) * (M + 1) + x % M;
+        const double pr = mul<EX>(cf[l * FP + y], tf[y]);
+        fine[y] = (l == 0) ? pr : add<EX>(fine[y], pr);
       }
       __syncthreads();
     }
-    // weak = project_back(wjac_f * fine) / bm (operators.py:153-154)
-    for (int x = threadIdx.x; x < MMM; x += blockDim.x) fine[x] = mul<EX>(__ldg(wjf + e * MMM + x), fine[x]);
-    __syncthreads();
-    contract_r<N, M, M, M, EX>(mt.Jt, fine, t1);
-    __syncthreads();
-    contract_s<N, N, M, M, EX>(mt.J, t1, t2);      // Jt column-major is J row-major
-    __syncthreads();
-    for (int x = threadIdx.x; x < NNN; x += blockDim.x) {
-      const int ij = x / N, p = x - ij * N;
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < M; ++k) s = mac<EX>(s, mt.J[k * N + p], t2[ij * M + k]);
-      out[f * PT + base + x] = sign * (s / __ldg(bm + base + x));   // sign is +-1: exact
+    // weak = project_back(wjac_f * fine) / bm (operators.py:153-154); J^T[a][p] = J[p][a]
+    for (int x = threadIdx.x; x < MMM; x += blockDim.x) {
+      const int y = (x / M) * (M + 1) + x % M;
+      fine[y] = mul<EX>(__ldg(wjf + e * MMM + x), fine[y]);
     }
+    __syncthreads();
+    // r: t1[a][q][r] = sum_p J[p][a] fine[p][q][r]; line (q, r); t1 lines pitch M+1
+    phase<M, N, true, EX, M * M>(
+        m.J, [&](int ln, int p) { const int q = ln / M, r = ln - q * M; return fine[(p * M + q) * (M + 1) + r]; },
+        [&](int ln, int& st) {
+          st = M * (M + 1);
+          const int q = ln / M, r = ln - q * M;
+          return t1 + q * (M + 1) + r;
+        });
+    __syncthreads();
+    // s: t2[a][b][r] = sum_q J[q][b] t1[a][q][r]; line (a, r); t2 lines pitch M+1
+    phase<M, N, true, EX, N * M>(
+        m.J, [&](int ln, int q) { const int a0 = ln / M, r = ln - a0 * M; return t1[(a0 * M + q) * (M + 1) + r]; },
+        [&](int ln, int& st) {
+          st = M + 1;
+          const int a0 = ln / M, r = ln - a0 * M;
+          return t2 + a0 * N * (M + 1) + r;
+        });
+    __syncthreads();
+    // t: w[a][b][c] = sum_r J[r][c] t2[a][b][r] into u (n^3), then / bm, * sign
+    phase<M, N, true, EX, N * N>(
+        m.J, [&](int ln, int r) { return t2[ln * (M + 1) + r]; },
+        [&](int ln, int& st) {
+          st = 1;
+          return u + ln * N;
+        });
+    __syncthreads();
+    for (int x = threadIdx.x; x < NNN; x += blockDim.x)
+      out[f * PT + base + x] = sign * (u[x] / __ldg(bm + base + x));   // sign is +-1: exact
     __syncthreads();
   }
 }
@@ -179,11 +220,7 @@ static int launch_dealias(const double* D, const double* J, const double* c, con
                           cudaStream_t st) {
   DealiasMats<N, M> m;
   for (int i = 0; i < N * N; ++i) m.D[i] = D[i];
-  for (int p = 0; p < M; ++p)
-    for (int i = 0; i < N; ++i) {
-      m.J[p * N + i] = J[p * N + i];
-      m.Jt[i * M + p] = J[p * N + i];
-    }
+  for (int i = 0; i < M * N; ++i) m.J[i] = J[i];
   const size_t smem = (size_t)dealias_smem_doubles<N, M>() * sizeof(double);
   static bool attr = false;
   if (!attr) {
@@ -193,9 +230,9 @@ static int launch_dealias(const double* D, const double* J, const double* c, con
   }
   if (E <= 0) return SF_OK;
   if (exact)
-    dealias_advect_kernel<N, M, true><<<(unsigned)E, 512, smem, st>>>(m, c, v, rx, wjf, bm, E, sign, out);
+    dealias_advect_kernel<N, M, true><<<(unsigned)E, 256, smem, st>>>(m, c, v, rx, wjf, bm, E, sign, out);
   else
-    dealias_advect_kernel<N, M, false><<<(unsigned)E, 512, smem, st>>>(m, c, v, rx, wjf, bm, E, sign, out);
+    dealias_advect_kernel<N, M, false><<<(unsigned)E, 256, smem, st>>>(m, c, v, rx, wjf, bm, E, sign, out);
   return check_launch("dealias_advect");
 }
 

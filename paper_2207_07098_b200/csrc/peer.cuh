@@ -69,7 +69,8 @@ __device__ __forceinline__ bool peer_allreduce_warp(const PeerCtx& c, double min
 #pragma unroll
     for (int j = 0; j < PEER_KMAX; ++j)
       if (j < k) dst[j] = v[j];
-    __threadfence_system();
+    // the values were written by this lane: its st.release.sys orders them before
+    // the flag for every acquirer (no separate fence.sys, ~1-2 us per reduction)
     st_release_sys(reinterpret_cast<unsigned long long*>(dst + PEER_KMAX), seq);
   }
   // 2. lane r waits (acquire) for rank r's slot in my mailbox and reads it
