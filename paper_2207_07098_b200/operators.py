@@ -57,6 +57,12 @@ class GlobalOp:
     Callable like the reference closure.  ``mask`` must be a 0/1 field (as built
     by BoundarySet); it is stored as per-element bitmasks, and the masked copies
     of shared gids are flagged in a private copy of the shared perm.
+
+    Whether the operator is masked is decided over all ranks (collective on a
+    multi-rank space): a rank whose slab holds no masked point still runs the
+    masked kernel, so every rank -- and a single-GPU run -- computes each element
+    with the same kernel variant (the masked and unmasked variants may round
+    differently in the last bit: FMA contraction is the compiler's per variant).
     """
 
     def __init__(self, space, lam_visc, lam_mass, mask=None):
@@ -71,7 +77,7 @@ class GlobalOp:
             if not bool(((m == 0.0) | (m == 1.0)).all()):
                 raise ValueError("make_global_op: mask must contain only 0.0 and 1.0")
             keep = m != 0.0
-            if not bool(keep.all()):
+            if space.comm.any(not bool(keep.all())):
                 self.masked = True
                 self.inmask = pack_bits(keep)
                 self.outsel = pack_bits(keep) | gs.shared_bits
