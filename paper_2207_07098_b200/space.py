@@ -368,16 +368,60 @@ class GatherScatter:
         return w.read(0)[0]
 
     def gather_unique(self, u):
-        if self.perm is None:
-            raise NotImplementedError("gather_unique on a partitioned space")
-        return u.reshape(-1)[self.perm[self.offsets[:-1]]]
+        """One value per global id, the value of its first copy in global local-
+        index order (space.py:62-64): shape (n_gid,).  On a partitioned space a
+        collective -- every rank contributes the gids whose first copy it holds
+        (lowest local index of the gid on the lowest rank that has one) and every
+        rank gets the whole vector, bit for bit."""
+        if self.perm is not None:
+            return u.reshape(-1)[self.perm[self.offsets[:-1]]]
+        from .partition import all_gather_cat
+
+        own = self._first_copies()
+        g = self.gid.long()[own]
+        v = u.reshape(-1)[own].to(torch.float64)
+        comm = self.comm
+        n = torch.tensor([own.numel()], dtype=torch.int64, device=self.device)
+        counts = all_gather_cat(comm, n).cpu().tolist()
+        m = max(counts)
+        pad_g = torch.zeros(m, dtype=torch.int64, device=self.device)
+        pad_v = torch.zeros(m, dtype=torch.float64, device=self.device)
+        pad_g[:g.numel()] = g
+        pad_v[:v.numel()] = v
+        all_g = all_gather_cat(comm, pad_g).view(comm.world, m)
+        all_v = all_gather_cat(comm, pad_v).view(comm.world, m)
+        out = torch.empty(self.n_gid, dtype=torch.float64, device=self.device)
+        for q, c in enumerate(counts):
+            out[all_g[q, :c]] = all_v[q, :c]
+        return out
+
+    def _first_copies(self):
+        """Local indices that are the first copy of their gid (partitioned space)."""
+        own = getattr(self, "_own_first", None)
+        if own is not None:
+            return own
+        g = self.gid.long()
+        idx = torch.arange(g.numel(), device=self.device)
+        first = torch.full((self.n_gid,), g.numel(), dtype=torch.int64, device=self.device)
+        first.scatter_reduce_(0, g, idx, reduce="amin", include_self=True)
+        keep = first[g] == idx
+        # a gid shared with a lower rank has its first copy there (ranks hold
+        # ascending element ranges); the halo plan sends every local copy of such gids
+        r = self.comm.rank
+        for q, sidx in self.plan.send_idx.items():
+            if q < r:
+                keep[sidx.long()] = False
+        self._own_first = idx[keep]
+        return self._own_first
 
     def scatter_unique(self, vals, shape):
+        """Spread per-global-id values (n_gid,) to every local copy (space.py:66-70)."""
+        vals = torch.as_tensor(vals, dtype=torch.float64, device=self.device)
         if self.perm is None:
-            raise NotImplementedError("scatter_unique on a partitioned space")
+            return vals[self.gid.long()].view(shape)
         counts = self.offsets[1:] - self.offsets[:-1]
         out = torch.empty(int(np.prod(shape)), dtype=torch.float64, device=self.device)
-        out[self.perm] = torch.repeat_interleave(vals.to(torch.float64), counts)
+        out[self.perm] = torch.repeat_interleave(vals, counts)
         return out.view(shape)
 
 

@@ -2,7 +2,8 @@
 build, on CPU over gloo: every rank builds only its element range's numbering
 and halo plan, and must get exactly what the global build gives it
 (dist.build_halo_plan over the reference-order global maps) -- gid slice,
-multiplicities, shared maps, send lists and receive counts -- on a perturbed
+multiplicities, shared maps, send lists and receive counts, and the
+gather_unique / scatter_unique helpers -- on a perturbed
 box (2, 3, 4 and 8 ranks) and on the curved cylinder mini-rotor mesh (2, 3, 4).
 """
 
@@ -58,6 +59,19 @@ def _worker(rank, world, port, payload, q):
             "send": all(torch.equal(plan.send_idx[p], ref.send_idx[p]) for p in ref.send_idx)
             and set(plan.send_idx) == set(ref.send_idx),
         }
+        # gather_unique / scatter_unique on the partitioned space (space.py:62-70):
+        # the reference's first-copy values, every rank the whole vector, bitwise
+        from paper_2207_07098_b200.space import GatherScatter
+
+        gsp = GatherScatter(g_loc, None, None, (e1 - e0, n, n, n), comm=comm, starts=starts, plan=plan,
+                            mult8=mult8, n_gid=n_gid)
+        u_full = torch.randn(E * nnn, generator=torch.Generator().manual_seed(7), dtype=torch.float64)
+        u_full[::5] = -0.0
+        want = u_full[perm[off[:-1]]]
+        got = gsp.gather_unique(u_full[e0 * nnn:e1 * nnn].view(e1 - e0, n, n, n))
+        ok["gather_unique"] = bool(torch.equal(got.view(torch.int64), want.view(torch.int64)))
+        ok["scatter_unique"] = bool(torch.equal(gsp.scatter_unique(want, (e1 - e0, n, n, n)).reshape(-1),
+                                                want[gid[e0 * nnn:e1 * nnn]]))
         q.put((rank, ok))
     finally:
         dist.destroy_process_group()
