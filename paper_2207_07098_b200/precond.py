@@ -456,6 +456,7 @@ class HybridSchwarz:
 
         def node_of(g, unused):
             """global gid -> node index (``unused`` where it is not a node)."""
+            g = g.contiguous()
             p1 = torch.searchsorted(loc_nodes, g).clamp(max=Lloc - 1)
             out = torch.where(loc_nodes[p1] == g, loc_rank[p1], torch.full_like(g, unused))
             if rem.numel():
