@@ -534,8 +534,15 @@ def bench_tgv(args, world, rank, dev):
     #          the caller's velocity field is copied in from pinned host memory and
     #          the new velocity is read back (the reference's Stepper works on host
     #          arrays); the rest of the FlowState stays resident on the device.
+    #          The read-back of step k's velocity and the upload of step k+1's
+    #          input (the caller hands the result back) run chunk by chunk on the
+    #          two copy directions at once; step 0's input is uploaded whole.
     vel_h = state.vel.cpu().pin_memory()
     out_h = torch.empty_like(vel_h).pin_memory()
+    s_d2h, s_h2d = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    n_chunk = 16
+    nel = vel_h.numel()
+    cuts = [nel * c // n_chunk for c in range(n_chunk + 1)]
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     clk = ClockSampler(torch.cuda.current_device())
@@ -558,14 +565,25 @@ def bench_tgv(args, world, rank, dev):
     p_its, v_its, cfls = [], [], []
     allocs0 = torch.cuda.memory_stats().get("num_device_alloc", 0)
     t0 = time.perf_counter()
+    v = vel_h.to(dev, non_blocking=True)
     for k in range(args.steps):
-        v = vel_h.to(dev, non_blocking=True)
         state = FlowState(state.time, state.nsteps, [v] + state.vel_hist[1:], state.curl_hist,
                           state.nl_hist, state.prs, state.primed)
         evs[k][0].record(stream)
         state, d = st.step(state)
         evs[k][1].record(stream)
-        out_h.copy_(state.vel, non_blocking=True)
+        # result -> caller (D2H), caller's next input -> device (H2D), pipelined
+        v = torch.empty_like(state.vel) if k + 1 < args.steps else None
+        src, hb = state.vel.view(-1), out_h.view(-1)
+        s_d2h.wait_event(evs[k][1])
+        for c in range(n_chunk):
+            lo, hi = cuts[c], cuts[c + 1]
+            with torch.cuda.stream(s_d2h):
+                hb[lo:hi].copy_(src[lo:hi], non_blocking=True)
+            if v is not None:
+                s_h2d.wait_stream(s_d2h)
+                with torch.cuda.stream(s_h2d):
+                    v.view(-1)[lo:hi].copy_(hb[lo:hi], non_blocking=True)
         torch.cuda.synchronize()
         vel_h, out_h = out_h, vel_h      # the result is the caller's next input (no host copy)
         p_its.append(d.p_iterations)
