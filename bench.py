@@ -585,6 +585,7 @@ def bench_tgv(args, world, rank, dev):
                 with torch.cuda.stream(s_h2d):
                     v.view(-1)[lo:hi].copy_(hb[lo:hi], non_blocking=True)
         torch.cuda.synchronize()
+        del src                          # the result buffer leaves with the state it belongs to
         vel_h, out_h = out_h, vel_h      # the result is the caller's next input (no host copy)
         p_its.append(d.p_iterations)
         v_its.append(list(d.v_iterations))
