@@ -18,11 +18,39 @@ by one tiny kernel (deterministic for a given GPU count); CFL uses MAX.
 """
 
 import os
+import sys
+import time
 
 import numpy as np
 import torch
 
 from . import _lib
+
+#: seconds a failing rank keeps its process (and so its IPC-mapped mailboxes and
+#: halo inboxes) alive after an uncaught exception -- well past the 5 s poll
+#: timeout of the peer kernels (csrc/peer.cuh), so a peer that is, or soon starts,
+#: spinning on this rank's flags times out and returns (every later peer call
+#: then returns at once) instead of polling unmapped memory after this exit
+ABORT_GRACE_S = float(os.environ.get("SEMFLOW_B200_ABORT_GRACE_S", "12"))
+
+
+def _abort_grace_hook(prev, grace=None):
+    def hook(tp, val, tb):
+        prev(tp, val, tb)
+        try:
+            sys.stderr.flush()
+            time.sleep(ABORT_GRACE_S if grace is None else grace)
+        except BaseException:
+            pass
+    hook.semflow_grace = True
+    return hook
+
+
+def install_abort_grace():
+    """On an uncaught exception, report it, then keep the process alive for
+    ABORT_GRACE_S before it exits (installed once peer memory is mapped)."""
+    if not getattr(sys.excepthook, "semflow_grace", False):
+        sys.excepthook = _abort_grace_hook(sys.excepthook)
 
 
 class Comm:
@@ -43,6 +71,7 @@ class Comm:
         if (self.world > 1 and torch.cuda.is_available() and dist.get_backend(group) == "nccl"
                 and os.environ.get("SEMFLOW_B200_PEER", "1") != "0"):
             self.peer = _PeerReducer(self)
+            install_abort_grace()
 
     def close(self):
         if self.peer is not None:

@@ -154,3 +154,19 @@ def test_interior_run():
     assert interior_run([3, 50], E) == (4, 50)                       # even bounds
     assert interior_run(list(range(E)), E) is None
     assert interior_run([0, 2], 3) is None
+
+
+def test_abort_grace_hook_reports_then_waits():
+    """A rank that dies with peer memory mapped keeps its process alive past the
+    peer kernels' poll timeout (dist.ABORT_GRACE_S) after reporting the error."""
+    import time
+
+    from paper_2207_07098_b200 import dist as sfdist
+
+    seen = []
+    hook = sfdist._abort_grace_hook(lambda tp, val, tb: seen.append((tp, time.perf_counter())), grace=0.2)
+    t0 = time.perf_counter()
+    hook(RuntimeError, RuntimeError("x"), None)
+    assert seen and seen[0][0] is RuntimeError and seen[0][1] - t0 < 0.1
+    assert time.perf_counter() - t0 >= 0.2
+    assert sfdist.ABORT_GRACE_S > 5.0          # the peer poll timeout (csrc/peer.cuh)
