@@ -1,6 +1,9 @@
 """The checked build (libsemflow_b200_checked.so, device bounds checks; the pool
 closes compute-sanitizer): it loads and exports the same ABI, runs the hot path
-clean, and traps on a corrupted index instead of reading out of bounds."""
+clean, and traps on a corrupted index instead of reading out of bounds.  The
+trap test faults the GPU on purpose (a device trap is reported as Xid 13 on the
+host), so it runs only when SEMFLOW_B200_TRAP_TEST=1 (its recorded run:
+profiles/r2_checked_build_gpu_suite.log)."""
 
 import os
 import subprocess
@@ -62,6 +65,8 @@ def test_checked_build_runs_clean():
 
 
 @pytest.mark.gpu
+@pytest.mark.skipif(os.environ.get("SEMFLOW_B200_TRAP_TEST", "0") != "1",
+                    reason="deliberately faults the GPU (device trap, Xid 13): opt-in with SEMFLOW_B200_TRAP_TEST=1")
 def test_checked_build_traps_bad_index():
     res = _run(True)
     assert res.returncode != 0
